@@ -1,0 +1,217 @@
+/*
+ * spde2d_b200.h — C ABI of the B200 hot path (the drop-in boundary).
+ *
+ * Plain pointers and sizes, POD structs, int return codes; no C++ or torch
+ * types cross this boundary.  Each entry point replaces one reference
+ * routine (file:line under /root/reference/proj):
+ *
+ *   s2b_operator_create      <- CommutatorSet consumption by MagnusLogBuilder
+ *                               (include/spde2d/magnus.hpp:61-86, src/magnus.cpp:88-139)
+ *   s2b_fields_create        <- CoefficientFields consumption by euler_step_into
+ *                               (include/spde2d/operators.hpp:15-25, src/euler.cpp:28-86)
+ *   s2b_paths_create_host    <- BrownianBatch (include/spde2d/stochastics.hpp:32-43)
+ *   s2b_paths_create_philox  <- simulate_brownian (src/stochastics.cpp:76-101), counter-based
+ *   s2b_solve_magnus         <- solve_iterated_magnus (include/spde2d/magnus.hpp:93-97,
+ *                               src/magnus.cpp:239-304) incl. expmv_into (sparse.cpp:427-503)
+ *   s2b_solve_euler          <- solve_euler (include/spde2d/euler.hpp:46-49, src/euler.cpp:95-182)
+ *   s2b_exact_reference      <- exact_reference (include/spde2d/exact_langevin.hpp:44-46)
+ *   s2b_errors               <- mean_rel_error / mean_abs_error / avg_mean_abs_error
+ *                               (include/spde2d/analysis.hpp:35-50, src/analysis.cpp:53-130)
+ *   s2b_exact_errors         <- exact_reference + the three norms, fused (no reference
+ *                               ensemble is materialised), plus moment sums for the
+ *                               cross-GPU allreduce
+ *   s2b_expmv                <- expmv_into on a general CSR matrix (sparse.hpp:149-151)
+ *
+ * Error codes mirror the reference's exception classes (errors.hpp:10-19):
+ * S2B_ERR_CONFIG <-> ConfigError, S2B_ERR_DIMENSION <-> DimensionError,
+ * S2B_ERR_RUNTIME <-> std::runtime_error; numerical failure inside the solvers
+ * is never an error — it is the per-path BlownUp status, as in the reference.
+ * All calls are stream-ordered on the context's stream and synchronous at
+ * return unless stated otherwise.  One context per GPU.
+ */
+#ifndef SPDE2D_B200_H
+#define SPDE2D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S2B_OK 0
+#define S2B_ERR_CONFIG 1
+#define S2B_ERR_DIMENSION 2
+#define S2B_ERR_EXPMV 3
+#define S2B_ERR_RUNTIME 4
+#define S2B_ERR_CUDA 5
+
+typedef struct s2b_context s2b_context;
+typedef struct s2b_operator s2b_operator;
+typedef struct s2b_fields s2b_fields;
+typedef struct s2b_paths s2b_paths;
+typedef struct s2b_ensemble s2b_ensemble;
+typedef struct s2b_magnus_session s2b_magnus_session;
+
+/* GridSpec (grid.hpp:28-40): interior nodes a + (i+1)(b-a)/(n+1). */
+typedef struct {
+    double ax, bx;
+    size_t nx;
+    double av, bv;
+    size_t nv;
+} s2b_grid;
+
+/* One spde2d::SparseMatrix in its CSR storage (sparse.hpp:36-73).  rows == 0 marks
+ * an absent matrix (e.g. A2/BA/BAA/BAB of a lower-order CommutatorSet). */
+typedef struct {
+    size_t rows;
+    const size_t *row_ptr;  /* rows + 1 */
+    const int32_t *col_idx; /* row_ptr[rows] */
+    const double *values;   /* row_ptr[rows] */
+} s2b_csr;
+
+/* MagnusConfig (magnus.hpp:19-28) + the horizon T. */
+typedef struct {
+    int order;
+    double dt;
+    double T;
+    double expmv_tol;
+    double expmv_theta;
+    double blowup_norm_cap;
+    const double *record_times; /* may be NULL when n_record == 0 (terminal only) */
+    size_t n_record;
+} s2b_magnus_config;
+
+/* EulerConfig (euler.hpp:12-16) + the horizon T. */
+typedef struct {
+    double dt;
+    double T;
+    const double *record_times;
+    size_t n_record;
+} s2b_euler_config;
+
+/* Result of the norms (RelError + MeanAbsError summary, analysis.hpp:28-50). */
+typedef struct {
+    double err;       /* mean relative Frobenius error; +inf if any app path blew up */
+    size_t blowups;   /* app paths blown up (mean_rel_error) */
+    double ame;       /* avg_mean_abs_error of the ME matrix */
+    size_t excluded;  /* app paths excluded from ME */
+    double sum_rel;   /* sum over non-blown paths of ||ref-app||_F/||ref||_F (ascending m) */
+    size_t used;      /* non-blown app paths */
+    size_t region_lo; /* central region [lo, hi] */
+    size_t region_hi;
+} s2b_error_stats;
+
+/* Per-run counters of the Magnus pass engine. */
+typedef struct {
+    int64_t passes;        /* stencil passes launched (one Taylor term of every live path) */
+    int64_t path_terms;    /* sum over paths of Taylor terms applied (= S*K summed) */
+    int64_t path_windows;  /* windows completed */
+    int64_t term_launches; /* launches of the dominant term kernel */
+    double term_kernel_ms; /* summed CUDA-event time of those launches (if timing enabled) */
+    double gridpoints;     /* nx*nv */
+} s2b_magnus_stats;
+
+const char *s2b_last_error(void);
+const char *s2b_version(void);
+
+/* ---- context ---------------------------------------------------------------- */
+int s2b_context_create(int device, s2b_context **out);
+int s2b_context_destroy(s2b_context *ctx);
+int s2b_context_synchronize(s2b_context *ctx);
+/* The cudaStream_t (as void*) all work of this context is ordered on. */
+void *s2b_context_stream(s2b_context *ctx);
+/* Number of kernels launched by this context so far. */
+int64_t s2b_context_launches(s2b_context *ctx);
+
+/* ---- operators ----------------------------------------------------------------
+ * sources: B, A, A2, BA, BAA, BAB (the CommutatorSet slot order of magnus.cpp:42-52).
+ * The CSR values are re-laid out as 2-D stencil weights, bit for bit. */
+int s2b_operator_create(s2b_context *ctx, const s2b_grid *grid, int order,
+                        const s2b_csr sources[6], s2b_operator **out);
+/* Host-kept builder (operators.cpp semantics, our C++): family 0 langevin-constant,
+ * 1 langevin-variable, 2 explicit fields (fields9: h fx fv gxx gxv gvv sig sigx sigv,
+ * NULL = identically zero).  Builds the CSR CommutatorSet on the host and uploads it. */
+int s2b_operator_build(s2b_context *ctx, const s2b_grid *grid, int family, double a,
+                       double sigma, const double *const *fields9, int order,
+                       s2b_operator **out);
+/* info: [0] union stencil points, [1] compressed (x-invariant) layout flag,
+ *       [2] radius x, [3] radius v, [4] source-offset pairs, [5] order */
+int s2b_operator_info(const s2b_operator *op, int64_t info[6]);
+int s2b_operator_destroy(s2b_operator *op);
+
+/* Euler coefficient fields; fields9 entries NULL = identically zero. */
+int s2b_fields_create(s2b_context *ctx, const s2b_grid *grid, const double *const *fields9,
+                      s2b_fields **out);
+int s2b_fields_build(s2b_context *ctx, const s2b_grid *grid, int family, double a, double sigma,
+                     s2b_fields **out);
+int s2b_fields_destroy(s2b_fields *f);
+
+/* Gaussian datum phi = exp(-(x^2+v^2)/2) at interior nodes, host-computed (n doubles). */
+int s2b_gaussian_datum(const s2b_grid *grid, double *out);
+
+/* ---- Brownian paths ------------------------------------------------------------
+ * Host mode: prefix values [M][steps+1] exactly as BrownianBatch::values (parity mode).
+ * Philox mode: N(0, dt_leb) increments from Philox4x32-10 keyed by (seed, path_offset+m)
+ * with the Lebesgue step as counter, prefix-summed sequentially per path on the GPU. */
+int s2b_paths_create_host(s2b_context *ctx, double dt_leb, size_t steps, size_t M,
+                          uint64_t seed, const double *values, s2b_paths **out);
+int s2b_paths_create_philox(s2b_context *ctx, double dt_leb, size_t steps, size_t M,
+                            uint64_t seed, uint64_t path_offset, s2b_paths **out);
+int s2b_paths_download(const s2b_paths *p, double *values_out);
+int s2b_paths_destroy(s2b_paths *p);
+
+/* ---- solvers -----------------------------------------------------------------
+ * Results stay on the device in an ensemble (one record per record time, last = T). */
+int s2b_solve_magnus(s2b_context *ctx, const s2b_operator *op, const s2b_magnus_config *cfg,
+                     const double *phi, const s2b_paths *paths, s2b_ensemble **out,
+                     s2b_magnus_stats *stats);
+int s2b_solve_euler(s2b_context *ctx, const s2b_fields *f, const s2b_euler_config *cfg,
+                    const double *phi, const s2b_paths *paths, s2b_ensemble **out);
+
+/* Resident Magnus session: state stays in HBM, windows are advanced on demand. */
+int s2b_magnus_session_create(s2b_context *ctx, const s2b_operator *op,
+                              const s2b_magnus_config *cfg, const double *phi,
+                              const s2b_paths *paths, s2b_magnus_session **out);
+/* Advance every live path by up to n_windows windows (stops at T). */
+int s2b_magnus_session_advance(s2b_magnus_session *s, size_t n_windows);
+/* Reset every path to phi at window 0 (reuses all buffers). */
+int s2b_magnus_session_reset(s2b_magnus_session *s);
+int s2b_magnus_session_stats(const s2b_magnus_session *s, s2b_magnus_stats *stats);
+/* Enable CUDA-event timing of every term-kernel launch (accumulated in the stats). */
+int s2b_magnus_session_set_timing(s2b_magnus_session *s, int enable);
+/* Snapshot of the current state (all paths) as a single-record ensemble at the current time. */
+int s2b_magnus_session_ensemble(s2b_magnus_session *s, s2b_ensemble **out);
+/* Finish: the ensemble of record times (valid once every path reached T). */
+int s2b_magnus_session_finish(s2b_magnus_session *s, s2b_ensemble **out);
+int s2b_magnus_session_destroy(s2b_magnus_session *s);
+
+/* ---- ensembles -------------------------------------------------------------- */
+/* info: [0] records, [1] M, [2] n, [3] nx, [4] nv */
+int s2b_ensemble_info(const s2b_ensemble *e, int64_t info[5], double *times);
+int s2b_ensemble_download(const s2b_ensemble *e, size_t record, double *states, uint8_t *status);
+/* Per-path Taylor-term and window counters of a Magnus ensemble (NULL-able outputs). */
+int s2b_ensemble_counters(const s2b_ensemble *e, int64_t *terms, int64_t *windows);
+int s2b_ensemble_destroy(s2b_ensemble *e);
+
+/* ---- exact solution + norms -------------------------------------------------- */
+int s2b_exact_reference(s2b_context *ctx, const s2b_grid *grid, double t, double a,
+                        double sigma, const s2b_paths *paths, s2b_ensemble **out);
+int s2b_errors(s2b_context *ctx, const s2b_ensemble *ref, size_t ref_record,
+               const s2b_ensemble *app, size_t app_record, int kappa, s2b_error_stats *out,
+               double *me_out);
+/* Fused: exact field at the record's time (a, sigma; path functionals over [0, t]) vs app.
+ * per_path_rel (M, NULL-able): ||ref-app||_F/||ref||_F (NaN for blown paths).
+ * moments (2n, NULL-able): sum_m u_m and sum_m u_m^2 over non-blown paths. */
+int s2b_exact_errors(s2b_context *ctx, const s2b_ensemble *app, size_t app_record, double a,
+                     double sigma, const s2b_paths *paths, int kappa, s2b_error_stats *out,
+                     double *me_out, double *per_path_rel, double *moments);
+
+/* ---- general expmv ------------------------------------------------------------ */
+int s2b_expmv(s2b_context *ctx, const s2b_csr *m, const double *x, double tol, double theta,
+              double *y, int report[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

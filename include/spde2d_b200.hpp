@@ -1,0 +1,316 @@
+// spde2d_b200.hpp — the C++ host API of the B200 solver.
+//
+// Same names, argument meaning and error behaviour as the reference library's
+// public headers (/root/reference/proj/include/spde2d/*.hpp), so a caller of
+// the reference (experiment.cpp, the CLI, the tests) compiles against this
+// header unchanged.  The host-kept pieces (grid, CSR operator builder,
+// coefficient sampling, commutators, the xoshiro Brownian batch) are
+// re-implemented here in C++ with the reference's exact arithmetic order, so
+// the operators they produce are bitwise the reference's.  The solvers and
+// reductions on the hot path (solve_iterated_magnus, solve_euler,
+// exact_reference, mean_rel_error, mean_abs_error, expmv) run on the GPU
+// through the C ABI in spde2d_b200.h — there is no CPU fallback.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <functional>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace spde2d {
+
+// ---- errors (reference errors.hpp:10-19, sparse.hpp:132-142) -----------------
+struct ConfigError : std::runtime_error {
+    explicit ConfigError(const std::string& w) : std::runtime_error(w) {}
+};
+struct DimensionError : std::runtime_error {
+    explicit DimensionError(const std::string& w) : std::runtime_error(w) {}
+};
+
+// ---- grid (reference grid.hpp:15-74) ------------------------------------------
+struct Grid1D {
+    double a = 0.0, b = 0.0;
+    std::size_t n = 0;
+    double delta = 0.0;
+    double node(std::size_t i) const { return a + static_cast<double>(i + 1) * delta; }
+};
+Grid1D build_grid(double a, double b, std::size_t n);
+
+struct GridSpec {
+    Grid1D x, v;
+    std::size_t dim() const { return x.n * v.n; }
+    std::optional<std::size_t> d() const {
+        return x.n == v.n ? std::optional<std::size_t>(x.n) : std::nullopt;
+    }
+};
+
+// Column-major nx-by-nv samples: entry (i, j) at j*nx + i.
+class Field {
+public:
+    Field() = default;
+    Field(std::size_t nx, std::size_t nv, double fill = 0.0) : nx_(nx), nv_(nv), v_(nx * nv, fill) {}
+    std::size_t nx() const { return nx_; }
+    std::size_t nv() const { return nv_; }
+    std::size_t size() const { return v_.size(); }
+    double& operator()(std::size_t i, std::size_t j) { return v_[j * nx_ + i]; }
+    double operator()(std::size_t i, std::size_t j) const { return v_[j * nx_ + i]; }
+    std::span<double> data() { return v_; }
+    std::span<const double> data() const { return v_; }
+    bool all_zero() const;
+
+private:
+    std::size_t nx_ = 0, nv_ = 0;
+    std::vector<double> v_;
+};
+std::vector<double> vectorize(const Field& f);
+Field devectorize(std::span<const double> vec, std::size_t nx, std::size_t nv);
+
+// ---- CSR sparse matrices (reference sparse.hpp:12-104) ------------------------
+struct Triplet {
+    std::size_t row = 0, col = 0;
+    double value = 0.0;
+};
+
+struct SparseView {
+    std::size_t rows = 0, cols = 0;
+    std::span<const std::size_t> row_ptr;
+    std::span<const std::int32_t> col_idx;
+    std::span<const double> values;
+    std::size_t nnz() const { return values.size(); }
+};
+
+class SparseMatrix {
+public:
+    SparseMatrix() = default;
+    SparseMatrix(std::size_t rows, std::size_t cols, std::vector<std::size_t> row_ptr,
+                 std::vector<std::int32_t> col_idx, std::vector<double> values);
+    static SparseMatrix from_triplets(std::size_t rows, std::size_t cols, std::vector<Triplet> t);
+    static SparseMatrix identity(std::size_t n);
+    static SparseMatrix zero(std::size_t rows, std::size_t cols);
+
+    std::size_t rows() const { return rows_; }
+    std::size_t cols() const { return cols_; }
+    std::size_t nnz() const { return val_.size(); }
+    std::size_t nonzero_diagonals() const;
+    std::span<const std::size_t> row_ptr() const { return rp_; }
+    std::span<const std::int32_t> col_idx() const { return ci_; }
+    std::span<const double> values() const { return val_; }
+    SparseView view() const { return SparseView{rows_, cols_, rp_, ci_, val_}; }
+
+private:
+    std::size_t rows_ = 0, cols_ = 0;
+    std::vector<std::size_t> rp_{0};
+    std::vector<std::int32_t> ci_;
+    std::vector<double> val_;
+};
+
+SparseMatrix tridiag(std::size_t n, double lo, double mid, double hi, double scale);
+SparseMatrix kron(const SparseMatrix& a, const SparseMatrix& b);
+SparseMatrix diag_of(std::span<const double> v);
+SparseMatrix spmm(const SparseMatrix& a, const SparseMatrix& b);
+void spmv(const SparseView& a, std::span<const double> x, std::span<double> y);
+std::vector<double> spmv(const SparseMatrix& a, std::span<const double> x);
+SparseMatrix commutator(const SparseMatrix& a, const SparseMatrix& b);
+double one_norm(const SparseView& m);
+inline double one_norm(const SparseMatrix& m) { return one_norm(m.view()); }
+SparseMatrix sparse_scale(const SparseMatrix& a, double s);
+SparseMatrix sparse_add(const SparseMatrix& a, const SparseMatrix& b);
+SparseMatrix sparse_sub(const SparseMatrix& a, const SparseMatrix& b);
+
+enum class ExpmvStatus { Ok, Overflow, ToleranceNotReached };
+struct ExpmvReport {
+    ExpmvStatus status = ExpmvStatus::Ok;
+    double residual = 0.0;
+    int segments = 0;
+    int max_terms = 0;
+};
+class ExpmvError : public std::runtime_error {
+public:
+    ExpmvError(ExpmvStatus s, double r, const std::string& w)
+        : std::runtime_error(w), status_(s), residual_(r) {}
+    ExpmvStatus status() const { return status_; }
+    double residual() const { return residual_; }
+
+private:
+    ExpmvStatus status_;
+    double residual_;
+};
+// exp(M) x on the GPU (the segmented-Taylor rule of the reference sparse.hpp:144-155).
+std::vector<double> expmv(const SparseMatrix& m, std::span<const double> v, double tol,
+                          double theta = 1.0);
+
+// ---- operators (reference operators.hpp:15-88) --------------------------------
+struct CoefficientFields {
+    Field h, fx, fv, gxx, gxv, gvv;
+    Field sig, sigx, sigv;
+    bool zero_h = true, zero_fx = true, zero_fv = true;
+    bool zero_gxx = true, zero_gxv = true, zero_gvv = true;
+    bool zero_sig = true, zero_sigx = true, zero_sigv = true;
+    void refresh_zero_flags();
+};
+
+enum class FamilyTag { LangevinConstant, LangevinVariable, Custom };
+
+struct CoefficientEvaluators {
+    using Fn = std::function<double(double, double)>;
+    Fn h, fx, fv, gxx, gxv, gvv, sig, sigx, sigv;
+};
+
+class CoefficientFamily {
+public:
+    static CoefficientFamily langevin_constant(double a, double sigma);
+    static CoefficientFamily langevin_variable(double a, double sigma);
+    static CoefficientFamily custom(CoefficientEvaluators evals);
+    FamilyTag tag() const { return tag_; }
+    double a() const { return a_; }
+    double sigma() const { return sigma_; }
+    const CoefficientEvaluators& evaluators() const { return ev_; }
+
+private:
+    CoefficientFamily(FamilyTag t, double a, double s, CoefficientEvaluators e)
+        : tag_(t), a_(a), sigma_(s), ev_(std::move(e)) {}
+    FamilyTag tag_;
+    double a_ = 0.0, sigma_ = 0.0;
+    CoefficientEvaluators ev_;
+};
+
+CoefficientFields sample_coefficients(const CoefficientFamily& family, const GridSpec& grid);
+SparseMatrix assemble_drift(const CoefficientFields& fields, const GridSpec& grid);
+SparseMatrix assemble_diffusion(const CoefficientFields& fields, const GridSpec& grid);
+
+struct CommutatorSet {
+    int order = 1;
+    SparseMatrix A, B;
+    SparseMatrix A2, BA;   // order >= 2
+    SparseMatrix BAA, BAB; // order 3
+};
+CommutatorSet precompute_commutators(const SparseMatrix& a, const SparseMatrix& b, int order);
+
+// ---- stochastics (reference stochastics.hpp:16-73) ----------------------------
+class NormalStream {
+public:
+    NormalStream(std::uint64_t seed, std::uint64_t trajectory);
+    double next();
+
+private:
+    std::uint64_t next_u64();
+    std::uint64_t s_[4];
+    double cached_ = 0.0;
+    bool has_cached_ = false;
+};
+
+struct BrownianBatch {
+    double T = 0.0, dt_leb = 0.0;
+    std::size_t M = 0;
+    std::uint64_t seed = 0;
+    std::size_t steps = 0;
+    std::vector<std::vector<double>> increments; // [m][k]
+    std::vector<std::vector<double>> values;     // [m][k], values[m][0] == 0
+    std::size_t index_of(double t) const;
+};
+BrownianBatch simulate_brownian(double T, double dt_leb, std::size_t M, std::uint64_t seed);
+
+struct PathSegment {
+    const std::vector<double>* path = nullptr;
+    std::size_t k0 = 0, k1 = 0;
+    double dt_leb = 0.0;
+    std::size_t steps() const { return k1 - k0; }
+    double length() const { return static_cast<double>(k1 - k0) * dt_leb; }
+    double value(std::size_t j) const { return (*path)[k0 + j] - (*path)[k0]; }
+    double terminal() const { return (*path)[k1] - (*path)[k0]; }
+};
+PathSegment window(const BrownianBatch& batch, double t0, double t1, std::size_t m);
+
+struct ItoFunctionals {
+    double h = 0.0, W = 0.0, IW = 0.0, IsW = 0.0, IW2 = 0.0;
+};
+ItoFunctionals lebesgue_functionals(const PathSegment& segment);
+
+// ---- solvers (reference magnus.hpp:13-108, euler.hpp:12-49) -------------------
+struct AdaptiveConfig {
+    bool enabled = false;
+    double tolerance = 1e-4;
+    double shrink = 0.5;
+};
+
+struct MagnusConfig {
+    int order = 3;
+    double dt = 0.1;
+    double expmv_tol = 1e-10;
+    double expmv_theta = 1.0;
+    double blowup_norm_cap = 1e10;
+    AdaptiveConfig adaptive;
+    int threads = 0; // accepted for API parity; the GPU ignores it
+    std::vector<double> record_times;
+};
+
+enum class TrajectoryStatus { Ok, BlownUp };
+
+struct SolutionEnsemble {
+    GridSpec grid;
+    double t = 0.0;
+    std::uint64_t seed = 0;
+    std::vector<std::vector<double>> states;
+    std::vector<TrajectoryStatus> status;
+    std::vector<double> seconds;
+    std::size_t trajectories() const { return status.size(); }
+    std::size_t blowup_count() const;
+};
+
+std::vector<SolutionEnsemble> solve_iterated_magnus(const MagnusConfig& cfg,
+                                                    const CommutatorSet& comms,
+                                                    std::span<const double> phi,
+                                                    const BrownianBatch& batch, double T,
+                                                    const GridSpec& grid);
+
+struct EulerConfig {
+    double dt = 1e-4;
+    int threads = 0;
+    std::vector<double> record_times;
+};
+
+std::vector<SolutionEnsemble> solve_euler(const EulerConfig& cfg, const CoefficientFields& fields,
+                                          const GridSpec& grid, const Field& phi,
+                                          const BrownianBatch& batch, double T);
+
+// ---- exact solution + norms (reference exact_langevin.hpp, analysis.hpp) -------
+struct LangevinParams {
+    double a = 1.1;
+    double sigma = 0.0;
+    double gap() const { return a - sigma * sigma; }
+};
+struct PathFunctionalsForExact {
+    double W = 0.0, IW = 0.0;
+};
+Field gaussian_datum(const GridSpec& grid);
+SolutionEnsemble exact_reference(const GridSpec& grid, double t, const LangevinParams& params,
+                                 const BrownianBatch& batch);
+
+struct CentralRegion {
+    std::size_t d = 0;
+    int kappa = 0;
+    std::size_t lo = 0, hi = 0;
+    std::size_t size() const { return hi - lo + 1; }
+};
+CentralRegion central_region(std::size_t d, int kappa);
+
+struct MeanAbsError {
+    Field me;
+    std::size_t excluded = 0;
+};
+MeanAbsError mean_abs_error(const SolutionEnsemble& ref, const SolutionEnsemble& app,
+                            const CentralRegion& region);
+double avg_mean_abs_error(const Field& me);
+
+struct RelError {
+    double err = 0.0;
+    std::size_t blowups = 0;
+};
+RelError mean_rel_error(const SolutionEnsemble& ref, const SolutionEnsemble& app,
+                        const CentralRegion& region);
+
+} // namespace spde2d

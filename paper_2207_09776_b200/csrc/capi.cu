@@ -1,0 +1,474 @@
+// The C ABI (include/spde2d_b200.h): handle lifetime, argument validation,
+// exception -> error-code translation, and the host-side plan_windows rules.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "s2b_internal.cuh"
+#include "spde2d_b200.hpp"
+
+namespace s2b {
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return S2B_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const spde2d::ConfigError& e) {
+        g_last_error = e.what();
+        return S2B_ERR_CONFIG;
+    } catch (const spde2d::DimensionError& e) {
+        g_last_error = e.what();
+        return S2B_ERR_DIMENSION;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return S2B_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return S2B_ERR_RUNTIME;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) fail(S2B_ERR_CONFIG, std::string("null argument: ") + what);
+}
+
+} // namespace
+
+void after_launch(s2b_context* ctx, const char* file, int line) {
+    ctx->launches += 1;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        fail(S2B_ERR_CUDA, std::string("kernel launch failed at ") + file + ":" + std::to_string(line) + ": " +
+                               cudaGetErrorString(e));
+}
+
+// BrownianBatch::index_of (stochastics.cpp:103-111)
+size_t index_of(double t, double dt_leb, size_t steps) {
+    const auto k = static_cast<long long>(std::llround(t / dt_leb));
+    if (k < 0 || static_cast<size_t>(k) > steps ||
+        std::abs(t - static_cast<double>(k) * dt_leb) > 1e-12 * std::max(1.0, std::abs(t)))
+        fail(S2B_ERR_CONFIG, "time " + std::to_string(t) + " is not on the Lebesgue grid");
+    return static_cast<size_t>(k);
+}
+
+// plan_windows (magnus.cpp:174-200); solve_euler uses the same rules (euler.cpp:102-122)
+WindowPlan plan_windows(double dt, double T, double dt_leb, size_t steps, const double* record_times,
+                        size_t n_record, const char* who) {
+    WindowPlan plan;
+    plan.total_steps = index_of(T, dt_leb, steps);
+    plan.dt_steps = index_of(dt, dt_leb, steps);
+    if (plan.dt_steps == 0) fail(S2B_ERR_CONFIG, std::string(who) + ": dt must be at least dt_leb");
+    if (plan.total_steps % plan.dt_steps != 0)
+        fail(S2B_ERR_CONFIG, std::string(who) + ": T must be an integer multiple of dt");
+    if (n_record == 0) {
+        plan.record_steps.push_back(plan.total_steps);
+    } else {
+        for (size_t q = 0; q < n_record; ++q) {
+            const size_t k = index_of(record_times[q], dt_leb, steps);
+            if (k == 0 || k > plan.total_steps || k % plan.dt_steps != 0)
+                fail(S2B_ERR_CONFIG, std::string(who) + ": record time " + std::to_string(record_times[q]) +
+                                         " is not a positive multiple of dt within [0, T]");
+            plan.record_steps.push_back(k);
+        }
+        std::sort(plan.record_steps.begin(), plan.record_steps.end());
+        if (plan.record_steps.back() != plan.total_steps) plan.record_steps.push_back(plan.total_steps);
+    }
+    return plan;
+}
+
+namespace {
+
+spde2d::GridSpec grid_spec(const s2b_grid* g) {
+    return spde2d::GridSpec{spde2d::build_grid(g->ax, g->bx, g->nx), spde2d::build_grid(g->av, g->bv, g->nv)};
+}
+
+spde2d::CoefficientFields host_fields(const s2b_grid* grid, int family, double a, double sigma,
+                                      const double* const* fields9) {
+    const spde2d::GridSpec g = grid_spec(grid);
+    if (family == 0) return spde2d::sample_coefficients(spde2d::CoefficientFamily::langevin_constant(a, sigma), g);
+    if (family == 1) return spde2d::sample_coefficients(spde2d::CoefficientFamily::langevin_variable(a, sigma), g);
+    if (family != 2) fail(S2B_ERR_CONFIG, "unknown coefficient family");
+    spde2d::CoefficientFields f = spde2d::sample_coefficients(spde2d::CoefficientFamily::custom({}), g);
+    spde2d::Field* all[9] = {&f.h, &f.fx, &f.fv, &f.gxx, &f.gxv, &f.gvv, &f.sig, &f.sigx, &f.sigv};
+    for (int k = 0; k < 9; ++k)
+        if (fields9 && fields9[k]) std::memcpy(all[k]->data().data(), fields9[k], g.dim() * sizeof(double));
+    f.refresh_zero_flags();
+    return f;
+}
+
+s2b_csr csr_of(const spde2d::SparseMatrix& m) {
+    s2b_csr c{};
+    c.rows = m.rows();
+    c.row_ptr = m.row_ptr().data();
+    c.col_idx = m.col_idx().data();
+    c.values = m.values().data();
+    return c;
+}
+
+} // namespace
+} // namespace s2b
+
+using namespace s2b;
+
+static MagnusSession* S(s2b_magnus_session* s) { return reinterpret_cast<MagnusSession*>(s); }
+static const MagnusSession* S(const s2b_magnus_session* s) { return reinterpret_cast<const MagnusSession*>(s); }
+
+extern "C" {
+
+const char* s2b_last_error(void) { return g_last_error.c_str(); }
+const char* s2b_version(void) { return "spde2d_b200 0.1 (sm_100a)"; }
+
+int s2b_context_create(int device, s2b_context** out) {
+    return guard([&] {
+        need(out, "out");
+        int count = 0;
+        S2B_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) fail(S2B_ERR_CONFIG, "no such CUDA device");
+        S2B_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        S2B_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) fail(S2B_ERR_CUDA, std::string("sm_100a build needs a Blackwell B200, found ") + prop.name);
+        auto* c = new s2b_context();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        S2B_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c;
+    });
+}
+
+int s2b_context_destroy(s2b_context* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int s2b_context_synchronize(s2b_context* ctx) {
+    return guard([&] {
+        need(ctx, "ctx");
+        S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+void* s2b_context_stream(s2b_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+int64_t s2b_context_launches(s2b_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int s2b_operator_create(s2b_context* ctx, const s2b_grid* grid, int order, const s2b_csr sources[6],
+                        s2b_operator** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(sources, "sources");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = make_operator(ctx, grid, order, sources);
+    });
+}
+
+int s2b_operator_build(s2b_context* ctx, const s2b_grid* grid, int family, double a, double sigma,
+                       const double* const* fields9, int order, s2b_operator** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        const spde2d::GridSpec g = grid_spec(grid);
+        const spde2d::CoefficientFields f = host_fields(grid, family, a, sigma, fields9);
+        const spde2d::CommutatorSet cs = spde2d::precompute_commutators(
+            spde2d::assemble_diffusion(f, g), spde2d::assemble_drift(f, g), order);
+        const s2b_csr src[6] = {csr_of(cs.B), csr_of(cs.A), csr_of(cs.A2), csr_of(cs.BA), csr_of(cs.BAA), csr_of(cs.BAB)};
+        *out = make_operator(ctx, grid, order, src);
+    });
+}
+
+int s2b_operator_info(const s2b_operator* op, int64_t info[6]) {
+    return guard([&] {
+        need(op, "op");
+        operator_info(op, info);
+    });
+}
+
+int s2b_operator_destroy(s2b_operator* op) {
+    return guard([&] { delete op; });
+}
+
+int s2b_fields_create(s2b_context* ctx, const s2b_grid* grid, const double* const* fields9, s2b_fields** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = make_fields(ctx, grid, fields9);
+    });
+}
+
+int s2b_fields_build(s2b_context* ctx, const s2b_grid* grid, int family, double a, double sigma, s2b_fields** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        const spde2d::CoefficientFields f = host_fields(grid, family, a, sigma, nullptr);
+        const double* f9[9] = {f.zero_h ? nullptr : f.h.data().data(),       f.zero_fx ? nullptr : f.fx.data().data(),
+                               f.zero_fv ? nullptr : f.fv.data().data(),     f.zero_gxx ? nullptr : f.gxx.data().data(),
+                               f.zero_gxv ? nullptr : f.gxv.data().data(),   f.zero_gvv ? nullptr : f.gvv.data().data(),
+                               f.zero_sig ? nullptr : f.sig.data().data(),   f.zero_sigx ? nullptr : f.sigx.data().data(),
+                               f.zero_sigv ? nullptr : f.sigv.data().data()};
+        *out = make_fields(ctx, grid, f9);
+    });
+}
+
+int s2b_fields_destroy(s2b_fields* f) {
+    return guard([&] { delete f; });
+}
+
+int s2b_gaussian_datum(const s2b_grid* grid, double* out) {
+    return guard([&] {
+        need(grid, "grid");
+        need(out, "out");
+        const spde2d::Field f = spde2d::gaussian_datum(grid_spec(grid));
+        std::memcpy(out, f.data().data(), f.size() * sizeof(double));
+    });
+}
+
+int s2b_paths_create_host(s2b_context* ctx, double dt_leb, size_t steps, size_t M, uint64_t seed,
+                          const double* values, s2b_paths** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(values, "values");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = make_paths_host(ctx, dt_leb, steps, M, seed, values);
+    });
+}
+
+int s2b_paths_create_philox(s2b_context* ctx, double dt_leb, size_t steps, size_t M, uint64_t seed,
+                            uint64_t path_offset, s2b_paths** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = make_paths_philox(ctx, dt_leb, steps, M, seed, path_offset);
+    });
+}
+
+int s2b_paths_download(const s2b_paths* p, double* values_out) {
+    return guard([&] {
+        need(p, "paths");
+        need(values_out, "values_out");
+        S2B_CUDA(cudaMemcpy(values_out, p->d_values.p, p->d_values.bytes(), cudaMemcpyDeviceToHost));
+    });
+}
+
+int s2b_paths_destroy(s2b_paths* p) {
+    return guard([&] { delete p; });
+}
+
+int s2b_solve_magnus(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfg, const double* phi,
+                     const s2b_paths* paths, s2b_ensemble** out, s2b_magnus_stats* stats) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(op, "op");
+        need(cfg, "cfg");
+        need(phi, "phi");
+        need(paths, "paths");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        MagnusSession* s = session_create(ctx, op, cfg, phi, paths);
+        try {
+            session_advance(s, static_cast<size_t>(-1) / 2);
+            if (stats) session_stats(s, stats);
+            *out = session_finish(s);
+        } catch (...) {
+            session_destroy(s);
+            throw;
+        }
+        session_destroy(s);
+    });
+}
+
+int s2b_solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler_config* cfg, const double* phi,
+                    const s2b_paths* paths, s2b_ensemble** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(f, "fields");
+        need(cfg, "cfg");
+        need(phi, "phi");
+        need(paths, "paths");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = solve_euler(ctx, f, cfg, phi, paths);
+    });
+}
+
+int s2b_magnus_session_create(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfg,
+                              const double* phi, const s2b_paths* paths, s2b_magnus_session** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(op, "op");
+        need(cfg, "cfg");
+        need(phi, "phi");
+        need(paths, "paths");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = reinterpret_cast<s2b_magnus_session*>(session_create(ctx, op, cfg, phi, paths));
+    });
+}
+
+int s2b_magnus_session_advance(s2b_magnus_session* s, size_t n_windows) {
+    return guard([&] {
+        need(s, "session");
+        session_advance(S(s), n_windows);
+    });
+}
+
+int s2b_magnus_session_reset(s2b_magnus_session* s) {
+    return guard([&] {
+        need(s, "session");
+        session_reset(S(s));
+    });
+}
+
+int s2b_magnus_session_stats(const s2b_magnus_session* s, s2b_magnus_stats* stats) {
+    return guard([&] {
+        need(s, "session");
+        need(stats, "stats");
+        session_stats(S(s), stats);
+    });
+}
+
+int s2b_magnus_session_set_timing(s2b_magnus_session* s, int enable) {
+    return guard([&] {
+        need(s, "session");
+        session_set_timing(S(s), enable != 0);
+    });
+}
+
+int s2b_magnus_session_ensemble(s2b_magnus_session* s, s2b_ensemble** out) {
+    return guard([&] {
+        need(s, "session");
+        need(out, "out");
+        *out = session_snapshot(S(s));
+    });
+}
+
+int s2b_magnus_session_finish(s2b_magnus_session* s, s2b_ensemble** out) {
+    return guard([&] {
+        need(s, "session");
+        need(out, "out");
+        *out = session_finish(S(s));
+    });
+}
+
+int s2b_magnus_session_destroy(s2b_magnus_session* s) {
+    return guard([&] { session_destroy(S(s)); });
+}
+
+int s2b_ensemble_info(const s2b_ensemble* e, int64_t info[5], double* times) {
+    return guard([&] {
+        need(e, "ensemble");
+        info[0] = static_cast<int64_t>(e->R);
+        info[1] = static_cast<int64_t>(e->M);
+        info[2] = static_cast<int64_t>(e->nx * e->nv);
+        info[3] = static_cast<int64_t>(e->nx);
+        info[4] = static_cast<int64_t>(e->nv);
+        if (times) std::copy(e->times.begin(), e->times.end(), times);
+    });
+}
+
+int s2b_ensemble_download(const s2b_ensemble* e, size_t record, double* states, uint8_t* status) {
+    return guard([&] {
+        need(e, "ensemble");
+        if (record >= e->R) fail(S2B_ERR_DIMENSION, "ensemble: record out of range");
+        S2B_CUDA(cudaSetDevice(e->ctx->device));
+        std::vector<uint8_t> st(e->M);
+        S2B_CUDA(cudaMemcpy(st.data(), e->status.p + record * e->M, e->M, cudaMemcpyDeviceToHost));
+        if (status) std::copy(st.begin(), st.end(), status);
+        if (states) {
+            const size_t n = e->nx * e->nv;
+            S2B_CUDA(cudaMemcpy(states, e->states[record].p, e->M * n * sizeof(double), cudaMemcpyDeviceToHost));
+            for (size_t m = 0; m < e->M; ++m)
+                if (st[m])
+                    for (size_t i = 0; i < n; ++i) states[m * n + i] = std::nan("");
+        }
+    });
+}
+
+int s2b_ensemble_counters(const s2b_ensemble* e, int64_t* terms, int64_t* windows) {
+    return guard([&] {
+        need(e, "ensemble");
+        if (terms) {
+            if (!e->terms.p) fail(S2B_ERR_CONFIG, "ensemble has no Magnus counters");
+            S2B_CUDA(cudaMemcpy(terms, e->terms.p, e->M * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        }
+        if (windows) {
+            if (!e->windows.p) fail(S2B_ERR_CONFIG, "ensemble has no Magnus counters");
+            S2B_CUDA(cudaMemcpy(windows, e->windows.p, e->M * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+int s2b_ensemble_destroy(s2b_ensemble* e) {
+    return guard([&] { delete e; });
+}
+
+int s2b_exact_reference(s2b_context* ctx, const s2b_grid* grid, double t, double a, double sigma,
+                        const s2b_paths* paths, s2b_ensemble** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(paths, "paths");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = exact_reference(ctx, grid, t, a, sigma, paths);
+    });
+}
+
+int s2b_errors(s2b_context* ctx, const s2b_ensemble* ref, size_t ref_record, const s2b_ensemble* app,
+               size_t app_record, int kappa, s2b_error_stats* out, double* me_out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(ref, "ref");
+        need(app, "app");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        errors(ctx, ref, ref_record, app, app_record, kappa, out, me_out);
+    });
+}
+
+int s2b_exact_errors(s2b_context* ctx, const s2b_ensemble* app, size_t app_record, double a, double sigma,
+                     const s2b_paths* paths, int kappa, s2b_error_stats* out, double* me_out,
+                     double* per_path_rel, double* moments) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(app, "app");
+        need(paths, "paths");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        exact_errors(ctx, app, app_record, a, sigma, paths, kappa, out, me_out, per_path_rel, moments);
+    });
+}
+
+int s2b_expmv(s2b_context* ctx, const s2b_csr* m, const double* x, double tol, double theta, double* y,
+              int report[4]) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "matrix");
+        need(x, "x");
+        need(y, "y");
+        need(report, "report");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        expmv_csr(ctx, m, x, tol, theta, y, report);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,198 @@
+// Euler-Maruyama on the GPU (solve_euler, src/euler.cpp:95-182).
+//
+// One launch advances every live path by one explicit step of euler_step_into
+// (src/euler.cpp:28-86).  The arithmetic is the reference's, term by term and
+// separately rounded (-fmad=false): central differences, the drift fold over the
+// non-zero fields in the order h, fx, fv, gxx, gxv, gvv with the 1/2 applied as
+// (0.5*g), the noise fold sig, sigx, sigv, then (u + drift*dt) + noise*dW.
+// Blow-up follows the reference exactly: a path is flagged when max|u+| is not
+// finite, and std::max there ignores NaN, so only an infinite |u+| flags it.
+// dW is the difference of prefix values (euler.cpp:156), so E-M and Magnus consume
+// the same paths.
+#include <algorithm>
+
+#include "s2b_internal.cuh"
+
+namespace s2b {
+
+namespace {
+
+struct EmArgs {
+    const double* f; // 9 * n (only mask fields valid)
+    int mask;
+    int nx, nv;
+    double st[5];
+    double dt;
+    const double* values;
+    size_t vstride; // steps + 1
+    size_t k0, k1;  // Lebesgue indices: dW = values[k1] - values[k0]
+    const double* in;
+    double* out;
+    int* blown;
+};
+
+template <bool GXV>
+__global__ void __launch_bounds__(256) em_step_kernel(EmArgs a) {
+    const int nx = a.nx, nv = a.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+    const int m = blockIdx.y;
+    if (a.blown[m]) return; // the reference stops a blown path (euler.cpp:159-162)
+    const double* u = a.in + static_cast<size_t>(m) * n;
+    double* o = a.out + static_cast<size_t>(m) * n;
+    const double* pv = a.values + static_cast<size_t>(m) * a.vstride;
+    const double dW = pv[a.k1] - pv[a.k0];
+    bool inf_seen = false;
+    for (size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(r % nx), j = static_cast<int>(r / nx);
+        const double uc = u[r];
+        const double uxm = i > 0 ? u[r - 1] : 0.0;
+        const double uxp = i + 1 < nx ? u[r + 1] : 0.0;
+        const double uvm = j > 0 ? u[r - nx] : 0.0;
+        const double uvp = j + 1 < nv ? u[r + nx] : 0.0;
+        const double dxu = (uxp - uxm) * a.st[0];
+        const double dvu = (uvp - uvm) * a.st[2];
+        const double* f = a.f;
+        double drift = 0.0;
+        if (a.mask & 1) drift += f[r] * uc;
+        if (a.mask & 2) drift += f[n + r] * dxu;
+        if (a.mask & 4) drift += f[2 * n + r] * dvu;
+        if (a.mask & 8) {
+            const double dxxu = (uxp - 2.0 * uc + uxm) * a.st[1];
+            drift += 0.5 * f[3 * n + r] * dxxu;
+        }
+        if (GXV) {
+            const bool up = j + 1 < nv, dn = j > 0, rt = i + 1 < nx, lf = i > 0;
+            const double upp = (up && rt) ? u[r + nx + 1] : 0.0;
+            const double upm = (up && lf) ? u[r + nx - 1] : 0.0;
+            const double ump = (dn && rt) ? u[r - nx + 1] : 0.0;
+            const double umm = (dn && lf) ? u[r - nx - 1] : 0.0;
+            const double dxvu = (upp - upm - ump + umm) * a.st[4];
+            drift += f[4 * n + r] * dxvu;
+        }
+        if (a.mask & 32) {
+            const double dvvu = (uvp - 2.0 * uc + uvm) * a.st[3];
+            drift += 0.5 * f[5 * n + r] * dvvu;
+        }
+        double noise = 0.0;
+        if (a.mask & 64) noise += f[6 * n + r] * uc;
+        if (a.mask & 128) noise += f[7 * n + r] * dxu;
+        if (a.mask & 256) noise += f[8 * n + r] * dvu;
+        const double next = uc + drift * a.dt + noise * dW;
+        o[r] = next;
+        inf_seen |= fabs(next) == __longlong_as_double(0x7FF0000000000000LL);
+    }
+    if (inf_seen) a.blown[m] = 1;
+}
+
+__global__ void em_record_status_kernel(const int* blown, uint8_t* status, size_t M) {
+    const size_t m = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (m < M) status[m] = blown[m] ? 1 : 0;
+}
+
+} // namespace
+
+s2b_fields* make_fields(s2b_context* ctx, const s2b_grid* grid, const double* const* fields9) {
+    const size_t nx = grid->nx, nv = grid->nv, n = nx * nv;
+    if (n == 0) fail(S2B_ERR_CONFIG, "fields: empty grid");
+    auto* f = new s2b_fields();
+    f->ctx = ctx;
+    f->nx = nx;
+    f->nv = nv;
+    f->grid = *grid;
+    f->d_f.alloc(9 * n);
+    S2B_CUDA(cudaMemset(f->d_f.p, 0, f->d_f.bytes()));
+    for (int k = 0; k < 9; ++k) {
+        if (!fields9 || !fields9[k]) continue;
+        bool nz = false;
+        for (size_t r = 0; r < n; ++r)
+            if (fields9[k][r] != 0.0) {
+                nz = true;
+                break;
+            }
+        if (!nz) continue; // CoefficientFields::refresh_zero_flags
+        f->mask |= 1 << k;
+        S2B_CUDA(cudaMemcpy(f->d_f.p + k * n, fields9[k], n * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    // EulerStencils::from_grid (euler.cpp:18-26)
+    const double dx = (grid->bx - grid->ax) / static_cast<double>(nx + 1);
+    const double dv = (grid->bv - grid->av) / static_cast<double>(nv + 1);
+    f->st[0] = 1.0 / (2.0 * dx);
+    f->st[1] = 1.0 / (dx * dx);
+    f->st[2] = 1.0 / (2.0 * dv);
+    f->st[3] = 1.0 / (dv * dv);
+    f->st[4] = 1.0 / (4.0 * dx * dv);
+    return f;
+}
+
+s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler_config* cfg,
+                          const double* phi, const s2b_paths* paths) {
+    const WindowPlan plan = plan_windows(cfg->dt, cfg->T, paths->dt_leb, paths->steps,
+                                         cfg->record_times, cfg->n_record, "solve_euler");
+    const size_t M = paths->M, n = f->nx * f->nv;
+    auto* e = new s2b_ensemble();
+    try {
+        e->ctx = ctx;
+        e->R = plan.record_steps.size();
+        e->M = M;
+        e->nx = f->nx;
+        e->nv = f->nv;
+        e->seed = paths->seed;
+        e->grid = f->grid;
+        for (size_t r : plan.record_steps) e->times.push_back(static_cast<double>(r) * paths->dt_leb);
+        e->status.alloc(e->R * M);
+        DevBuf<double> U[2] = {DevBuf<double>(M * n), DevBuf<double>(M * n)};
+        DevBuf<int> blown(M);
+        S2B_CUDA(cudaMemsetAsync(blown.p, 0, blown.bytes(), ctx->stream));
+        for (size_t m = 0; m < M; ++m)
+            S2B_CUDA(cudaMemcpyAsync(U[0].p + m * n, phi, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        EmArgs a{};
+        a.f = f->d_f.p;
+        a.mask = f->mask;
+        a.nx = static_cast<int>(f->nx);
+        a.nv = static_cast<int>(f->nv);
+        std::copy(f->st, f->st + 5, a.st);
+        a.dt = cfg->dt;
+        a.values = paths->d_values.p;
+        a.vstride = paths->steps + 1;
+        a.blown = blown.p;
+        const size_t nsteps = plan.total_steps / plan.dt_steps;
+        const unsigned gx = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64));
+        size_t rec = 0;
+        int cur = 0;
+        for (size_t k = 0; k < nsteps; ++k) {
+            a.k0 = k * plan.dt_steps;
+            a.k1 = (k + 1) * plan.dt_steps;
+            a.in = U[cur].p;
+            a.out = U[cur ^ 1].p;
+            dim3 grid(gx, static_cast<unsigned>(M));
+            if (f->mask & 16)
+                em_step_kernel<true><<<grid, 256, 0, ctx->stream>>>(a);
+            else
+                em_step_kernel<false><<<grid, 256, 0, ctx->stream>>>(a);
+            S2B_LAUNCHED(ctx);
+            cur ^= 1;
+            const size_t done = (k + 1) * plan.dt_steps;
+            while (rec < plan.record_steps.size() && plan.record_steps[rec] == done) {
+                if (rec + 1 == plan.record_steps.size()) {
+                    e->states.push_back(std::move(U[cur])); // last record: the final state itself
+                } else {
+                    DevBuf<double> snap(M * n);
+                    S2B_CUDA(cudaMemcpyAsync(snap.p, U[cur].p, snap.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
+                    e->states.push_back(std::move(snap));
+                }
+                em_record_status_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, ctx->stream>>>(
+                    blown.p, e->status.p + rec * M, M);
+                S2B_LAUNCHED(ctx);
+                ++rec;
+            }
+        }
+        S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        delete e;
+        throw;
+    }
+    return e;
+}
+
+} // namespace s2b

@@ -1,0 +1,1254 @@
+// Iterated stochastic Magnus on the GPU: the pass engine.
+//
+// Reference path replaced: solve_iterated_magnus (src/magnus.cpp:239-304) with
+// MagnusLogBuilder::fill (:141-160), log_coefficients (:26-40),
+// lebesgue_functionals (src/stochastics.cpp:121-141) and expmv_into
+// (src/sparse.cpp:427-503).
+//
+// B200 design:
+//  * The logarithm Y of every path-window is never materialised.  The six
+//    CommutatorSet matrices are re-laid out once as 2-D stencil weights; when
+//    they are x-invariant away from the two x-boundary columns on each side
+//    (the Langevin families) they compress to W[pair][j][class] (a few 100 KB).
+//  * All (path, window) functionals, the six scalar weights c_s and the
+//    segment counts s = ceil(||Y||_1 / theta) are computed up front, in
+//    parallel in time (functionals_kernel, norm_*_kernel).
+//  * A "pass" applies ONE Taylor term to EVERY live path: each path runs its
+//    own (window, segment, k) state machine, so paths never wait for each
+//    other and the reference's per-path stopping rule (two consecutive term
+//    inf-norms <= tol * ||accum||_inf, 55-term cap) is replicated exactly.
+//    term_tma_kernel streams the path's term/accum rows through a TMA
+//    (cp.async.bulk) shared-memory ring, keeps a (2Rv+1)-row register window
+//    per thread and rebuilds Y for its row strip from the compressed weights;
+//    per-path inf-norms are max-reduced with 64-bit atomics (order-independent,
+//    hence deterministic).  control_kernel then advances every path's state
+//    machine and compacts the live list.
+//  * Bitwise parity: all arithmetic is separately rounded (-fmad=false) in the
+//    reference's order: Y assembly in slot order from 0.0, the matvec summed
+//    in ascending stencil offset (= the DIA diagonal order of sparse.cpp:412-423)
+//    from 0.0, t = next * (1/(s*k)), accum += t.  Column sums for ||Y||_1 are
+//    accumulated in ascending row order like one_norm (sparse.cpp:263-271).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "s2b_internal.cuh"
+
+namespace s2b {
+
+namespace {
+
+constexpr int kMaxTerms = 55;   // sparse.cpp:435
+constexpr int kStripRows = 32;  // output rows per work item (compressed kernel)
+constexpr int kStages = 4;      // TMA ring depth
+
+__host__ __device__ constexpr int box_bit(int dx, int dv) { return (dv + kBoxR) * kBoxW + (dx + kBoxR); }
+
+__device__ __forceinline__ int xclass(int i, int nx) {
+    return i == 0 ? 0 : (i == 1 ? 1 : (i == nx - 2 ? 3 : (i == nx - 1 ? 4 : 2)));
+}
+
+__device__ __forceinline__ unsigned long long abs_bits(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFFFFFULL;
+}
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ULL;
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+    return a > b ? a : b;
+}
+
+__device__ __forceinline__ unsigned long long warp_umax(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ---- per (path, window) functionals and logarithm weights ---------------------------
+// lebesgue_functionals (stochastics.cpp:121-141) + log_coefficients (magnus.cpp:26-40),
+// one thread per (path, window): all windows of all paths at once.
+__global__ void functionals_kernel(const double* __restrict__ values, size_t steps, size_t M,
+                                   size_t dt_steps, size_t nwin, double dt, int order,
+                                   double* __restrict__ ctab) {
+    const size_t id = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (id >= M * nwin) return;
+    const size_t m = id / nwin, w = id % nwin;
+    const double* p = values + m * (steps + 1);
+    const size_t k0 = w * dt_steps, k1 = k0 + dt_steps;
+    const double base = p[k0];
+    double iw = 0.0, isw = 0.0, iw2 = 0.0;
+    for (size_t j = 0; j < dt_steps; ++j) {
+        const double wv = p[k0 + j] - base;
+        const double s = static_cast<double>(j) * dt;
+        iw += wv;
+        isw += s * wv;
+        iw2 += wv * wv;
+    }
+    const double h = static_cast<double>(k1 - k0) * dt;
+    const double W = p[k1] - p[k0];
+    const double IW = iw * dt, IsW = isw * dt, IW2 = iw2 * dt;
+    double c[6] = {h, W, 0.0, 0.0, 0.0, 0.0};
+    if (order >= 2) {
+        c[2] = -0.5 * h;
+        c[3] = IW - 0.5 * h * W;
+    }
+    if (order >= 3) {
+        c[4] = 0.5 * IW2 - 0.5 * W * IW + h * W * W / 12.0;
+        c[5] = IsW - 0.5 * h * IW - h * h * W / 12.0;
+    }
+    double* out = ctab + id * 6;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) out[s] = c[s];
+}
+
+// Y value of one stencil bit at one row: MagnusLogBuilder::fill's fold (magnus.cpp:147-159),
+// 0.0 start, slots in order, zero coefficients skipped.
+struct OpView {
+    const int* pair_begin; // kBoxBits + 1
+    const int* pair_slot;
+    const double* w;
+    int nx, nv;
+    int compressed;
+};
+
+__device__ __forceinline__ double y_entry(const OpView& op, const double* c, int bit, int i, int j) {
+    double y = 0.0;
+    const int q0 = op.pair_begin[bit], q1 = op.pair_begin[bit + 1];
+    for (int q = q0; q < q1; ++q) {
+        const double cs = c[op.pair_slot[q]];
+        if (cs == 0.0) continue;
+        const double wv = op.compressed
+                              ? op.w[(static_cast<size_t>(q) * op.nv + j) * kClasses + xclass(i, op.nx)]
+                              : op.w[static_cast<size_t>(q) * op.nx * op.nv + static_cast<size_t>(j) * op.nx + i];
+        y += cs * wv;
+    }
+    return y;
+}
+
+// ||Y||_1 column sum of column (i, j): rows in ascending order (descending stencil bit),
+// only rows inside the grid (one_norm, sparse.cpp:263-271).
+__device__ double column_sum(const OpView& op, const double* c, const int* bits, int nbits, int i,
+                             int j) {
+    double s = 0.0;
+    for (int e = nbits - 1; e >= 0; --e) {
+        const int b = bits[e];
+        const int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
+        const int ir = i - dx, jr = j - dv;
+        if (ir < 0 || ir >= op.nx || jr < 0 || jr >= op.nv) continue;
+        s += fabs(y_entry(op, c, b, ir, jr));
+    }
+    return s;
+}
+
+// Segment count per (path, window): s = max(1, ceil(norm/theta)), 0 marks norm == 0
+// (expmv returns its input unchanged, sparse.cpp:449).  One block per (path, window).
+// Compressed layout: only columns whose stencil rows touch a boundary class, plus one
+// interior representative, are distinct.
+__global__ void norm_kernel(OpView op, const int* __restrict__ bits, int nbits, int rx,
+                            const double* __restrict__ ctab, size_t count, double theta,
+                            int* __restrict__ stab, double* __restrict__ norms) {
+    const size_t id = blockIdx.x;
+    if (id >= count) return;
+    __shared__ double c[6];
+    __shared__ unsigned long long red[32];
+    if (threadIdx.x < 6) c[threadIdx.x] = ctab[id * 6 + threadIdx.x];
+    __syncthreads();
+    unsigned long long best = 0;
+    const int lim = rx + 2; // i <= lim or i >= nx-1-lim are the distinct columns
+    const int ncol_i = op.compressed ? min(op.nx, 2 * lim + 2) : op.nx;
+    const int total = ncol_i * op.nv;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+        const int ii = t % ncol_i, j = t / ncol_i;
+        int i = ii;
+        if (op.compressed && op.nx > 2 * lim + 2 && ii > lim) i = op.nx - (2 * lim + 2) + ii;
+        const double s = column_sum(op, c, bits, nbits, i, j);
+        best = umax64(best, abs_bits(s)); // colsums are >= 0; NaN ranks above +inf
+    }
+    best = warp_umax(best);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long v = threadIdx.x < (blockDim.x + 31) / 32 ? red[threadIdx.x] : 0ULL;
+        v = warp_umax(v);
+        if (threadIdx.x == 0) {
+            const double norm = __longlong_as_double(static_cast<long long>(v));
+            int s = 0;
+            if (norm != 0.0) {
+                const double q = ceil(norm / theta);
+                s = q > 1.0 ? (q < 2147483647.0 ? static_cast<int>(q) : INT_MAX) : 1;
+            }
+            stab[id] = s;
+            if (norms) norms[id] = norm;
+        }
+    }
+}
+
+// ---- path state machine ---------------------------------------------------------
+struct Ctl {
+    int* win;       // current window
+    int* seg;       // segment within the window
+    int* k;         // next Taylor term (1-based)
+    int* nseg;      // segments of the current window
+    int* status;    // 0 live, 1 finished/paused-at-T, 2 blown
+    int* par;       // which of the two buffers holds the current term/accum
+    int* rec_next;  // next record index
+    double* prev;   // previous term inf-norm
+    long long* terms;
+    long long* windows;
+    unsigned long long* tn; // running max |t| (bits)
+    unsigned long long* sn; // running max |accum| (bits)
+    int* act_in;
+    int* act_out;
+    int* cnt; // cnt[0] live-in, cnt[1] live-out, cnt[2] records queued
+    int4* recq; // (path, record, parity, -)
+    uint8_t* rec_status; // [R][M]
+    const int* stab;     // [M][nwin]
+    const long long* rec_steps; // [R]
+    int R;
+    int nwin;
+    int dt_steps;
+    int win_stop; // pause when reaching this window
+    double tol;
+    double cap;
+    size_t M;
+};
+
+// Enter window `w` of path p whose state is in parity `par`: skip zero-norm windows,
+// queue record snapshots at window ends, finish at win_stop.  Returns true if the path
+// has a term to run.
+__device__ bool enter_window(const Ctl& c, int p, int w, int par) {
+    while (true) {
+        if (w >= c.win_stop) {
+            c.win[p] = w;
+            c.status[p] = w >= c.nwin ? 1 : 0;
+            return false;
+        }
+        const int s = c.stab[static_cast<size_t>(p) * c.nwin + w];
+        if (s != 0) {
+            c.win[p] = w;
+            c.nseg[p] = s;
+            c.seg[p] = 0;
+            c.k[p] = 1;
+            c.prev[p] = __longlong_as_double(static_cast<long long>(kInfBits));
+            return true;
+        }
+        // norm == 0: exp(Y)u = u, the window completes immediately
+        c.windows[p] += 1;
+        const long long step = static_cast<long long>(w + 1) * c.dt_steps;
+        int r = c.rec_next[p];
+        while (r < c.R && c.rec_steps[r] == step) {
+            c.rec_status[static_cast<size_t>(r) * c.M + p] = 0;
+            if (r < c.R - 1) c.recq[atomicAdd(&c.cnt[2], 1)] = make_int4(p, r, par, 0);
+            ++r;
+        }
+        c.rec_next[p] = r;
+        ++w;
+    }
+}
+
+__global__ void init_kernel(Ctl c, int first_window) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= static_cast<int>(c.M)) return;
+    if (c.status[p] == 2) return; // blown paths stay blown
+    c.tn[p] = 0;
+    c.sn[p] = 0;
+    if (first_window == 0) {
+        c.par[p] = 0;
+        c.rec_next[p] = 0;
+        c.terms[p] = 0;
+        c.windows[p] = 0;
+    }
+    if (enter_window(c, p, first_window, c.par[p])) c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
+}
+
+// After a pass: evaluate the stopping rule of expmv_into (sparse.cpp:463-492) and the
+// window-level blow-up rule of solve_iterated_magnus (magnus.cpp:277-291) per live path.
+__global__ void control_kernel(Ctl c) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= c.cnt[0]) return;
+    const int p = c.act_in[a];
+    const unsigned long long tb = c.tn[p], sb = c.sn[p];
+    c.tn[p] = 0;
+    c.sn[p] = 0;
+    const int par = c.par[p] ^ 1; // the pass wrote the other buffer pair
+    c.par[p] = par;
+    c.terms[p] += 1;
+    if (tb >= kInfBits || sb >= kInfBits) { // non-finite term or accum: Overflow
+        c.status[p] = 2;
+        return;
+    }
+    const double tn = __longlong_as_double(static_cast<long long>(tb));
+    const double sn = __longlong_as_double(static_cast<long long>(sb));
+    const double gate = c.tol * sn;
+    const int k = c.k[p];
+    if (tn <= gate && c.prev[p] <= gate) {
+        const int seg = c.seg[p] + 1;
+        if (seg < c.nseg[p]) {
+            c.seg[p] = seg;
+            c.k[p] = 1;
+            c.prev[p] = __longlong_as_double(static_cast<long long>(kInfBits));
+        } else {
+            // window done: u = accum, max|u| == sn (magnus.cpp:282-286)
+            if (sn > c.cap) {
+                c.status[p] = 2;
+                return;
+            }
+            const int w = c.win[p];
+            c.windows[p] += 1;
+            const long long step = static_cast<long long>(w + 1) * c.dt_steps;
+            int r = c.rec_next[p];
+            while (r < c.R && c.rec_steps[r] == step) {
+                c.rec_status[static_cast<size_t>(r) * c.M + p] = 0;
+                if (r < c.R - 1) c.recq[atomicAdd(&c.cnt[2], 1)] = make_int4(p, r, par, 0);
+                ++r;
+            }
+            c.rec_next[p] = r;
+            if (!enter_window(c, p, w + 1, par)) return;
+        }
+    } else {
+        if (k >= kMaxTerms) { // ToleranceNotReached
+            c.status[p] = 2;
+            return;
+        }
+        c.prev[p] = tn;
+        c.k[p] = k + 1;
+    }
+    c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
+}
+
+// Copy queued record snapshots S[par][p] -> rec[r][p].
+__global__ void record_kernel(const int* __restrict__ cnt, const int4* __restrict__ recq,
+                              const double* __restrict__ S0, const double* __restrict__ S1,
+                              double* const* __restrict__ rec, size_t n) {
+    const int nq = cnt[2];
+    for (int q = blockIdx.y; q < nq; q += gridDim.y) {
+        const int4 e = recq[q];
+        const double* src = (e.z ? S1 : S0) + static_cast<size_t>(e.x) * n;
+        double* dst = rec[e.y] + static_cast<size_t>(e.x) * n;
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<size_t>(gridDim.x) * blockDim.x)
+            dst[i] = src[i];
+    }
+}
+
+__global__ void swap_counts_kernel(int* cnt) {
+    cnt[0] = cnt[1];
+    cnt[1] = 0;
+    cnt[2] = 0;
+}
+
+// ---- term kernels --------------------------------------------------------------
+struct TermArgs {
+    OpView op;
+    const double* ctab; // [M][nwin][6]
+    int nwin;
+    const int* act;
+    const int* cnt; // cnt[0] = live paths this pass
+    const int* win;
+    const int* k;
+    const int* nseg;
+    const int* par;
+    double* T0;
+    double* T1;
+    double* S0;
+    double* S1;
+    unsigned long long* tn;
+    unsigned long long* sn;
+    int nstrips;
+    int8_t e2bit[kBoxBits];
+};
+
+// Generic kernel: one thread per (path, point); any stencil, full or compressed weights.
+__global__ void term_generic_kernel(TermArgs a, const int* __restrict__ bits, int nbits) {
+    const int nx = a.op.nx, nv = a.op.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+    const int blocks_per_path = static_cast<int>((n + blockDim.x - 1) / blockDim.x);
+    const long long work = static_cast<long long>(a.cnt[0]) * blocks_per_path;
+    __shared__ double c[6];
+    __shared__ unsigned long long red[2][32];
+    for (long long wi = blockIdx.x; wi < work; wi += gridDim.x) {
+        const int p = a.act[wi / blocks_per_path];
+        const size_t r = (wi % blocks_per_path) * static_cast<size_t>(blockDim.x) + threadIdx.x;
+        __syncthreads();
+        if (threadIdx.x < 6) c[threadIdx.x] = a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + threadIdx.x];
+        __syncthreads();
+        const int kk = a.k[p];
+        const int par = a.par[p];
+        const double inv = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
+        const double* Sin = (par ? a.S1 : a.S0) + static_cast<size_t>(p) * n;
+        const double* in = kk == 1 ? Sin : (par ? a.T1 : a.T0) + static_cast<size_t>(p) * n;
+        double* Tout = (par ? a.T0 : a.T1) + static_cast<size_t>(p) * n;
+        double* Sout = (par ? a.S0 : a.S1) + static_cast<size_t>(p) * n;
+        unsigned long long tb = 0, sb = 0;
+        if (r < n) {
+            const int i = static_cast<int>(r % nx), j = static_cast<int>(r / nx);
+            double y = 0.0;
+            for (int e = 0; e < nbits; ++e) {
+                const int b = bits[e];
+                const int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
+                const int ii = i + dx, jj = j + dv;
+                const double x = (ii >= 0 && ii < nx && jj >= 0 && jj < nv) ? in[static_cast<size_t>(jj) * nx + ii] : 0.0;
+                y += y_entry(a.op, c, b, i, j) * x;
+            }
+            const double t = y * inv;
+            const double s = Sin[r] + t;
+            Tout[r] = t;
+            Sout[r] = s;
+            tb = abs_bits(t);
+            sb = abs_bits(s);
+        }
+        tb = warp_umax(tb);
+        sb = warp_umax(sb);
+        if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = tb;
+            red[1][threadIdx.x >> 5] = sb;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int nw = (blockDim.x + 31) / 32;
+            unsigned long long t2 = threadIdx.x < nw ? red[0][threadIdx.x] : 0ULL;
+            unsigned long long s2 = threadIdx.x < nw ? red[1][threadIdx.x] : 0ULL;
+            t2 = warp_umax(t2);
+            s2 = warp_umax(s2);
+            if (threadIdx.x == 0) {
+                if (t2) atomicMax(&a.tn[p], t2);
+                if (s2) atomicMax(&a.sn[p], s2);
+            }
+        }
+    }
+}
+
+// ---- TMA-fed compressed-stencil term kernel ----------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <uint64_t MASK>
+struct MaskInfo {
+    static constexpr int count() {
+        int n = 0;
+        for (int b = 0; b < kBoxBits; ++b) n += (MASK >> b) & 1;
+        return n;
+    }
+    static constexpr int rank(int bit) {
+        int n = 0;
+        for (int b = 0; b < bit; ++b) n += (MASK >> b) & 1;
+        return n;
+    }
+    static constexpr bool has(int dx, int dv) { return (MASK >> box_bit(dx, dv)) & 1; }
+};
+
+// One work item = (live path, strip of kStripRows output rows).  Threads own two adjacent
+// x-points (i = 2t, 2t+1); rows stream through a TMA ring (input row r and accum row
+// r - KRV per stage), each thread keeps a (2KRV+1) x (2 NP) register window.
+template <int KRX, int KRV, uint64_t MASK>
+__global__ void __launch_bounds__(512) term_tma_kernel(TermArgs a) {
+    constexpr int H = KRX <= 2 ? 2 : 4;             // zero halo (doubles) on each side
+    constexpr int AOFF = (H - KRX) & ~1;            // first loaded smem index relative to 2t
+    constexpr int LAST = 1 + KRX + H;               // last needed smem index relative to 2t
+    constexpr int NP = (LAST - AOFF) / 2 + 1;       // 16-byte pairs loaded per row
+    constexpr int WROWS = 2 * KRV + 1;
+    constexpr int NBM = MaskInfo<MASK>::count();
+    constexpr int J = kStripRows;
+
+    const int nx = a.op.nx, nv = a.op.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+    const int NT = blockDim.x;
+    const int RW = 2 * NT + 2 * H; // smem row width (doubles)
+    const int t = threadIdx.x;
+    const int i0 = 2 * t;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    double* rows = reinterpret_cast<double*>(smem_raw + 128);                // kStages x RW
+    double* srow = rows + kStages * RW;                                        // kStages x 2NT
+    double* Ys = srow + kStages * 2 * NT;                                      // J x 5 x NBM
+    __shared__ double c[6];
+    __shared__ unsigned long long red[2][16];
+
+    for (int q = t; q < kStages * RW; q += NT) rows[q] = 0.0;
+    if (t == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int clsA = xclass(i0, nx), clsB = xclass(i0 + 1, nx);
+    const bool validA = i0 < nx, validB = i0 + 1 < nx;
+    uint32_t gstep = 0; // running stage counter across work items (mbarrier phases)
+
+    const long long work = static_cast<long long>(a.cnt[0]) * a.nstrips;
+    for (long long wi = blockIdx.x; wi < work; wi += gridDim.x) {
+        const int p = a.act[wi / a.nstrips];
+        const int strip = static_cast<int>(wi % a.nstrips);
+        const int j0 = strip * J;
+        const int jend = min(j0 + J, nv);
+        const int kk = a.k[p];
+        const int par = a.par[p];
+        const double inv = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
+        const double* Sin = (par ? a.S1 : a.S0) + static_cast<size_t>(p) * n;
+        const double* in = kk == 1 ? Sin : (par ? a.T1 : a.T0) + static_cast<size_t>(p) * n;
+        double* Tout = (par ? a.T0 : a.T1) + static_cast<size_t>(p) * n;
+        double* Sout = (par ? a.S0 : a.S1) + static_cast<size_t>(p) * n;
+        const int nsteps = (jend - j0) + 2 * KRV;
+
+        // producer: stage s carries input row j0-KRV+s and accum row j0-2KRV+s
+        auto issue = [&](int s) {
+            const uint32_t g = gstep + s;
+            const int slot = g % kStages;
+            const int r = j0 - KRV + s;
+            const int ro = r - KRV;
+            uint32_t bytes = 0;
+            const bool has_in = r >= 0 && r < nv;
+            const bool has_s = s >= 2 * KRV && ro < jend;
+            if (has_in) bytes += nx * 8;
+            if (has_s) bytes += nx * 8;
+            if (bytes) {
+                mbar_expect_tx(&full[slot], bytes);
+                if (has_in) tma_row(rows + slot * RW + H, in + static_cast<size_t>(r) * nx, nx * 8, &full[slot]);
+                if (has_s) tma_row(srow + slot * 2 * NT, Sin + static_cast<size_t>(ro) * nx, nx * 8, &full[slot]);
+            } else {
+                mbar_arrive(&full[slot]);
+            }
+        };
+
+        __syncthreads(); // previous item fully consumed the ring and Ys
+        if (t == 0) {
+            for (int s = 0; s < kStages - 1 && s < nsteps; ++s) issue(s);
+        }
+        if (t < 6) c[t] = a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + t];
+        __syncthreads();
+        // rebuild Y for this strip: Ys[jj][cls][e] (fill fold, slot order, from 0.0)
+        for (int q = t; q < (jend - j0) * kClasses * NBM; q += NT) {
+            const int e = q % NBM;
+            const int cls = (q / NBM) % kClasses;
+            const int jj = q / (NBM * kClasses);
+            const int b = a.e2bit[e];
+            const int j = j0 + jj;
+            double y = 0.0;
+            const int q0 = a.op.pair_begin[b], q1 = a.op.pair_begin[b + 1];
+            for (int pq = q0; pq < q1; ++pq) {
+                const double cs = c[a.op.pair_slot[pq]];
+                if (cs == 0.0) continue;
+                y += cs * a.op.w[(static_cast<size_t>(pq) * nv + j) * kClasses + cls];
+            }
+            Ys[q] = y;
+        }
+        __syncthreads();
+
+        double win[WROWS][2 * NP];
+#pragma unroll
+        for (int r = 0; r < WROWS; ++r)
+#pragma unroll
+            for (int q = 0; q < 2 * NP; ++q) win[r][q] = 0.0;
+        unsigned long long tb = 0, sb = 0;
+
+        // steps are unrolled by WROWS so the register ring index is static
+        for (int base = 0; base < nsteps; base += WROWS) {
+#pragma unroll
+            for (int ph = 0; ph < WROWS; ++ph) {
+                const int s = base + ph;
+                if (s < nsteps) {
+                    if (t == 0 && s + kStages - 1 < nsteps) issue(s + kStages - 1);
+                    const uint32_t g = gstep + s;
+                    const int slot = g % kStages;
+                    mbar_wait(&full[slot], (g / kStages) & 1);
+                    const int r = j0 - KRV + s;
+                    // new input row into register row (s mod WROWS) == ph (base is a multiple)
+                    if (r >= 0 && r < nv) {
+                        const double2* src = reinterpret_cast<const double2*>(rows + slot * RW + i0 + AOFF);
+#pragma unroll
+                        for (int q = 0; q < NP; ++q) {
+                            const double2 v2 = src[q];
+                            win[ph][2 * q] = v2.x;
+                            win[ph][2 * q + 1] = v2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 2 * NP; ++q) win[ph][q] = 0.0;
+                    }
+                    const int jo = r - KRV; // output row
+                    if (s >= 2 * KRV && jo < jend) {
+                        const double2 sv = reinterpret_cast<const double2*>(srow + slot * 2 * NT)[t];
+                        const double* yA = Ys + ((jo - j0) * kClasses + clsA) * NBM;
+                        const double* yB = Ys + ((jo - j0) * kClasses + clsB) * NBM;
+                        double accA = 0.0, accB = 0.0;
+                        // ascending stencil offset == ascending DIA diagonal (sparse.cpp:412-423)
+#pragma unroll
+                        for (int dv = -KRV; dv <= KRV; ++dv) {
+                            // register row holding input row jo+dv: (s - KRV + dv) mod WROWS
+                            const int rr = ((ph - KRV + dv) % WROWS + WROWS) % WROWS;
+#pragma unroll
+                            for (int dx = -KRX; dx <= KRX; ++dx) {
+                                if (MaskInfo<MASK>::has(dx, dv)) {
+                                    const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
+                                    const int col = H + dx - AOFF;
+                                    const double wa = yA[e];
+                                    const double wb = yB[e];
+                                    accA += wa * win[rr][col];
+                                    accB += wb * win[rr][col + 1];
+                                }
+                            }
+                        }
+                        const size_t off = static_cast<size_t>(jo) * nx + i0;
+                        if (validA) {
+                            const double tA = accA * inv;
+                            const double sA = sv.x + tA;
+                            const double tB = accB * inv;
+                            const double sB = sv.y + tB;
+                            if (validB) {
+                                *reinterpret_cast<double2*>(Tout + off) = make_double2(tA, tB);
+                                *reinterpret_cast<double2*>(Sout + off) = make_double2(sA, sB);
+                                tb = umax64(tb, umax64(abs_bits(tA), abs_bits(tB)));
+                                sb = umax64(sb, umax64(abs_bits(sA), abs_bits(sB)));
+                            } else {
+                                Tout[off] = tA;
+                                Sout[off] = sA;
+                                tb = umax64(tb, abs_bits(tA));
+                                sb = umax64(sb, abs_bits(sA));
+                            }
+                        }
+                    }
+                    __syncthreads(); // slot consumed by every thread
+                }
+            }
+        }
+        gstep += nsteps;
+
+        tb = warp_umax(tb);
+        sb = warp_umax(sb);
+        if ((t & 31) == 0) {
+            red[0][t >> 5] = tb;
+            red[1][t >> 5] = sb;
+        }
+        __syncthreads();
+        if (t < 32) {
+            const int nw = (NT + 31) / 32;
+            unsigned long long t2 = t < nw ? red[0][t] : 0ULL;
+            unsigned long long s2 = t < nw ? red[1][t] : 0ULL;
+            t2 = warp_umax(t2);
+            s2 = warp_umax(s2);
+            if (t == 0) {
+                if (t2) atomicMax(&a.tn[p], t2);
+                if (s2) atomicMax(&a.sn[p], s2);
+            }
+        }
+    }
+}
+
+constexpr uint64_t mask_of(std::initializer_list<std::pair<int, int>> pts) {
+    uint64_t m = 0;
+    for (auto [dx, dv] : pts) m |= 1ULL << box_bit(dx, dv);
+    return m;
+}
+constexpr uint64_t box_mask(int rx, int rv) {
+    uint64_t m = 0;
+    for (int dv = -rv; dv <= rv; ++dv)
+        for (int dx = -rx; dx <= rx; ++dx) m |= 1ULL << box_bit(dx, dv);
+    return m;
+}
+// Union stencils of the Langevin families: orders 1, 2, 3.
+constexpr uint64_t kMask5 = mask_of({{0, 0}, {-1, 0}, {1, 0}, {0, -1}, {0, 1}});
+constexpr uint64_t kMask11 = kMask5 | mask_of({{0, -2}, {0, 2}, {-1, -1}, {1, -1}, {-1, 1}, {1, 1}});
+constexpr uint64_t kMask19 =
+    kMask11 | mask_of({{-1, -2}, {1, -2}, {-1, 2}, {1, 2}, {-2, -1}, {2, -1}, {-2, 1}, {2, 1}});
+constexpr uint64_t kBox22 = box_mask(2, 2);
+constexpr uint64_t kBox23 = box_mask(2, 3);
+constexpr uint64_t kBox33 = box_mask(3, 3);
+
+struct Variant {
+    uint64_t mask;
+    int rx, rv;
+};
+constexpr Variant kVariants[] = {
+    {0, 0, 0},        // 0: generic
+    {kMask5, 1, 1},   // 1
+    {kMask11, 1, 2},  // 2
+    {kMask19, 2, 2},  // 3
+    {kBox22, 2, 2},   // 4
+    {kBox23, 2, 3},   // 5
+    {kBox33, 3, 3},   // 6
+};
+
+template <int V>
+void launch_term_variant(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, size_t work) {
+    constexpr Variant v = kVariants[V];
+    auto kern = term_tma_kernel<v.rx, v.rv, v.mask>;
+    static int configured_device = -1;
+    static int blocks_per_sm = 1;
+    if (configured_device != ctx->device) {
+        S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured_device = ctx->device;
+    }
+    S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, nt, smem));
+    blocks_per_sm = std::max(1, blocks_per_sm);
+    const size_t cap = static_cast<size_t>(ctx->num_sms) * blocks_per_sm;
+    const int grid = static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
+    kern<<<grid, nt, smem, ctx->stream>>>(a);
+}
+
+int tma_popcount(int variant) { return __builtin_popcountll(kVariants[variant].mask); }
+
+} // namespace
+
+int grid_for(s2b_context* ctx, size_t work, int threads) {
+    (void)threads;
+    const size_t cap = static_cast<size_t>(ctx->num_sms) * 16;
+    return static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
+}
+
+void launch_functionals(s2b_context* ctx, const double* values, size_t steps, size_t M,
+                        size_t dt_steps, size_t nwin, double dt_leb, int order, double* ctab) {
+    const size_t total = M * nwin;
+    const int bs = 128;
+    functionals_kernel<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, ctx->stream>>>(
+        values, steps, M, dt_steps, nwin, dt_leb, order, ctab);
+    S2B_LAUNCHED(ctx);
+}
+
+// ---- operator preparation (host) ---------------------------------------------------
+namespace {
+
+struct SourceStencil {
+    std::map<int, std::vector<double>> w; // bit -> full weight array (n)
+};
+
+} // namespace
+
+s2b_operator* make_operator(s2b_context* ctx, const s2b_grid* grid, int order,
+                            const s2b_csr sources[6]) {
+    if (order < 1 || order > 3) fail(S2B_ERR_CONFIG, "operator: order must be in {1, 2, 3}");
+    const size_t nx = grid->nx, nv = grid->nv, n = nx * nv;
+    if (nx == 0 || nv == 0) fail(S2B_ERR_CONFIG, "operator: empty grid");
+    static const int min_order[6] = {1, 1, 2, 2, 3, 3}; // slot_min_order, magnus.cpp:54
+    std::vector<SourceStencil> st(6);
+    int rx = 0, rv = 0;
+    for (int s = 0; s < 6; ++s) {
+        if (min_order[s] > order) continue;
+        const s2b_csr& m = sources[s];
+        if (m.rows == 0) fail(S2B_ERR_CONFIG, "operator: commutator set lacks a matrix required by the order");
+        if (m.rows != n) fail(S2B_ERR_DIMENSION, "operator: matrix size does not match the grid");
+        for (size_t r = 0; r < n; ++r) {
+            const long long i = static_cast<long long>(r % nx), j = static_cast<long long>(r / nx);
+            for (size_t q = m.row_ptr[r]; q < m.row_ptr[r + 1]; ++q) {
+                const long long col = m.col_idx[q];
+                if (col < 0 || static_cast<size_t>(col) >= n) fail(S2B_ERR_DIMENSION, "operator: column out of range");
+                const long long dx = col % static_cast<long long>(nx) - i;
+                const long long dv = col / static_cast<long long>(nx) - j;
+                if (std::llabs(dx) > kBoxR || std::llabs(dv) > kBoxR)
+                    fail(S2B_ERR_CONFIG, "operator: stencil radius exceeds 3 in x or v");
+                rx = std::max<int>(rx, static_cast<int>(std::llabs(dx)));
+                rv = std::max<int>(rv, static_cast<int>(std::llabs(dv)));
+                const int b = box_bit(static_cast<int>(dx), static_cast<int>(dv));
+                auto& arr = st[s].w[b];
+                if (arr.empty()) arr.assign(n, 0.0);
+                arr[r] = m.values[q];
+            }
+        }
+    }
+    auto* op = new s2b_operator();
+    op->ctx = ctx;
+    op->order = order;
+    op->nx = nx;
+    op->nv = nv;
+    op->rx = rx;
+    op->rv = rv;
+    op->grid = *grid;
+    op->dx_delta = (grid->bx - grid->ax) / static_cast<double>(nx + 1);
+    op->dv_delta = (grid->bv - grid->av) / static_cast<double>(nv + 1);
+    // pairs grouped by bit (ascending), slot order inside a bit
+    op->pair_begin.assign(kBoxBits + 1, 0);
+    std::vector<const std::vector<double>*> pw;
+    for (int b = 0; b < kBoxBits; ++b) {
+        op->pair_begin[b] = static_cast<int>(op->pair_slot.size());
+        for (int s = 0; s < 6; ++s) {
+            auto it = st[s].w.find(b);
+            if (it == st[s].w.end()) continue;
+            op->pair_slot.push_back(s);
+            pw.push_back(&it->second);
+            op->union_mask |= 1ULL << b;
+        }
+    }
+    op->pair_begin[kBoxBits] = static_cast<int>(op->pair_slot.size());
+    op->npairs = static_cast<int>(op->pair_slot.size());
+
+    // x-invariance check: W(i, j) == W(class representative, j) bitwise for every pair
+    bool comp = nx >= 5;
+    auto rep = [&](size_t i) -> size_t { return (i >= 2 && i + 2 < nx) ? 2 : i; };
+    for (size_t q = 0; comp && q < pw.size(); ++q) {
+        const auto& w = *pw[q];
+        for (size_t j = 0; comp && j < nv; ++j)
+            for (size_t i = 0; i < nx; ++i)
+                if (std::memcmp(&w[j * nx + i], &w[j * nx + rep(i)], sizeof(double)) != 0) {
+                    comp = false;
+                    break;
+                }
+    }
+    op->compressed = comp ? 1 : 0;
+    std::vector<double> hw;
+    if (comp) {
+        hw.assign(static_cast<size_t>(op->npairs) * nv * kClasses, 0.0);
+        const size_t cls_i[kClasses] = {0, 1, 2, nx - 2, nx - 1};
+        for (size_t q = 0; q < pw.size(); ++q)
+            for (size_t j = 0; j < nv; ++j)
+                for (int c = 0; c < kClasses; ++c)
+                    hw[(q * nv + j) * kClasses + c] = (*pw[q])[j * nx + cls_i[c]];
+    } else {
+        hw.assign(static_cast<size_t>(op->npairs) * n, 0.0);
+        for (size_t q = 0; q < pw.size(); ++q) std::copy(pw[q]->begin(), pw[q]->end(), hw.begin() + q * n);
+    }
+    op->d_w.alloc(hw.size());
+    op->d_pair_begin.alloc(op->pair_begin.size());
+    op->d_pair_slot.alloc(std::max<size_t>(1, op->pair_slot.size()));
+    S2B_CUDA(cudaMemcpy(op->d_w.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice));
+    S2B_CUDA(cudaMemcpy(op->d_pair_begin.p, op->pair_begin.data(), op->pair_begin.size() * sizeof(int),
+                        cudaMemcpyHostToDevice));
+    if (!op->pair_slot.empty())
+        S2B_CUDA(cudaMemcpy(op->d_pair_slot.p, op->pair_slot.data(), op->pair_slot.size() * sizeof(int),
+                            cudaMemcpyHostToDevice));
+
+    // kernel variant: compressed weights, even nx (16-byte rows), nx <= 1024, mask fits
+    op->variant = 0;
+    if (comp && nx % 2 == 0 && nx <= 1024) {
+        for (int v = 1; v < static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0])); ++v) {
+            if ((op->union_mask & ~kVariants[v].mask) == 0) {
+                op->variant = v;
+                break;
+            }
+        }
+    }
+    return op;
+}
+
+void operator_info(const s2b_operator* op, int64_t info[6]) {
+    info[0] = __builtin_popcountll(op->union_mask);
+    info[1] = op->compressed;
+    info[2] = op->rx;
+    info[3] = op->rv;
+    info[4] = op->npairs;
+    info[5] = op->order;
+}
+
+// ---- session -------------------------------------------------------------------
+struct MagnusSession {
+    s2b_context* ctx = nullptr;
+    const s2b_operator* op = nullptr;
+    const s2b_paths* paths = nullptr;
+    s2b_magnus_config cfg{};
+    std::vector<double> record_times;
+    WindowPlan plan;
+    size_t M = 0, n = 0, nwin = 0;
+    int R = 0;
+    int cur_window = 0; // all live paths are paused at this window boundary
+    std::vector<double> phi;
+
+    DevBuf<double> T[2], S[2];
+    std::vector<DevBuf<double>> rec; // R-1 record buffers
+    DevBuf<double*> rec_ptrs;
+    DevBuf<double> ctab;
+    DevBuf<int> stab;
+    DevBuf<int> iv;              // win seg k nseg status par rec_next  (7 x M)
+    DevBuf<double> prev;
+    DevBuf<long long> terms, windows;
+    DevBuf<unsigned long long> tn, sn;
+    DevBuf<int> act[2];
+    DevBuf<int> cnt;
+    DevBuf<int4> recq;
+    DevBuf<uint8_t> rec_status;
+    DevBuf<long long> rec_steps;
+    DevBuf<int> bits;
+    int nbits = 0;
+    int* h_cnt = nullptr; // pinned
+    int cur = 0;          // which act[] is the input list
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    s2b_magnus_stats stats{};
+
+    Ctl ctl(int win_stop) {
+        Ctl c{};
+        c.win = iv.p;
+        c.seg = iv.p + M;
+        c.k = iv.p + 2 * M;
+        c.nseg = iv.p + 3 * M;
+        c.status = iv.p + 4 * M;
+        c.par = iv.p + 5 * M;
+        c.rec_next = iv.p + 6 * M;
+        c.prev = prev.p;
+        c.terms = terms.p;
+        c.windows = windows.p;
+        c.tn = tn.p;
+        c.sn = sn.p;
+        c.act_in = act[cur].p;
+        c.act_out = act[cur ^ 1].p;
+        c.cnt = cnt.p;
+        c.recq = recq.p;
+        c.rec_status = rec_status.p;
+        c.stab = stab.p;
+        c.rec_steps = rec_steps.p;
+        c.R = R;
+        c.nwin = static_cast<int>(nwin);
+        c.dt_steps = static_cast<int>(plan.dt_steps);
+        c.win_stop = win_stop;
+        c.tol = cfg.expmv_tol;
+        c.cap = cfg.blowup_norm_cap;
+        c.M = M;
+        return c;
+    }
+};
+
+} // namespace s2b
+
+namespace s2b {
+
+void session_reset(MagnusSession* s);
+
+namespace {
+
+void run_records(MagnusSession& s) {
+    if (s.R <= 1) return;
+    dim3 grid(static_cast<unsigned>(std::min<size_t>((s.n + 255) / 256, 64)), 64);
+    record_kernel<<<grid, 256, 0, s.ctx->stream>>>(s.cnt.p, s.recq.p, s.S[0].p, s.S[1].p, s.rec_ptrs.p, s.n);
+    S2B_LAUNCHED(s.ctx);
+}
+
+void swap_lists(MagnusSession& s) {
+    swap_counts_kernel<<<1, 1, 0, s.ctx->stream>>>(s.cnt.p);
+    S2B_LAUNCHED(s.ctx);
+    s.cur ^= 1;
+}
+
+TermArgs term_args(MagnusSession& s) {
+    TermArgs a{};
+    a.op = OpView{s.op->d_pair_begin.p, s.op->d_pair_slot.p, s.op->d_w.p, static_cast<int>(s.op->nx),
+                  static_cast<int>(s.op->nv), s.op->compressed};
+    a.ctab = s.ctab.p;
+    a.nwin = static_cast<int>(s.nwin);
+    a.act = s.act[s.cur].p;
+    a.cnt = s.cnt.p;
+    a.win = s.iv.p;
+    a.k = s.iv.p + 2 * s.M;
+    a.nseg = s.iv.p + 3 * s.M;
+    a.par = s.iv.p + 5 * s.M;
+    a.T0 = s.T[0].p;
+    a.T1 = s.T[1].p;
+    a.S0 = s.S[0].p;
+    a.S1 = s.S[1].p;
+    a.tn = s.tn.p;
+    a.sn = s.sn.p;
+    a.nstrips = static_cast<int>((s.op->nv + kStripRows - 1) / kStripRows);
+    const uint64_t mask = kVariants[s.op->variant].mask;
+    int e = 0;
+    for (int b = 0; b < kBoxBits; ++b)
+        if ((mask >> b) & 1) a.e2bit[e++] = static_cast<int8_t>(b);
+    return a;
+}
+
+void launch_term(MagnusSession& s) {
+    TermArgs a = term_args(s);
+    const int variant = s.op->variant;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (s.timing) {
+        S2B_CUDA(cudaEventCreate(&e0));
+        S2B_CUDA(cudaEventCreate(&e1));
+        S2B_CUDA(cudaEventRecord(e0, s.ctx->stream));
+    }
+    if (variant == 0) {
+        const int bs = 256;
+        const size_t blocks_per_path = (s.n + bs - 1) / bs;
+        const int grid = grid_for(s.ctx, s.M * blocks_per_path, bs);
+        term_generic_kernel<<<grid, bs, 0, s.ctx->stream>>>(a, s.bits.p, s.nbits);
+    } else {
+        const int nt = static_cast<int>(((s.op->nx / 2) + 31) / 32 * 32);
+        const int H = kVariants[variant].rx <= 2 ? 2 : 4;
+        const size_t rw = 2 * static_cast<size_t>(nt) + 2 * H;
+        const size_t smem = 128 + kStages * rw * 8 + kStages * 2 * static_cast<size_t>(nt) * 8 +
+                            static_cast<size_t>(kStripRows) * kClasses * tma_popcount(variant) * 8;
+        const size_t work = s.M * static_cast<size_t>(a.nstrips);
+        switch (variant) {
+        case 1: launch_term_variant<1>(s.ctx, a, nt, smem, work); break;
+        case 2: launch_term_variant<2>(s.ctx, a, nt, smem, work); break;
+        case 3: launch_term_variant<3>(s.ctx, a, nt, smem, work); break;
+        case 4: launch_term_variant<4>(s.ctx, a, nt, smem, work); break;
+        case 5: launch_term_variant<5>(s.ctx, a, nt, smem, work); break;
+        case 6: launch_term_variant<6>(s.ctx, a, nt, smem, work); break;
+        }
+    }
+    S2B_LAUNCHED(s.ctx);
+    s.stats.term_launches += 1;
+    if (s.timing) {
+        S2B_CUDA(cudaEventRecord(e1, s.ctx->stream));
+        s.ev.push_back(e0);
+        s.ev.push_back(e1);
+    }
+}
+
+void collect_timing(MagnusSession& s) {
+    for (size_t q = 0; q + 1 < s.ev.size(); q += 2) {
+        float ms = 0.f;
+        S2B_CUDA(cudaEventElapsedTime(&ms, s.ev[q], s.ev[q + 1]));
+        s.stats.term_kernel_ms += ms;
+        cudaEventDestroy(s.ev[q]);
+        cudaEventDestroy(s.ev[q + 1]);
+    }
+    s.ev.clear();
+}
+
+} // namespace
+
+MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfg,
+                              const double* phi, const s2b_paths* paths) {
+    if (cfg->order < 1 || cfg->order > 3 || cfg->order > op->order)
+        fail(S2B_ERR_CONFIG, "solve_iterated_magnus: unsupported order");
+    if (cfg->order != op->order)
+        fail(S2B_ERR_CONFIG, "solve_iterated_magnus: operator was prepared for a different order");
+    if (!(cfg->expmv_tol > 0.0)) fail(S2B_ERR_CONFIG, "expmv: tol must be positive");
+    if (!(cfg->expmv_theta > 0.0)) fail(S2B_ERR_CONFIG, "expmv: theta must be positive");
+    const size_t n = op->nx * op->nv;
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(phi[i])) fail(S2B_ERR_CONFIG, "solve_iterated_magnus: non-finite datum");
+    auto* s = new MagnusSession();
+    try {
+        s->ctx = ctx;
+        s->op = op;
+        s->paths = paths;
+        s->cfg = *cfg;
+        s->record_times.assign(cfg->record_times, cfg->record_times + cfg->n_record);
+        s->cfg.record_times = s->record_times.data();
+        s->plan = plan_windows(cfg->dt, cfg->T, paths->dt_leb, paths->steps, cfg->record_times,
+                               cfg->n_record, "solver");
+        s->M = paths->M;
+        s->n = n;
+        s->nwin = s->plan.total_steps / s->plan.dt_steps;
+        s->R = static_cast<int>(s->plan.record_steps.size());
+        s->phi.assign(phi, phi + n);
+        const size_t M = s->M;
+        for (int b = 0; b < 2; ++b) {
+            s->T[b].alloc(M * n);
+            s->S[b].alloc(M * n);
+        }
+        std::vector<double*> rp;
+        for (int r = 0; r + 1 < s->R; ++r) {
+            s->rec.emplace_back(M * n);
+            rp.push_back(s->rec.back().p);
+        }
+        s->rec_ptrs.alloc(std::max<size_t>(1, rp.size()));
+        if (!rp.empty())
+            S2B_CUDA(cudaMemcpy(s->rec_ptrs.p, rp.data(), rp.size() * sizeof(double*), cudaMemcpyHostToDevice));
+        s->ctab.alloc(M * s->nwin * 6);
+        s->stab.alloc(M * s->nwin);
+        s->iv.alloc(7 * M);
+        s->prev.alloc(M);
+        s->terms.alloc(M);
+        s->windows.alloc(M);
+        s->tn.alloc(M);
+        s->sn.alloc(M);
+        s->act[0].alloc(M);
+        s->act[1].alloc(M);
+        s->cnt.alloc(4);
+        s->recq.alloc(M * std::max(1, s->R));
+        s->rec_status.alloc(static_cast<size_t>(s->R) * M);
+        s->rec_steps.alloc(s->R);
+        std::vector<long long> rs(s->plan.record_steps.begin(), s->plan.record_steps.end());
+        S2B_CUDA(cudaMemcpy(s->rec_steps.p, rs.data(), rs.size() * sizeof(long long), cudaMemcpyHostToDevice));
+        std::vector<int> bits;
+        for (int b = 0; b < kBoxBits; ++b)
+            if ((op->union_mask >> b) & 1) bits.push_back(b);
+        s->nbits = static_cast<int>(bits.size());
+        s->bits.alloc(std::max<size_t>(1, bits.size()));
+        if (!bits.empty())
+            S2B_CUDA(cudaMemcpy(s->bits.p, bits.data(), bits.size() * sizeof(int), cudaMemcpyHostToDevice));
+        S2B_CUDA(cudaMallocHost(&s->h_cnt, 4 * sizeof(int)));
+
+        // all (path, window) weights and segment counts, in parallel in time
+        launch_functionals(ctx, paths->d_values.p, paths->steps, M, s->plan.dt_steps, s->nwin,
+                           paths->dt_leb, cfg->order, s->ctab.p);
+        OpView ov{op->d_pair_begin.p, op->d_pair_slot.p, op->d_w.p, static_cast<int>(op->nx),
+                  static_cast<int>(op->nv), op->compressed};
+        const size_t count = M * s->nwin;
+        for (size_t off = 0; off < count; off += 1u << 30) {
+            const size_t chunk = std::min<size_t>(count - off, 1u << 30);
+            norm_kernel<<<static_cast<unsigned>(chunk), 256, 0, ctx->stream>>>(
+                ov, s->bits.p, s->nbits, op->rx, s->ctab.p + off * 6, chunk, cfg->expmv_theta,
+                s->stab.p + off, nullptr);
+            S2B_LAUNCHED(ctx);
+        }
+        session_reset(s);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    return s;
+}
+
+void session_reset(MagnusSession* s) {
+    const size_t M = s->M, n = s->n;
+    for (size_t m = 0; m < M; ++m)
+        S2B_CUDA(cudaMemcpyAsync(s->S[0].p + m * n, s->phi.data(), n * sizeof(double),
+                                 cudaMemcpyHostToDevice, s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->iv.p, 0, s->iv.bytes(), s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->rec_status.p, 1, s->rec_status.bytes(), s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), s->ctx->stream));
+    s->cur = 0;
+    s->cur_window = 0;
+    s->stats = s2b_magnus_stats{};
+    s->stats.gridpoints = static_cast<double>(n);
+    S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+}
+
+void session_advance(MagnusSession* s, size_t n_windows) {
+    if (n_windows == 0 || static_cast<size_t>(s->cur_window) >= s->nwin) return;
+    const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
+    {
+        // (re)activate every live path at the current window boundary; window 0 also
+        // initialises the per-path state (parity, records, counters)
+        Ctl c = s->ctl(stop);
+        S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), s->ctx->stream));
+        init_kernel<<<static_cast<unsigned>((s->M + 127) / 128), 128, 0, s->ctx->stream>>>(c, s->cur_window);
+        S2B_LAUNCHED(s->ctx);
+        run_records(*s);
+        swap_lists(*s);
+    }
+    int chunk = 4;
+    while (true) {
+        S2B_CUDA(cudaMemcpyAsync(s->h_cnt, s->cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s->ctx->stream));
+        S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        if (s->timing) collect_timing(*s);
+        if (s->h_cnt[0] == 0) break;
+        for (int q = 0; q < chunk; ++q) {
+            launch_term(*s);
+            Ctl c = s->ctl(stop);
+            control_kernel<<<static_cast<unsigned>((s->M + 255) / 256), 256, 0, s->ctx->stream>>>(c);
+            S2B_LAUNCHED(s->ctx);
+            run_records(*s);
+            swap_lists(*s);
+            s->stats.passes += 1;
+        }
+        chunk = std::min(chunk * 2, 64);
+    }
+    s->cur_window = stop;
+}
+
+void session_stats(const MagnusSession* s, s2b_magnus_stats* out) {
+    *out = s->stats;
+    std::vector<long long> t(s->M), w(s->M);
+    S2B_CUDA(cudaMemcpy(t.data(), s->terms.p, s->M * sizeof(long long), cudaMemcpyDeviceToHost));
+    S2B_CUDA(cudaMemcpy(w.data(), s->windows.p, s->M * sizeof(long long), cudaMemcpyDeviceToHost));
+    out->path_terms = 0;
+    out->path_windows = 0;
+    for (size_t m = 0; m < s->M; ++m) {
+        out->path_terms += t[m];
+        out->path_windows += w[m];
+    }
+}
+
+void session_set_timing(MagnusSession* s, bool on) { s->timing = on; }
+
+namespace {
+__global__ void gather_kernel(const int* __restrict__ par, const double* __restrict__ S0,
+                              const double* __restrict__ S1, double* __restrict__ dst, size_t n,
+                              size_t M) {
+    const size_t m = blockIdx.y;
+    if (m >= M) return;
+    const double* src = (par[m] ? S1 : S0) + m * n;
+    double* d = dst + m * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        d[i] = src[i];
+}
+__global__ void live_status_kernel(const int* __restrict__ status, uint8_t* __restrict__ out, size_t M) {
+    const size_t m = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (m < M) out[m] = status[m] == 2 ? 1 : 0;
+}
+} // namespace
+
+s2b_ensemble* session_snapshot(MagnusSession* s) {
+    auto* e = new s2b_ensemble();
+    e->ctx = s->ctx;
+    e->R = 1;
+    e->M = s->M;
+    e->nx = s->op->nx;
+    e->nv = s->op->nv;
+    e->seed = s->paths->seed;
+    e->grid = s->op->grid;
+    e->times.push_back(static_cast<double>(s->cur_window * s->plan.dt_steps) * s->paths->dt_leb);
+    e->states.emplace_back(s->M * s->n);
+    e->status.alloc(s->M);
+    dim3 g(static_cast<unsigned>(std::min<size_t>((s->n + 255) / 256, 128)), static_cast<unsigned>(s->M));
+    gather_kernel<<<g, 256, 0, s->ctx->stream>>>(s->iv.p + 5 * s->M, s->S[0].p, s->S[1].p, e->states[0].p, s->n, s->M);
+    S2B_LAUNCHED(s->ctx);
+    live_status_kernel<<<static_cast<unsigned>((s->M + 255) / 256), 256, 0, s->ctx->stream>>>(s->iv.p + 4 * s->M, e->status.p, s->M);
+    S2B_LAUNCHED(s->ctx);
+    e->terms.alloc(s->M);
+    e->windows.alloc(s->M);
+    S2B_CUDA(cudaMemcpyAsync(e->terms.p, s->terms.p, s->M * sizeof(long long), cudaMemcpyDeviceToDevice, s->ctx->stream));
+    S2B_CUDA(cudaMemcpyAsync(e->windows.p, s->windows.p, s->M * sizeof(long long), cudaMemcpyDeviceToDevice, s->ctx->stream));
+    S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    return e;
+}
+
+s2b_ensemble* session_finish(MagnusSession* s) {
+    if (static_cast<size_t>(s->cur_window) < s->nwin) session_advance(s, s->nwin - s->cur_window);
+    auto* e = new s2b_ensemble();
+    e->ctx = s->ctx;
+    e->R = s->R;
+    e->M = s->M;
+    e->nx = s->op->nx;
+    e->nv = s->op->nv;
+    e->seed = s->paths->seed;
+    e->grid = s->op->grid;
+    for (size_t r = 0; r < static_cast<size_t>(s->R); ++r)
+        e->times.push_back(static_cast<double>(s->plan.record_steps[r]) * s->paths->dt_leb);
+    for (auto& b : s->rec) e->states.push_back(std::move(b));
+    s->rec.clear();
+    // final record: gather the current buffers into T[0]'s storage (no longer needed)
+    DevBuf<double> fin = std::move(s->T[0]);
+    dim3 g(static_cast<unsigned>(std::min<size_t>((s->n + 255) / 256, 128)), static_cast<unsigned>(s->M));
+    gather_kernel<<<g, 256, 0, s->ctx->stream>>>(s->iv.p + 5 * s->M, s->S[0].p, s->S[1].p, fin.p, s->n, s->M);
+    S2B_LAUNCHED(s->ctx);
+    e->states.push_back(std::move(fin));
+    e->status = std::move(s->rec_status);
+    e->terms = std::move(s->terms);
+    e->windows = std::move(s->windows);
+    S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    return e;
+}
+
+void session_destroy(MagnusSession* s) {
+    if (!s) return;
+    for (auto ev : s->ev) cudaEventDestroy(ev);
+    if (s->h_cnt) cudaFreeHost(s->h_cnt);
+    delete s;
+}
+
+} // namespace s2b
