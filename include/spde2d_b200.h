@@ -110,6 +110,7 @@ typedef struct {
     int64_t term_launches; /* launches of the dominant term kernel */
     double term_kernel_ms; /* summed CUDA-event time of those launches (if timing enabled) */
     double gridpoints;     /* nx*nv */
+    int64_t path_segments; /* sum over paths of Taylor segments (one k=1 term each) */
 } s2b_magnus_stats;
 
 const char *s2b_last_error(void);
@@ -159,6 +160,10 @@ int s2b_paths_create_host(s2b_context *ctx, double dt_leb, size_t steps, size_t 
 int s2b_paths_create_philox(s2b_context *ctx, double dt_leb, size_t steps, size_t M,
                             uint64_t seed, uint64_t path_offset, s2b_paths **out);
 int s2b_paths_download(const s2b_paths *p, double *values_out);
+/* Overwrite columns [k0, k1] of every path's prefix values from a host array laid out
+ * like BrownianBatch::values ([M][steps+1]); the columns copied are the inputs of the
+ * windows covering [k0, k1] (pinned host memory makes this an async DMA). */
+int s2b_paths_upload(s2b_paths *p, size_t k0, size_t k1, const double *values);
 int s2b_paths_destroy(s2b_paths *p);
 
 /* ---- solvers -----------------------------------------------------------------
@@ -184,6 +189,9 @@ int s2b_magnus_session_set_timing(s2b_magnus_session *s, int enable);
 int s2b_magnus_session_ensemble(s2b_magnus_session *s, s2b_ensemble **out);
 /* Finish: the ensemble of record times (valid once every path reached T). */
 int s2b_magnus_session_finish(s2b_magnus_session *s, s2b_ensemble **out);
+/* sum_m u_m and sum_m u_m^2 (2n doubles, host) over live paths at the current time;
+ * live_paths (NULL-able) receives the number of non-blown paths. */
+int s2b_magnus_session_moments(s2b_magnus_session *s, double *moments, double *live_paths);
 int s2b_magnus_session_destroy(s2b_magnus_session *s);
 
 /* ---- ensembles -------------------------------------------------------------- */

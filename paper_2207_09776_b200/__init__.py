@@ -280,6 +280,11 @@ class BrownianPaths:
                                              C.byref(h)))
         return cls(h, ctx, dt_leb, steps, M, seed)
 
+    def upload(self, k0, k1, values):
+        """Overwrite Lebesgue columns [k0, k1] of every path from a host [M][steps+1] array
+        (asynchronous on the context stream when `values` is pinned)."""
+        _check(lib().s2b_paths_upload(self.h, k0, k1, _dptr(values)))
+
     def values(self):
         out = np.empty((self.M, self.steps + 1))
         _check(lib().s2b_paths_download(self.h, _dptr(out)))
@@ -444,6 +449,14 @@ class MagnusSession:
         st = _capi.MagnusStats()
         _check(lib().s2b_magnus_session_stats(self.h, C.byref(st)))
         return {k: getattr(st, k) for k, _ in _capi.MagnusStats._fields_}
+
+    def moments(self, out=None):
+        """(sum_m u_m, sum_m u_m^2) over live paths at the current time, and the live count."""
+        n = self.grid.dim()
+        out = np.empty(2 * n) if out is None else out
+        live = C.c_double()
+        _check(lib().s2b_magnus_session_moments(self.h, _dptr(out), C.byref(live)))
+        return out[:n], out[n:], int(live.value)
 
     def snapshot(self):
         h = C.c_void_p()

@@ -47,7 +47,7 @@ class ErrorStats(C.Structure):
 class MagnusStats(C.Structure):
     _fields_ = [("passes", C.c_int64), ("path_terms", C.c_int64), ("path_windows", C.c_int64),
                 ("term_launches", C.c_int64), ("term_kernel_ms", C.c_double),
-                ("gridpoints", C.c_double)]
+                ("gridpoints", C.c_double), ("path_segments", C.c_int64)]
 
 
 # Exported symbols with their ctypes signatures (restype int unless noted).
@@ -75,6 +75,7 @@ SIGNATURES = {
     "s2b_paths_create_philox": (C.c_int, [_VP, C.c_double, C.c_size_t, C.c_size_t, C.c_uint64,
                                           C.c_uint64, _P(_VP)]),
     "s2b_paths_download": (C.c_int, [_VP, _P(C.c_double)]),
+    "s2b_paths_upload": (C.c_int, [_VP, C.c_size_t, C.c_size_t, _P(C.c_double)]),
     "s2b_paths_destroy": (C.c_int, [_VP]),
     "s2b_solve_magnus": (C.c_int, [_VP, _VP, _P(MagnusConfig), _P(C.c_double), _VP, _P(_VP),
                                    _P(MagnusStats)]),
@@ -87,6 +88,7 @@ SIGNATURES = {
     "s2b_magnus_session_set_timing": (C.c_int, [_VP, C.c_int]),
     "s2b_magnus_session_ensemble": (C.c_int, [_VP, _P(_VP)]),
     "s2b_magnus_session_finish": (C.c_int, [_VP, _P(_VP)]),
+    "s2b_magnus_session_moments": (C.c_int, [_VP, _P(C.c_double), _P(C.c_double)]),
     "s2b_magnus_session_destroy": (C.c_int, [_VP]),
     "s2b_ensemble_info": (C.c_int, [_VP, _P(C.c_int64), _P(C.c_double)]),
     "s2b_ensemble_download": (C.c_int, [_VP, C.c_size_t, _P(C.c_double), _P(C.c_uint8)]),

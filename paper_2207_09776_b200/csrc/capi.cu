@@ -269,6 +269,17 @@ int s2b_paths_download(const s2b_paths* p, double* values_out) {
     });
 }
 
+int s2b_paths_upload(s2b_paths* p, size_t k0, size_t k1, const double* values) {
+    return guard([&] {
+        need(p, "paths");
+        need(values, "values");
+        if (k1 < k0 || k1 > p->steps) fail(S2B_ERR_DIMENSION, "paths_upload: column range out of bounds");
+        const size_t pitch = (p->steps + 1) * sizeof(double);
+        S2B_CUDA(cudaMemcpy2DAsync(p->d_values.p + k0, pitch, values + k0, pitch, (k1 - k0 + 1) * sizeof(double),
+                                   p->M, cudaMemcpyHostToDevice, p->ctx->stream));
+    });
+}
+
 int s2b_paths_destroy(s2b_paths* p) {
     return guard([&] { delete p; });
 }
@@ -366,6 +377,14 @@ int s2b_magnus_session_finish(s2b_magnus_session* s, s2b_ensemble** out) {
         need(s, "session");
         need(out, "out");
         *out = session_finish(S(s));
+    });
+}
+
+int s2b_magnus_session_moments(s2b_magnus_session* s, double* moments, double* live_paths) {
+    return guard([&] {
+        need(s, "session");
+        need(moments, "moments");
+        session_moments(S(s), moments, live_paths);
     });
 }
 

@@ -29,14 +29,15 @@ struct EmArgs {
     const double* in;
     double* out;
     int* blown;
+    size_t M;
 };
 
 template <bool GXV>
 __global__ void __launch_bounds__(256) em_step_kernel(EmArgs a) {
     const int nx = a.nx, nv = a.nv;
     const size_t n = static_cast<size_t>(nx) * nv;
-    const int m = blockIdx.y;
-    if (a.blown[m]) return; // the reference stops a blown path (euler.cpp:159-162)
+  for (size_t m = blockIdx.y; m < a.M; m += gridDim.y) {
+    if (a.blown[m]) continue; // the reference stops a blown path (euler.cpp:159-162)
     const double* u = a.in + static_cast<size_t>(m) * n;
     double* o = a.out + static_cast<size_t>(m) * n;
     const double* pv = a.values + static_cast<size_t>(m) * a.vstride;
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(256) em_step_kernel(EmArgs a) {
         inf_seen |= fabs(next) == __longlong_as_double(0x7FF0000000000000LL);
     }
     if (inf_seen) a.blown[m] = 1;
+  }
 }
 
 __global__ void em_record_status_kernel(const int* blown, uint8_t* status, size_t M) {
@@ -144,8 +146,7 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         DevBuf<double> U[2] = {DevBuf<double>(M * n), DevBuf<double>(M * n)};
         DevBuf<int> blown(M);
         S2B_CUDA(cudaMemsetAsync(blown.p, 0, blown.bytes(), ctx->stream));
-        for (size_t m = 0; m < M; ++m)
-            S2B_CUDA(cudaMemcpyAsync(U[0].p + m * n, phi, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        broadcast_rows(ctx, U[0].p, phi, n, M);
         EmArgs a{};
         a.f = f->d_f.p;
         a.mask = f->mask;
@@ -156,6 +157,7 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         a.values = paths->d_values.p;
         a.vstride = paths->steps + 1;
         a.blown = blown.p;
+        a.M = M;
         const size_t nsteps = plan.total_steps / plan.dt_steps;
         const unsigned gx = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64));
         size_t rec = 0;
@@ -165,7 +167,7 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
             a.k1 = (k + 1) * plan.dt_steps;
             a.in = U[cur].p;
             a.out = U[cur ^ 1].p;
-            dim3 grid(gx, static_cast<unsigned>(M));
+            dim3 grid(gx, static_cast<unsigned>(std::min<size_t>(M, 65535)));
             if (f->mask & 16)
                 em_step_kernel<true><<<grid, 256, 0, ctx->stream>>>(a);
             else

@@ -70,11 +70,12 @@ __device__ __forceinline__ unsigned long long warp_umax(unsigned long long v) {
 // lebesgue_functionals (stochastics.cpp:121-141) + log_coefficients (magnus.cpp:26-40),
 // one thread per (path, window): all windows of all paths at once.
 __global__ void functionals_kernel(const double* __restrict__ values, size_t steps, size_t M,
-                                   size_t dt_steps, size_t nwin, double dt, int order,
-                                   double* __restrict__ ctab) {
-    const size_t id = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (id >= M * nwin) return;
-    const size_t m = id / nwin, w = id % nwin;
+                                   size_t dt_steps, size_t nwin, size_t w0, size_t nw, double dt,
+                                   int order, double* __restrict__ ctab) {
+    const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (tid >= M * nw) return;
+    const size_t m = tid / nw, w = w0 + tid % nw;
+    const size_t id = m * nwin + w;
     const double* p = values + m * (steps + 1);
     const size_t k0 = w * dt_steps, k1 = k0 + dt_steps;
     const double base = p[k0];
@@ -147,10 +148,9 @@ __device__ double column_sum(const OpView& op, const double* c, const int* bits,
 // Compressed layout: only columns whose stencil rows touch a boundary class, plus one
 // interior representative, are distinct.
 __global__ void norm_kernel(OpView op, const int* __restrict__ bits, int nbits, int rx,
-                            const double* __restrict__ ctab, size_t count, double theta,
-                            int* __restrict__ stab, double* __restrict__ norms) {
-    const size_t id = blockIdx.x;
-    if (id >= count) return;
+                            const double* __restrict__ ctab, size_t nwin, size_t w0, size_t nw,
+                            double theta, int* __restrict__ stab, double* __restrict__ norms) {
+    const size_t id = (blockIdx.x / nw) * nwin + w0 + blockIdx.x % nw;
     __shared__ double c[6];
     __shared__ unsigned long long red[32];
     if (threadIdx.x < 6) c[threadIdx.x] = ctab[id * 6 + threadIdx.x];
@@ -197,6 +197,7 @@ struct Ctl {
     double* prev;   // previous term inf-norm
     long long* terms;
     long long* windows;
+    long long* segments;
     unsigned long long* tn; // running max |t| (bits)
     unsigned long long* sn; // running max |accum| (bits)
     int* act_in;
@@ -259,6 +260,7 @@ __global__ void init_kernel(Ctl c, int first_window) {
         c.rec_next[p] = 0;
         c.terms[p] = 0;
         c.windows[p] = 0;
+        c.segments[p] = 0;
     }
     if (enter_window(c, p, first_window, c.par[p])) c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
 }
@@ -285,6 +287,7 @@ __global__ void control_kernel(Ctl c) {
     const int k = c.k[p];
     if (tn <= gate && c.prev[p] <= gate) {
         const int seg = c.seg[p] + 1;
+        c.segments[p] += 1;
         if (seg < c.nseg[p]) {
             c.seg[p] = seg;
             c.k[p] = 1;
@@ -728,15 +731,6 @@ int grid_for(s2b_context* ctx, size_t work, int threads) {
     return static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
 }
 
-void launch_functionals(s2b_context* ctx, const double* values, size_t steps, size_t M,
-                        size_t dt_steps, size_t nwin, double dt_leb, int order, double* ctab) {
-    const size_t total = M * nwin;
-    const int bs = 128;
-    functionals_kernel<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, ctx->stream>>>(
-        values, steps, M, dt_steps, nwin, dt_leb, order, ctab);
-    S2B_LAUNCHED(ctx);
-}
-
 // ---- operator preparation (host) ---------------------------------------------------
 namespace {
 
@@ -880,7 +874,7 @@ struct MagnusSession {
     DevBuf<int> stab;
     DevBuf<int> iv;              // win seg k nseg status par rec_next  (7 x M)
     DevBuf<double> prev;
-    DevBuf<long long> terms, windows;
+    DevBuf<long long> terms, windows, segments;
     DevBuf<unsigned long long> tn, sn;
     DevBuf<int> act[2];
     DevBuf<int> cnt;
@@ -907,6 +901,7 @@ struct MagnusSession {
         c.prev = prev.p;
         c.terms = terms.p;
         c.windows = windows.p;
+        c.segments = segments.p;
         c.tn = tn.p;
         c.sn = sn.p;
         c.act_in = act[cur].p;
@@ -1071,6 +1066,7 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
         s->prev.alloc(M);
         s->terms.alloc(M);
         s->windows.alloc(M);
+        s->segments.alloc(M);
         s->tn.alloc(M);
         s->sn.alloc(M);
         s->act[0].alloc(M);
@@ -1090,19 +1086,6 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
             S2B_CUDA(cudaMemcpy(s->bits.p, bits.data(), bits.size() * sizeof(int), cudaMemcpyHostToDevice));
         S2B_CUDA(cudaMallocHost(&s->h_cnt, 4 * sizeof(int)));
 
-        // all (path, window) weights and segment counts, in parallel in time
-        launch_functionals(ctx, paths->d_values.p, paths->steps, M, s->plan.dt_steps, s->nwin,
-                           paths->dt_leb, cfg->order, s->ctab.p);
-        OpView ov{op->d_pair_begin.p, op->d_pair_slot.p, op->d_w.p, static_cast<int>(op->nx),
-                  static_cast<int>(op->nv), op->compressed};
-        const size_t count = M * s->nwin;
-        for (size_t off = 0; off < count; off += 1u << 30) {
-            const size_t chunk = std::min<size_t>(count - off, 1u << 30);
-            norm_kernel<<<static_cast<unsigned>(chunk), 256, 0, ctx->stream>>>(
-                ov, s->bits.p, s->nbits, op->rx, s->ctab.p + off * 6, chunk, cfg->expmv_theta,
-                s->stab.p + off, nullptr);
-            S2B_LAUNCHED(ctx);
-        }
         session_reset(s);
     } catch (...) {
         delete s;
@@ -1113,9 +1096,7 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
 
 void session_reset(MagnusSession* s) {
     const size_t M = s->M, n = s->n;
-    for (size_t m = 0; m < M; ++m)
-        S2B_CUDA(cudaMemcpyAsync(s->S[0].p + m * n, s->phi.data(), n * sizeof(double),
-                                 cudaMemcpyHostToDevice, s->ctx->stream));
+    broadcast_rows(s->ctx, s->S[0].p, s->phi.data(), n, M);
     S2B_CUDA(cudaMemsetAsync(s->iv.p, 0, s->iv.bytes(), s->ctx->stream));
     S2B_CUDA(cudaMemsetAsync(s->rec_status.p, 1, s->rec_status.bytes(), s->ctx->stream));
     S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), s->ctx->stream));
@@ -1126,9 +1107,32 @@ void session_reset(MagnusSession* s) {
     S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
 }
 
+// Functionals, logarithm weights and segment counts of windows [w0, w1) of every path,
+// all in parallel in time, from the device path values as they are now.
+void prepare_windows(MagnusSession* s, size_t w0, size_t w1) {
+    const size_t M = s->M, nw = w1 - w0;
+    if (nw == 0) return;
+    const s2b_operator* op = s->op;
+    const size_t total = M * nw;
+    functionals_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s->ctx->stream>>>(
+        s->paths->d_values.p, s->paths->steps, M, s->plan.dt_steps, s->nwin, w0, nw,
+        s->paths->dt_leb, s->cfg.order, s->ctab.p);
+    S2B_LAUNCHED(s->ctx);
+    OpView ov{op->d_pair_begin.p, op->d_pair_slot.p, op->d_w.p, static_cast<int>(op->nx),
+              static_cast<int>(op->nv), op->compressed};
+    for (size_t m0 = 0; m0 < M; m0 += (1u << 30) / nw) {
+        const size_t mc = std::min<size_t>(M - m0, (1u << 30) / nw);
+        norm_kernel<<<static_cast<unsigned>(mc * nw), 256, 0, s->ctx->stream>>>(
+            ov, s->bits.p, s->nbits, op->rx, s->ctab.p + m0 * s->nwin * 6, s->nwin, w0, nw,
+            s->cfg.expmv_theta, s->stab.p + m0 * s->nwin, nullptr);
+        S2B_LAUNCHED(s->ctx);
+    }
+}
+
 void session_advance(MagnusSession* s, size_t n_windows) {
     if (n_windows == 0 || static_cast<size_t>(s->cur_window) >= s->nwin) return;
     const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
+    prepare_windows(s, s->cur_window, stop);
     {
         // (re)activate every live path at the current window boundary; window 0 also
         // initialises the per-path state (parity, records, counters)
@@ -1164,11 +1168,15 @@ void session_stats(const MagnusSession* s, s2b_magnus_stats* out) {
     std::vector<long long> t(s->M), w(s->M);
     S2B_CUDA(cudaMemcpy(t.data(), s->terms.p, s->M * sizeof(long long), cudaMemcpyDeviceToHost));
     S2B_CUDA(cudaMemcpy(w.data(), s->windows.p, s->M * sizeof(long long), cudaMemcpyDeviceToHost));
+    std::vector<long long> g(s->M);
+    S2B_CUDA(cudaMemcpy(g.data(), s->segments.p, s->M * sizeof(long long), cudaMemcpyDeviceToHost));
     out->path_terms = 0;
     out->path_windows = 0;
+    out->path_segments = 0;
     for (size_t m = 0; m < s->M; ++m) {
         out->path_terms += t[m];
         out->path_windows += w[m];
+        out->path_segments += g[m];
     }
 }
 
@@ -1178,13 +1186,13 @@ namespace {
 __global__ void gather_kernel(const int* __restrict__ par, const double* __restrict__ S0,
                               const double* __restrict__ S1, double* __restrict__ dst, size_t n,
                               size_t M) {
-    const size_t m = blockIdx.y;
-    if (m >= M) return;
-    const double* src = (par[m] ? S1 : S0) + m * n;
-    double* d = dst + m * n;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x)
-        d[i] = src[i];
+    for (size_t m = blockIdx.y; m < M; m += gridDim.y) {
+        const double* src = (par[m] ? S1 : S0) + m * n;
+        double* d = dst + m * n;
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<size_t>(gridDim.x) * blockDim.x)
+            d[i] = src[i];
+    }
 }
 __global__ void live_status_kernel(const int* __restrict__ status, uint8_t* __restrict__ out, size_t M) {
     const size_t m = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -1204,7 +1212,7 @@ s2b_ensemble* session_snapshot(MagnusSession* s) {
     e->times.push_back(static_cast<double>(s->cur_window * s->plan.dt_steps) * s->paths->dt_leb);
     e->states.emplace_back(s->M * s->n);
     e->status.alloc(s->M);
-    dim3 g(static_cast<unsigned>(std::min<size_t>((s->n + 255) / 256, 128)), static_cast<unsigned>(s->M));
+    dim3 g(static_cast<unsigned>(std::min<size_t>((s->n + 255) / 256, 128)), static_cast<unsigned>(std::min<size_t>(s->M, 65535)));
     gather_kernel<<<g, 256, 0, s->ctx->stream>>>(s->iv.p + 5 * s->M, s->S[0].p, s->S[1].p, e->states[0].p, s->n, s->M);
     S2B_LAUNCHED(s->ctx);
     live_status_kernel<<<static_cast<unsigned>((s->M + 255) / 256), 256, 0, s->ctx->stream>>>(s->iv.p + 4 * s->M, e->status.p, s->M);
@@ -1233,7 +1241,7 @@ s2b_ensemble* session_finish(MagnusSession* s) {
     s->rec.clear();
     // final record: gather the current buffers into T[0]'s storage (no longer needed)
     DevBuf<double> fin = std::move(s->T[0]);
-    dim3 g(static_cast<unsigned>(std::min<size_t>((s->n + 255) / 256, 128)), static_cast<unsigned>(s->M));
+    dim3 g(static_cast<unsigned>(std::min<size_t>((s->n + 255) / 256, 128)), static_cast<unsigned>(std::min<size_t>(s->M, 65535)));
     gather_kernel<<<g, 256, 0, s->ctx->stream>>>(s->iv.p + 5 * s->M, s->S[0].p, s->S[1].p, fin.p, s->n, s->M);
     S2B_LAUNCHED(s->ctx);
     e->states.push_back(std::move(fin));
@@ -1242,6 +1250,42 @@ s2b_ensemble* session_finish(MagnusSession* s) {
     e->windows = std::move(s->windows);
     S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
     return e;
+}
+
+namespace {
+// sum_m u_m and sum_m u_m^2 over live (not blown) paths, ascending m, reading each path's
+// current buffer; the statistic the multi-GPU path all-reduces.
+__global__ void session_moments_kernel(const int* __restrict__ par, const int* __restrict__ status,
+                                       const double* __restrict__ S0, const double* __restrict__ S1,
+                                       size_t M, size_t n, double* __restrict__ mom) {
+    const size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (r >= n) return;
+    double s1 = 0.0, s2 = 0.0;
+    for (size_t m = 0; m < M; ++m) {
+        if (status[m] == 2) continue;
+        const double u = (par[m] ? S1 : S0)[m * n + r];
+        s1 += u;
+        s2 += u * u;
+    }
+    mom[r] = s1;
+    mom[n + r] = s2;
+}
+} // namespace
+
+void session_moments(MagnusSession* s, double* host_out, double* live_out) {
+    DevBuf<double> mom(2 * s->n);
+    session_moments_kernel<<<static_cast<unsigned>((s->n + 127) / 128), 128, 0, s->ctx->stream>>>(
+        s->iv.p + 5 * s->M, s->iv.p + 4 * s->M, s->S[0].p, s->S[1].p, s->M, s->n, mom.p);
+    S2B_LAUNCHED(s->ctx);
+    S2B_CUDA(cudaMemcpyAsync(host_out, mom.p, mom.bytes(), cudaMemcpyDeviceToHost, s->ctx->stream));
+    std::vector<int> st(s->M);
+    S2B_CUDA(cudaMemcpyAsync(st.data(), s->iv.p + 4 * s->M, s->M * sizeof(int), cudaMemcpyDeviceToHost, s->ctx->stream));
+    S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    if (live_out) {
+        size_t live = 0;
+        for (int v : st) live += v != 2;
+        *live_out = static_cast<double>(live);
+    }
 }
 
 void session_destroy(MagnusSession* s) {

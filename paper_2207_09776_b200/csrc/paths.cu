@@ -75,7 +75,27 @@ __global__ void prefix_kernel(double* values, size_t steps, size_t M) {
     }
 }
 
+__global__ void broadcast_kernel(const double* __restrict__ src, double* __restrict__ dst, size_t n) {
+    double* d = dst + blockIdx.y * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        d[i] = src[i];
+}
+
 } // namespace
+
+// dst[m][:] = host_src[:] for m < M (one H2D copy, then a device broadcast).
+void broadcast_rows(s2b_context* ctx, double* dst, const double* host_src, size_t n, size_t M) {
+    DevBuf<double> tmp(n);
+    S2B_CUDA(cudaMemcpyAsync(tmp.p, host_src, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    for (size_t m0 = 0; m0 < M; m0 += 65535) {
+        const size_t mc = std::min<size_t>(65535, M - m0);
+        dim3 g(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64)), static_cast<unsigned>(mc));
+        broadcast_kernel<<<g, 256, 0, ctx->stream>>>(tmp.p, dst + m0 * n, n);
+        S2B_LAUNCHED(ctx);
+    }
+    S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+}
 
 s2b_paths* make_paths_host(s2b_context* ctx, double dt_leb, size_t steps, size_t M, uint64_t seed,
                            const double* values) {

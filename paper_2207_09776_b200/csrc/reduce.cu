@@ -78,12 +78,13 @@ __global__ void path_w_iw_kernel(const double* values, size_t stride, size_t k1,
 
 __global__ void exact_field_kernel(ExactParams p, const double2* wiw, double* out, size_t M) {
     const size_t n = static_cast<size_t>(p.nx) * p.nv;
-    const size_t m = blockIdx.y;
-    const double2 f = wiw[m];
-    for (size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; r < n;
-         r += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(r % p.nx), j = static_cast<int>(r / p.nx);
-        out[m * n + r] = exact_value(p, f.x, f.y, i, j);
+    for (size_t m = blockIdx.y; m < M; m += gridDim.y) {
+        const double2 f = wiw[m];
+        for (size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; r < n;
+             r += static_cast<size_t>(gridDim.x) * blockDim.x) {
+            const int i = static_cast<int>(r % p.nx), j = static_cast<int>(r / p.nx);
+            out[m * n + r] = exact_value(p, f.x, f.y, i, j);
+        }
     }
 }
 
@@ -257,7 +258,7 @@ s2b_ensemble* exact_reference(s2b_context* ctx, const s2b_grid* grid, double t, 
     path_w_iw_kernel<<<static_cast<unsigned>((M + 127) / 128), 128, 0, ctx->stream>>>(
         paths->d_values.p, paths->steps + 1, k1, paths->dt_leb, M, wiw.p);
     S2B_LAUNCHED(ctx);
-    dim3 g(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 256)), static_cast<unsigned>(M));
+    dim3 g(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 256)), static_cast<unsigned>(std::min<size_t>(M, 65535)));
     exact_field_kernel<<<g, 256, 0, ctx->stream>>>(p, wiw.p, e->states[0].p, M);
     S2B_LAUNCHED(ctx);
     S2B_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -138,9 +138,8 @@ WindowPlan plan_windows(double dt, double T, double dt_leb, size_t steps,
                         const double* record_times, size_t n_record, const char* who);
 
 // Launch helpers implemented in the .cu files.
-void launch_functionals(s2b_context* ctx, const double* values, size_t steps, size_t M,
-                        size_t dt_steps, size_t nwin, double dt_leb, int order, double* ctab);
 int grid_for(s2b_context* ctx, size_t work, int threads);
+void broadcast_rows(s2b_context* ctx, double* dst, const double* host_src, size_t n, size_t M);
 
 // Entry points behind the C ABI (implemented per .cu file).
 s2b_operator* make_operator(s2b_context* ctx, const s2b_grid* grid, int order, const s2b_csr sources[6]);
@@ -155,6 +154,7 @@ void session_set_timing(MagnusSession* s, bool on);
 s2b_ensemble* session_snapshot(MagnusSession* s);
 s2b_ensemble* session_finish(MagnusSession* s);
 void session_destroy(MagnusSession* s);
+void session_moments(MagnusSession* s, double* host_out, double* live_out);
 s2b_paths* make_paths_host(s2b_context* ctx, double dt_leb, size_t steps, size_t M, uint64_t seed,
                            const double* values);
 s2b_paths* make_paths_philox(s2b_context* ctx, double dt_leb, size_t steps, size_t M, uint64_t seed,
