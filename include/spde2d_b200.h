@@ -151,6 +151,21 @@ int s2b_fields_destroy(s2b_fields *f);
 /* Gaussian datum phi = exp(-(x^2+v^2)/2) at interior nodes, host-computed (n doubles). */
 int s2b_gaussian_datum(const s2b_grid *grid, double *out);
 
+/* ---- host-kept builder (no GPU needed) -----------------------------------------
+ * The CSR CommutatorSet and CoefficientFields exactly as the reference builds them
+ * (operators.cpp:134-208 arithmetic order), for callers that hand CSR to
+ * s2b_operator_create or want to inspect it.  Pointers returned by the accessors stay
+ * valid until s2b_host_ops_destroy. */
+typedef struct s2b_host_ops s2b_host_ops;
+int s2b_host_ops_build(const s2b_grid *grid, int family, double a, double sigma,
+                       const double *const *fields9, int order, s2b_host_ops **out);
+int s2b_host_ops_csr(const s2b_host_ops *h, int slot, s2b_csr *out);
+int s2b_host_ops_field(const s2b_host_ops *h, int which, const double **data, int *is_zero);
+int s2b_host_ops_destroy(s2b_host_ops *h);
+/* simulate_brownian (stochastics.cpp:76-101) on the host: values [M][steps+1]. */
+int s2b_host_simulate_brownian(double T, double dt_leb, size_t M, uint64_t seed,
+                               double *values_out);
+
 /* ---- Brownian paths ------------------------------------------------------------
  * Host mode: prefix values [M][steps+1] exactly as BrownianBatch::values (parity mode).
  * Philox mode: N(0, dt_leb) increments from Philox4x32-10 keyed by (seed, path_offset+m)

@@ -241,6 +241,55 @@ class Fields:
             pass
 
 
+class HostOps:
+    """Host-kept CommutatorSet + CoefficientFields from the C++ builder (no GPU needed):
+    the CSR the GPU operator is laid out from (operators.cpp:134-208 arithmetic)."""
+
+    def __init__(self, grid: GridSpec, family="langevin-constant", a=1.1,
+                 sigma=1.0 / np.sqrt(10.0), order=3, fields=None):
+        arr, keep = _fields_array(fields)
+        h = C.c_void_p()
+        _check(lib().s2b_host_ops_build(C.byref(grid.c()), FAMILIES[family], a, sigma, arr, order,
+                                        C.byref(h)))
+        self.h, self.grid, self.order = h, grid, order
+
+    def csr(self, slot):
+        s = SLOTS.index(slot) if isinstance(slot, str) else slot
+        m = _capi.Csr()
+        _check(lib().s2b_host_ops_csr(self.h, s, C.byref(m)))
+        if m.rows == 0:
+            return None
+        rp = np.ctypeslib.as_array(m.row_ptr, (m.rows + 1,)).astype(np.uint64).copy()
+        nnz = int(rp[-1])
+        ci = np.ctypeslib.as_array(m.col_idx, (nnz,)).copy() if nnz else np.zeros(0, np.int32)
+        v = np.ctypeslib.as_array(m.values, (nnz,)).copy() if nnz else np.zeros(0)
+        return rp, ci, v
+
+    def sources(self):
+        return [self.csr(s) for s in range(6)]
+
+    def field(self, name):
+        d = C.POINTER(C.c_double)()
+        z = C.c_int()
+        _check(lib().s2b_host_ops_field(self.h, FIELD_NAMES.index(name), C.byref(d), C.byref(z)))
+        return np.ctypeslib.as_array(d, (self.grid.dim(),)).copy(), bool(z.value)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().s2b_host_ops_destroy(self.h)
+        except Exception:
+            pass
+
+
+def simulate_brownian(T, dt_leb, M, seed) -> np.ndarray:
+    """Host BrownianBatch::values [M][steps+1] (the reference's xoshiro256++ stream)."""
+    steps = int(round(T / dt_leb))
+    out = np.empty((M, steps + 1))
+    _check(lib().s2b_host_simulate_brownian(T, dt_leb, M, seed, _dptr(out)))
+    return out
+
+
 def gaussian_datum(grid: GridSpec) -> np.ndarray:
     """phi = exp(-(x^2+v^2)/2) at the interior nodes, column-major (exact_langevin.cpp:29-39)."""
     out = np.empty(grid.dim())

@@ -70,6 +70,13 @@ SIGNATURES = {
     "s2b_fields_build": (C.c_int, [_VP, _P(Grid), C.c_int, C.c_double, C.c_double, _P(_VP)]),
     "s2b_fields_destroy": (C.c_int, [_VP]),
     "s2b_gaussian_datum": (C.c_int, [_P(Grid), _P(C.c_double)]),
+    "s2b_host_ops_build": (C.c_int, [_P(Grid), C.c_int, C.c_double, C.c_double,
+                                     _P(_P(C.c_double)), C.c_int, _P(_VP)]),
+    "s2b_host_ops_csr": (C.c_int, [_VP, C.c_int, _P(Csr)]),
+    "s2b_host_ops_field": (C.c_int, [_VP, C.c_int, _P(_P(C.c_double)), _P(C.c_int)]),
+    "s2b_host_ops_destroy": (C.c_int, [_VP]),
+    "s2b_host_simulate_brownian": (C.c_int, [C.c_double, C.c_double, C.c_size_t, C.c_uint64,
+                                             _P(C.c_double)]),
     "s2b_paths_create_host": (C.c_int, [_VP, C.c_double, C.c_size_t, C.c_size_t, C.c_uint64,
                                         _P(C.c_double), _P(_VP)]),
     "s2b_paths_create_philox": (C.c_int, [_VP, C.c_double, C.c_size_t, C.c_size_t, C.c_uint64,

@@ -240,6 +240,68 @@ int s2b_gaussian_datum(const s2b_grid* grid, double* out) {
     });
 }
 
+struct s2b_host_ops {
+    spde2d::GridSpec grid;
+    spde2d::CoefficientFields fields;
+    spde2d::CommutatorSet comms;
+};
+
+int s2b_host_ops_build(const s2b_grid* grid, int family, double a, double sigma, const double* const* fields9,
+                       int order, s2b_host_ops** out) {
+    return guard([&] {
+        need(grid, "grid");
+        need(out, "out");
+        auto* h = new s2b_host_ops();
+        try {
+            h->grid = grid_spec(grid);
+            h->fields = host_fields(grid, family, a, sigma, fields9);
+            h->comms = spde2d::precompute_commutators(spde2d::assemble_diffusion(h->fields, h->grid),
+                                                      spde2d::assemble_drift(h->fields, h->grid), order);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int s2b_host_ops_csr(const s2b_host_ops* h, int slot, s2b_csr* out) {
+    return guard([&] {
+        need(h, "host_ops");
+        need(out, "out");
+        const spde2d::SparseMatrix* all[6] = {&h->comms.B, &h->comms.A, &h->comms.A2,
+                                              &h->comms.BA, &h->comms.BAA, &h->comms.BAB};
+        if (slot < 0 || slot > 5) fail(S2B_ERR_CONFIG, "host_ops: slot out of range");
+        *out = csr_of(*all[slot]);
+    });
+}
+
+int s2b_host_ops_field(const s2b_host_ops* h, int which, const double** data, int* is_zero) {
+    return guard([&] {
+        need(h, "host_ops");
+        const spde2d::CoefficientFields& f = h->fields;
+        const spde2d::Field* all[9] = {&f.h, &f.fx, &f.fv, &f.gxx, &f.gxv, &f.gvv, &f.sig, &f.sigx, &f.sigv};
+        const bool z[9] = {f.zero_h, f.zero_fx, f.zero_fv, f.zero_gxx, f.zero_gxv, f.zero_gvv,
+                           f.zero_sig, f.zero_sigx, f.zero_sigv};
+        if (which < 0 || which > 8) fail(S2B_ERR_CONFIG, "host_ops: field out of range");
+        *data = all[which]->data().data();
+        *is_zero = z[which] ? 1 : 0;
+    });
+}
+
+int s2b_host_ops_destroy(s2b_host_ops* h) {
+    return guard([&] { delete h; });
+}
+
+int s2b_host_simulate_brownian(double T, double dt_leb, size_t M, uint64_t seed, double* values_out) {
+    return guard([&] {
+        need(values_out, "values_out");
+        const spde2d::BrownianBatch b = spde2d::simulate_brownian(T, dt_leb, M, seed);
+        for (size_t m = 0; m < M; ++m)
+            std::memcpy(values_out + m * (b.steps + 1), b.values[m].data(), (b.steps + 1) * sizeof(double));
+    });
+}
+
 int s2b_paths_create_host(s2b_context* ctx, double dt_leb, size_t steps, size_t M, uint64_t seed,
                           const double* values, s2b_paths** out) {
     return guard([&] {

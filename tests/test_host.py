@@ -1,0 +1,115 @@
+"""CPU tests of the host side: the C ABI library loads and exports every symbol the header
+declares, and the host-kept C++ builder (grid, CSR operators, commutators, xoshiro Brownian
+batch) is bitwise the reference's.  No GPU compute is called here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "spde2d_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(s2b_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(s2b):
+    from paper_2207_09776_b200 import _capi
+    L = _capi.lib()
+    decl = declared_symbols()
+    assert len(decl) > 40
+    missing = [s for s in decl if not hasattr(L, s)]
+    assert not missing, missing
+    # the Python binding covers the whole header too
+    assert sorted(set(decl) - set(_capi.SIGNATURES)) == []
+
+
+def test_library_has_no_oracle_dependency():
+    """The product .so must not link or embed the oracle/reference code."""
+    import subprocess
+    lib = os.path.join(ROOT, "paper_2207_09776_b200", "lib", "libspde2d_b200.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True).stdout
+    assert "ref_" not in " ".join(l.split()[-1] for l in out.splitlines() if l.strip())
+    assert "rs_" not in " ".join(l.split()[-1] for l in out.splitlines() if l.strip()).split("s2b")[0]
+    deps = subprocess.run(["ldd", lib], capture_output=True, text=True).stdout
+    assert "spde2d_ref" not in deps and "restate" not in deps
+
+
+@pytest.mark.parametrize("family,d,order", [
+    ("langevin-constant", 10, 3), ("langevin-constant", 50, 3), ("langevin-variable", 16, 3),
+    ("langevin-variable", 9, 2), ("langevin-constant", 5, 1), ("langevin-constant", 3, 3)])
+def test_host_builder_bitwise_vs_reference(ref, s2b, family, d, order):
+    g = s2b.GridSpec.square(d)
+    host = s2b.HostOps(g, family, order=order)
+    ops = ref.Ops(family, d, order=order)
+    for slot in ref.SLOTS:
+        a, b = host.csr(slot), ops.csr(slot)
+        if b is None:
+            assert a is None
+            continue
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), slot
+    for name in ref.FIELD_NAMES:
+        fa, za = host.field(name)
+        fb, zb = ops.field(name)
+        assert za == zb and np.array_equal(fa, fb)
+
+
+def test_host_builder_custom_fields_bitwise(ref, s2b):
+    d = 12
+    g = s2b.GridSpec.square(d)
+    x = g.nodes(0)
+    X, V = np.meshgrid(x, x, indexing="xy")
+    fields = {"h": (0.2 * np.cos(X)).ravel(), "fx": (-V).ravel(), "fv": (0.3 * np.sin(X)).ravel(),
+              "gxx": (0.05 + 0 * X).ravel(), "gxv": (0.02 * np.sin(X + V)).ravel(),
+              "gvv": (1.1 + 0.1 * np.cos(X)).ravel(), "sig": (0.1 * np.cos(V)).ravel(),
+              "sigx": (0.05 * np.sin(X)).ravel(), "sigv": (0.3 + 0 * X).ravel()}
+    host = s2b.HostOps(g, "fields", order=3, fields=fields)
+    ops = ref.Ops("fields", d, order=3, fields=fields)
+    for slot in ref.SLOTS:
+        for x_, y_ in zip(host.csr(slot), ops.csr(slot)):
+            assert np.array_equal(x_, y_), slot
+
+
+def test_host_brownian_bitwise_vs_reference(ref, s2b):
+    for seed in (1, 424242):
+        a = s2b.simulate_brownian(0.3, 1e-3, 7, seed)
+        b, _ = ref.simulate_brownian(0.3, 1e-3, 7, seed)
+        assert np.array_equal(a, b)
+    assert np.all(a[:, 0] == 0.0)
+
+
+def test_host_errors_mirror_reference(s2b):
+    g = s2b.GridSpec.square(8)
+    with pytest.raises(s2b.ConfigError):
+        s2b.HostOps(g, "langevin-constant", a=0.05, sigma=1.0)  # a - sigma^2 <= 0
+    with pytest.raises(s2b.ConfigError):
+        s2b.HostOps(g, "langevin-constant", order=4)
+    with pytest.raises(s2b.ConfigError):
+        s2b.simulate_brownian(1.0, 0.3, 4, 1)  # incommensurate
+    with pytest.raises(s2b.ConfigError):
+        s2b.simulate_brownian(1.0, 1e-3, 0, 1)
+    with pytest.raises(s2b.ConfigError):
+        s2b.HostOps(s2b.GridSpec(0, 4), "langevin-constant")
+
+
+def test_central_region_mirror(s2b, rs):
+    for d in (4, 20, 64, 256, 300):
+        for kappa in range(0, 6):
+            try:
+                want = rs.central_region(d, kappa)
+            except ValueError:
+                with pytest.raises(s2b.ConfigError):
+                    s2b.central_region(d, kappa)
+                continue
+            assert s2b.central_region(d, kappa) == want
+
+
+def test_gaussian_datum_bitwise(ref, s2b):
+    for d in (7, 16):
+        assert np.array_equal(s2b.gaussian_datum(s2b.GridSpec.square(d)),
+                              ref.Ops("langevin-constant", d, order=1).datum())
