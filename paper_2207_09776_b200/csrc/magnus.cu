@@ -35,38 +35,16 @@
 #include <map>
 #include <set>
 
-#include "s2b_internal.cuh"
+#include "magnus_common.cuh"
 
 namespace s2b {
 
+using namespace mg;
+
+int mg::tma_popcount(int variant) { return __builtin_popcountll(kVariants[variant].mask); }
+
 namespace {
 
-constexpr int kMaxTerms = 55;   // sparse.cpp:435
-constexpr int kStripRows = 32;  // output rows per work item (compressed kernel)
-constexpr int kStages = 4;      // TMA ring depth
-
-__host__ __device__ constexpr int box_bit(int dx, int dv) { return (dv + kBoxR) * kBoxW + (dx + kBoxR); }
-
-__device__ __forceinline__ int xclass(int i, int nx) {
-    return i == 0 ? 0 : (i == 1 ? 1 : (i == nx - 2 ? 3 : (i == nx - 1 ? 4 : 2)));
-}
-
-__device__ __forceinline__ unsigned long long abs_bits(double v) {
-    return static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFFFFFULL;
-}
-constexpr unsigned long long kInfBits = 0x7FF0000000000000ULL;
-
-__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
-    return a > b ? a : b;
-}
-
-__device__ __forceinline__ unsigned long long warp_umax(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
-// ---- per (path, window) functionals and logarithm weights ---------------------------
 // lebesgue_functionals (stochastics.cpp:121-141) + log_coefficients (magnus.cpp:26-40),
 // one thread per (path, window): all windows of all paths at once.
 __global__ void functionals_kernel(const double* __restrict__ values, size_t steps, size_t M,
@@ -106,14 +84,6 @@ __global__ void functionals_kernel(const double* __restrict__ values, size_t ste
 
 // Y value of one stencil bit at one row: MagnusLogBuilder::fill's fold (magnus.cpp:147-159),
 // 0.0 start, slots in order, zero coefficients skipped.
-struct OpView {
-    const int* pair_begin; // kBoxBits + 1
-    const int* pair_slot;
-    const double* w;
-    int nx, nv;
-    int compressed;
-};
-
 __device__ __forceinline__ double y_entry(const OpView& op, const double* c, int bit, int i, int j) {
     double y = 0.0;
     const int q0 = op.pair_begin[bit], q1 = op.pair_begin[bit + 1];
@@ -343,25 +313,6 @@ __global__ void swap_counts_kernel(int* cnt) {
 }
 
 // ---- term kernels --------------------------------------------------------------
-struct TermArgs {
-    OpView op;
-    const double* ctab; // [M][nwin][6]
-    int nwin;
-    const int* act;
-    const int* cnt; // cnt[0] = live paths this pass
-    const int* win;
-    const int* k;
-    const int* nseg;
-    const int* par;
-    double* T0;
-    double* T1;
-    double* S0;
-    double* S1;
-    unsigned long long* tn;
-    unsigned long long* sn;
-    int nstrips;
-    int8_t e2bit[kBoxBits];
-};
 
 // Generic kernel: one thread per (path, point); any stencil, full or compressed weights.
 __global__ void term_generic_kernel(TermArgs a, const int* __restrict__ bits, int nbits) {
@@ -423,305 +374,7 @@ __global__ void term_generic_kernel(TermArgs a, const int* __restrict__ bits, in
     }
 }
 
-// ---- TMA-fed compressed-stencil term kernel ----------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-        "@!P bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
-template <uint64_t MASK>
-struct MaskInfo {
-    static constexpr int count() {
-        int n = 0;
-        for (int b = 0; b < kBoxBits; ++b) n += (MASK >> b) & 1;
-        return n;
-    }
-    static constexpr int rank(int bit) {
-        int n = 0;
-        for (int b = 0; b < bit; ++b) n += (MASK >> b) & 1;
-        return n;
-    }
-    static constexpr bool has(int dx, int dv) { return (MASK >> box_bit(dx, dv)) & 1; }
-};
-
-// One work item = (live path, strip of kStripRows output rows).  Threads own two adjacent
-// x-points (i = 2t, 2t+1); rows stream through a TMA ring (input row r and accum row
-// r - KRV per stage), each thread keeps a (2KRV+1) x (2 NP) register window.
-template <int KRX, int KRV, uint64_t MASK>
-__global__ void __launch_bounds__(512) term_tma_kernel(TermArgs a) {
-    constexpr int H = KRX <= 2 ? 2 : 4;             // zero halo (doubles) on each side
-    constexpr int AOFF = (H - KRX) & ~1;            // first loaded smem index relative to 2t
-    constexpr int LAST = 1 + KRX + H;               // last needed smem index relative to 2t
-    constexpr int NP = (LAST - AOFF) / 2 + 1;       // 16-byte pairs loaded per row
-    constexpr int WROWS = 2 * KRV + 1;
-    constexpr int NBM = MaskInfo<MASK>::count();
-    constexpr int J = kStripRows;
-
-    const int nx = a.op.nx, nv = a.op.nv;
-    const size_t n = static_cast<size_t>(nx) * nv;
-    const int NT = blockDim.x;
-    const int RW = 2 * NT + 2 * H; // smem row width (doubles)
-    const int t = threadIdx.x;
-    const int i0 = 2 * t;
-
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-    double* rows = reinterpret_cast<double*>(smem_raw + 128);                // kStages x RW
-    double* srow = rows + kStages * RW;                                        // kStages x 2NT
-    double* Ys = srow + kStages * 2 * NT;                                      // J x 5 x NBM
-    __shared__ double c[6];
-    __shared__ unsigned long long red[2][16];
-
-    for (int q = t; q < kStages * RW; q += NT) rows[q] = 0.0;
-    if (t == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    const int clsA = xclass(i0, nx), clsB = xclass(i0 + 1, nx);
-    const bool validA = i0 < nx, validB = i0 + 1 < nx;
-    uint32_t gstep = 0; // running stage counter across work items (mbarrier phases)
-
-    const long long work = static_cast<long long>(a.cnt[0]) * a.nstrips;
-    for (long long wi = blockIdx.x; wi < work; wi += gridDim.x) {
-        const int p = a.act[wi / a.nstrips];
-        const int strip = static_cast<int>(wi % a.nstrips);
-        const int j0 = strip * J;
-        const int jend = min(j0 + J, nv);
-        const int kk = a.k[p];
-        const int par = a.par[p];
-        const double inv = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
-        const double* Sin = (par ? a.S1 : a.S0) + static_cast<size_t>(p) * n;
-        const double* in = kk == 1 ? Sin : (par ? a.T1 : a.T0) + static_cast<size_t>(p) * n;
-        double* Tout = (par ? a.T0 : a.T1) + static_cast<size_t>(p) * n;
-        double* Sout = (par ? a.S0 : a.S1) + static_cast<size_t>(p) * n;
-        const int nsteps = (jend - j0) + 2 * KRV;
-
-        // producer: stage s carries input row j0-KRV+s and accum row j0-2KRV+s
-        auto issue = [&](int s) {
-            const uint32_t g = gstep + s;
-            const int slot = g % kStages;
-            const int r = j0 - KRV + s;
-            const int ro = r - KRV;
-            uint32_t bytes = 0;
-            const bool has_in = r >= 0 && r < nv;
-            const bool has_s = s >= 2 * KRV && ro < jend;
-            if (has_in) bytes += nx * 8;
-            if (has_s) bytes += nx * 8;
-            if (bytes) {
-                mbar_expect_tx(&full[slot], bytes);
-                if (has_in) tma_row(rows + slot * RW + H, in + static_cast<size_t>(r) * nx, nx * 8, &full[slot]);
-                if (has_s) tma_row(srow + slot * 2 * NT, Sin + static_cast<size_t>(ro) * nx, nx * 8, &full[slot]);
-            } else {
-                mbar_arrive(&full[slot]);
-            }
-        };
-
-        __syncthreads(); // previous item fully consumed the ring and Ys
-        if (t == 0) {
-            for (int s = 0; s < kStages - 1 && s < nsteps; ++s) issue(s);
-        }
-        if (t < 6) c[t] = a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + t];
-        __syncthreads();
-        // rebuild Y for this strip: Ys[jj][cls][e] (fill fold, slot order, from 0.0)
-        for (int q = t; q < (jend - j0) * kClasses * NBM; q += NT) {
-            const int e = q % NBM;
-            const int cls = (q / NBM) % kClasses;
-            const int jj = q / (NBM * kClasses);
-            const int b = a.e2bit[e];
-            const int j = j0 + jj;
-            double y = 0.0;
-            const int q0 = a.op.pair_begin[b], q1 = a.op.pair_begin[b + 1];
-            for (int pq = q0; pq < q1; ++pq) {
-                const double cs = c[a.op.pair_slot[pq]];
-                if (cs == 0.0) continue;
-                y += cs * a.op.w[(static_cast<size_t>(pq) * nv + j) * kClasses + cls];
-            }
-            Ys[q] = y;
-        }
-        __syncthreads();
-
-        double win[WROWS][2 * NP];
-#pragma unroll
-        for (int r = 0; r < WROWS; ++r)
-#pragma unroll
-            for (int q = 0; q < 2 * NP; ++q) win[r][q] = 0.0;
-        unsigned long long tb = 0, sb = 0;
-
-        // steps are unrolled by WROWS so the register ring index is static
-        for (int base = 0; base < nsteps; base += WROWS) {
-#pragma unroll
-            for (int ph = 0; ph < WROWS; ++ph) {
-                const int s = base + ph;
-                if (s < nsteps) {
-                    if (t == 0 && s + kStages - 1 < nsteps) issue(s + kStages - 1);
-                    const uint32_t g = gstep + s;
-                    const int slot = g % kStages;
-                    mbar_wait(&full[slot], (g / kStages) & 1);
-                    const int r = j0 - KRV + s;
-                    // new input row into register row (s mod WROWS) == ph (base is a multiple)
-                    if (r >= 0 && r < nv) {
-                        const double2* src = reinterpret_cast<const double2*>(rows + slot * RW + i0 + AOFF);
-#pragma unroll
-                        for (int q = 0; q < NP; ++q) {
-                            const double2 v2 = src[q];
-                            win[ph][2 * q] = v2.x;
-                            win[ph][2 * q + 1] = v2.y;
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 2 * NP; ++q) win[ph][q] = 0.0;
-                    }
-                    const int jo = r - KRV; // output row
-                    if (s >= 2 * KRV && jo < jend) {
-                        const double2 sv = reinterpret_cast<const double2*>(srow + slot * 2 * NT)[t];
-                        const double* yA = Ys + ((jo - j0) * kClasses + clsA) * NBM;
-                        const double* yB = Ys + ((jo - j0) * kClasses + clsB) * NBM;
-                        double accA = 0.0, accB = 0.0;
-                        // ascending stencil offset == ascending DIA diagonal (sparse.cpp:412-423)
-#pragma unroll
-                        for (int dv = -KRV; dv <= KRV; ++dv) {
-                            // register row holding input row jo+dv: (s - KRV + dv) mod WROWS
-                            const int rr = ((ph - KRV + dv) % WROWS + WROWS) % WROWS;
-#pragma unroll
-                            for (int dx = -KRX; dx <= KRX; ++dx) {
-                                if (MaskInfo<MASK>::has(dx, dv)) {
-                                    const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
-                                    const int col = H + dx - AOFF;
-                                    const double wa = yA[e];
-                                    const double wb = yB[e];
-                                    accA += wa * win[rr][col];
-                                    accB += wb * win[rr][col + 1];
-                                }
-                            }
-                        }
-                        const size_t off = static_cast<size_t>(jo) * nx + i0;
-                        if (validA) {
-                            const double tA = accA * inv;
-                            const double sA = sv.x + tA;
-                            const double tB = accB * inv;
-                            const double sB = sv.y + tB;
-                            if (validB) {
-                                *reinterpret_cast<double2*>(Tout + off) = make_double2(tA, tB);
-                                *reinterpret_cast<double2*>(Sout + off) = make_double2(sA, sB);
-                                tb = umax64(tb, umax64(abs_bits(tA), abs_bits(tB)));
-                                sb = umax64(sb, umax64(abs_bits(sA), abs_bits(sB)));
-                            } else {
-                                Tout[off] = tA;
-                                Sout[off] = sA;
-                                tb = umax64(tb, abs_bits(tA));
-                                sb = umax64(sb, abs_bits(sA));
-                            }
-                        }
-                    }
-                    __syncthreads(); // slot consumed by every thread
-                }
-            }
-        }
-        gstep += nsteps;
-
-        tb = warp_umax(tb);
-        sb = warp_umax(sb);
-        if ((t & 31) == 0) {
-            red[0][t >> 5] = tb;
-            red[1][t >> 5] = sb;
-        }
-        __syncthreads();
-        if (t < 32) {
-            const int nw = (NT + 31) / 32;
-            unsigned long long t2 = t < nw ? red[0][t] : 0ULL;
-            unsigned long long s2 = t < nw ? red[1][t] : 0ULL;
-            t2 = warp_umax(t2);
-            s2 = warp_umax(s2);
-            if (t == 0) {
-                if (t2) atomicMax(&a.tn[p], t2);
-                if (s2) atomicMax(&a.sn[p], s2);
-            }
-        }
-    }
-}
-
-constexpr uint64_t mask_of(std::initializer_list<std::pair<int, int>> pts) {
-    uint64_t m = 0;
-    for (auto [dx, dv] : pts) m |= 1ULL << box_bit(dx, dv);
-    return m;
-}
-constexpr uint64_t box_mask(int rx, int rv) {
-    uint64_t m = 0;
-    for (int dv = -rv; dv <= rv; ++dv)
-        for (int dx = -rx; dx <= rx; ++dx) m |= 1ULL << box_bit(dx, dv);
-    return m;
-}
-// Union stencils of the Langevin families: orders 1, 2, 3.
-constexpr uint64_t kMask5 = mask_of({{0, 0}, {-1, 0}, {1, 0}, {0, -1}, {0, 1}});
-constexpr uint64_t kMask11 = kMask5 | mask_of({{0, -2}, {0, 2}, {-1, -1}, {1, -1}, {-1, 1}, {1, 1}});
-constexpr uint64_t kMask19 =
-    kMask11 | mask_of({{-1, -2}, {1, -2}, {-1, 2}, {1, 2}, {-2, -1}, {2, -1}, {-2, 1}, {2, 1}});
-constexpr uint64_t kBox22 = box_mask(2, 2);
-constexpr uint64_t kBox23 = box_mask(2, 3);
-constexpr uint64_t kBox33 = box_mask(3, 3);
-
-struct Variant {
-    uint64_t mask;
-    int rx, rv;
-};
-constexpr Variant kVariants[] = {
-    {0, 0, 0},        // 0: generic
-    {kMask5, 1, 1},   // 1
-    {kMask11, 1, 2},  // 2
-    {kMask19, 2, 2},  // 3
-    {kBox22, 2, 2},   // 4
-    {kBox23, 2, 3},   // 5
-    {kBox33, 3, 3},   // 6
-};
-
-template <int V>
-void launch_term_variant(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, size_t work) {
-    constexpr Variant v = kVariants[V];
-    auto kern = term_tma_kernel<v.rx, v.rv, v.mask>;
-    static int configured_device = -1;
-    static int blocks_per_sm = 1;
-    if (configured_device != ctx->device) {
-        S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured_device = ctx->device;
-    }
-    S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, nt, smem));
-    blocks_per_sm = std::max(1, blocks_per_sm);
-    const size_t cap = static_cast<size_t>(ctx->num_sms) * blocks_per_sm;
-    const int grid = static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
-    kern<<<grid, nt, smem, ctx->stream>>>(a);
-}
-
-int tma_popcount(int variant) { return __builtin_popcountll(kVariants[variant].mask); }
 
 } // namespace
 
@@ -984,20 +637,19 @@ void launch_term(MagnusSession& s) {
         const int grid = grid_for(s.ctx, s.M * blocks_per_path, bs);
         term_generic_kernel<<<grid, bs, 0, s.ctx->stream>>>(a, s.bits.p, s.nbits);
     } else {
-        const int nt = static_cast<int>(((s.op->nx / 2) + 31) / 32 * 32);
+        const int nye = kClasses * tma_popcount(variant);
+        const int nt = static_cast<int>((std::max<size_t>((s.op->nx + 1) / 2, nye) + 31) / 32 * 32);
         const int H = kVariants[variant].rx <= 2 ? 2 : 4;
         const size_t rw = 2 * static_cast<size_t>(nt) + 2 * H;
         const size_t smem = 128 + kStages * rw * 8 + kStages * 2 * static_cast<size_t>(nt) * 8 +
-                            static_cast<size_t>(kStripRows) * kClasses * tma_popcount(variant) * 8;
+                            (2 + 6) * static_cast<size_t>(nye) * 8;
         const size_t work = s.M * static_cast<size_t>(a.nstrips);
-        switch (variant) {
-        case 1: launch_term_variant<1>(s.ctx, a, nt, smem, work); break;
-        case 2: launch_term_variant<2>(s.ctx, a, nt, smem, work); break;
-        case 3: launch_term_variant<3>(s.ctx, a, nt, smem, work); break;
-        case 4: launch_term_variant<4>(s.ctx, a, nt, smem, work); break;
-        case 5: launch_term_variant<5>(s.ctx, a, nt, smem, work); break;
-        case 6: launch_term_variant<6>(s.ctx, a, nt, smem, work); break;
-        }
+        if (nt <= 128)
+            launch_term_nt128(s.ctx, variant, a, nt, smem, work);
+        else if (nt <= 256)
+            launch_term_nt256(s.ctx, variant, a, nt, smem, work);
+        else
+            launch_term_nt512(s.ctx, variant, a, nt, smem, work);
     }
     S2B_LAUNCHED(s.ctx);
     s.stats.term_launches += 1;

@@ -1,0 +1,163 @@
+// Shared by the Magnus pass-engine translation units (magnus.cu, term_nt*.cu).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <initializer_list>
+#include <utility>
+
+#include "s2b_internal.cuh"
+
+namespace s2b {
+namespace mg {
+
+constexpr int kMaxTerms = 55;   // sparse.cpp:435
+constexpr int kStripRows = 32;  // output rows per work item (compressed kernel)
+constexpr int kStages = 6;      // TMA ring depth
+
+__host__ __device__ constexpr int box_bit(int dx, int dv) { return (dv + kBoxR) * kBoxW + (dx + kBoxR); }
+
+__device__ __forceinline__ int xclass(int i, int nx) {
+    return i == 0 ? 0 : (i == 1 ? 1 : (i == nx - 2 ? 3 : (i == nx - 1 ? 4 : 2)));
+}
+
+__device__ __forceinline__ unsigned long long abs_bits(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFFFFFULL;
+}
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ULL;
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+    return a > b ? a : b;
+}
+
+__device__ __forceinline__ unsigned long long warp_umax(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+struct OpView {
+    const int* pair_begin; // kBoxBits + 1
+    const int* pair_slot;
+    const double* w;
+    int nx, nv;
+    int compressed;
+};
+
+struct TermArgs {
+    OpView op;
+    const double* ctab; // [M][nwin][6]
+    int nwin;
+    const int* act;
+    const int* cnt; // cnt[0] = live paths this pass
+    const int* win;
+    const int* k;
+    const int* nseg;
+    const int* par;
+    double* T0;
+    double* T1;
+    double* S0;
+    double* S1;
+    unsigned long long* tn;
+    unsigned long long* sn;
+    int nstrips;
+    int8_t e2bit[kBoxBits];
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <uint64_t MASK>
+struct MaskInfo {
+    static constexpr int count() {
+        int n = 0;
+        for (int b = 0; b < kBoxBits; ++b) n += (MASK >> b) & 1;
+        return n;
+    }
+    static constexpr int rank(int bit) {
+        int n = 0;
+        for (int b = 0; b < bit; ++b) n += (MASK >> b) & 1;
+        return n;
+    }
+    static constexpr bool has(int dx, int dv) { return (MASK >> box_bit(dx, dv)) & 1; }
+};
+
+// One work item = (live path, strip of kStripRows output rows).  Threads own two adjacent
+// x-points (i = 2t, 2t+1).  Rows stream through a kStages-deep TMA ring (stage s carries
+// input row j0-KRV+s and accum row j0-2KRV+s); each thread keeps a (2KRV+1)-row register
+// window of its x-neighbourhood.  The Y values of the next output row (5 x-classes x the
+// mask's stencil points) are folded from the compressed weights one step ahead, by the
+// threads that own those entries, into a double-buffered shared row.  Warps without an
+// x-boundary point read one Y set for both of their points.
+constexpr uint64_t mask_of(std::initializer_list<std::pair<int, int>> pts) {
+    uint64_t m = 0;
+    for (auto [dx, dv] : pts) m |= 1ULL << box_bit(dx, dv);
+    return m;
+}
+constexpr uint64_t box_mask(int rx, int rv) {
+    uint64_t m = 0;
+    for (int dv = -rv; dv <= rv; ++dv)
+        for (int dx = -rx; dx <= rx; ++dx) m |= 1ULL << box_bit(dx, dv);
+    return m;
+}
+// Union stencils of the Langevin families: orders 1, 2, 3.
+constexpr uint64_t kMask5 = mask_of({{0, 0}, {-1, 0}, {1, 0}, {0, -1}, {0, 1}});
+constexpr uint64_t kMask11 = kMask5 | mask_of({{0, -2}, {0, 2}, {-1, -1}, {1, -1}, {-1, 1}, {1, 1}});
+constexpr uint64_t kMask19 =
+    kMask11 | mask_of({{-1, -2}, {1, -2}, {-1, 2}, {1, 2}, {-2, -1}, {2, -1}, {-2, 1}, {2, 1}});
+constexpr uint64_t kBox22 = box_mask(2, 2);
+constexpr uint64_t kBox23 = box_mask(2, 3);
+constexpr uint64_t kBox33 = box_mask(3, 3);
+
+struct Variant {
+    uint64_t mask;
+    int rx, rv;
+};
+constexpr Variant kVariants[] = {
+    {0, 0, 0},        // 0: generic
+    {kMask5, 1, 1},   // 1
+    {kMask11, 1, 2},  // 2
+    {kMask19, 2, 2},  // 3
+    {kBox22, 2, 2},   // 4
+    {kBox23, 2, 3},   // 5
+    {kBox33, 3, 3},   // 6
+};
+
+// Block-size classes: (max threads, min resident blocks) -> register budget.
+int tma_popcount(int variant);
+// term_tma_kernel launchers, one translation unit per block-size class
+void launch_term_nt128(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
+void launch_term_nt256(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
+void launch_term_nt512(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
+
+} // namespace mg
+} // namespace s2b

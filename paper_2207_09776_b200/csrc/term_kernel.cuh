@@ -1,0 +1,279 @@
+// The TMA-fed compressed-stencil Taylor-term kernel (see magnus.cu for the engine).
+#pragma once
+
+#include "magnus_common.cuh"
+
+namespace s2b {
+namespace mg {
+
+template <int KRX, int KRV, uint64_t MASK, int NTMAX, int MINB>
+__global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
+    constexpr int H = KRX <= 2 ? 2 : 4;             // zero halo (doubles) on each side
+    constexpr int AOFF = (H - KRX) & ~1;            // first loaded smem index relative to 2t
+    constexpr int LAST = 1 + KRX + H;               // last needed smem index relative to 2t
+    constexpr int NP = (LAST - AOFF) / 2 + 1;       // 16-byte pairs loaded per row
+    constexpr int WROWS = 2 * KRV + 1;
+    constexpr int NBM = MaskInfo<MASK>::count();
+    constexpr int NYE = kClasses * NBM;             // Y entries of one row
+    constexpr int J = kStripRows;
+
+    const int nx = a.op.nx, nv = a.op.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+    const int NT = blockDim.x;
+    const int RW = 2 * NT + 2 * H; // smem row width (doubles)
+    const int t = threadIdx.x;
+    const int i0 = 2 * t;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    double* rows = reinterpret_cast<double*>(smem_raw + 128); // kStages x RW
+    double* srow = rows + kStages * RW;                       // kStages x 2NT
+    double* Ys = srow + kStages * 2 * NT;                     // 2 x NYE
+    __shared__ double c[6];
+    __shared__ unsigned long long red[2][32];
+
+    for (int q = t; q < kStages * RW; q += NT) rows[q] = 0.0;
+    if (t == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int clsA = xclass(i0, nx), clsB = xclass(i0 + 1, nx);
+    const bool validA = i0 < nx, validB = i0 + 1 < nx;
+    const bool wfast = __all_sync(0xffffffffu, clsA == 2 && clsB == 2);
+    uint32_t gstep = 0; // running stage counter across work items (mbarrier phases)
+
+    // Y entry owned by this thread (q = t < NYE; the launch makes NT >= NYE): the row's fold
+    // over its source pairs (MagnusLogBuilder::fill order: slots ascending, from 0.0).  The
+    // weights of the next row are loaded one step ahead into registers; the pair
+    // coefficients of the current work item sit in shared memory (cq[k][q]).
+    constexpr int kMaxPairs = 6;
+    double* cq = Ys + 2 * NYE; // kMaxPairs x NYE
+    const bool owner = t < NYE;
+    int own_cls = 0, own_q0 = 0, own_np = 0;
+    if (owner) {
+        const int bit = a.e2bit[t % NBM];
+        own_cls = t / NBM;
+        own_q0 = __ldg(a.op.pair_begin + bit);
+        own_np = __ldg(a.op.pair_begin + bit + 1) - own_q0;
+    }
+    double own_w[kMaxPairs];
+    auto load_w = [&](int j) {
+#pragma unroll
+        for (int k = 0; k < kMaxPairs; ++k)
+            if (k < own_np)
+                own_w[k] = __ldg(a.op.w + (static_cast<size_t>(own_q0 + k) * nv + j) * kClasses + own_cls);
+    };
+    auto fold_y = [&](int b) {
+        if (owner) {
+            double y = 0.0;
+#pragma unroll
+            for (int k = 0; k < kMaxPairs; ++k) {
+                if (k < own_np) {
+                    const double cs = cq[k * NYE + t];
+                    if (cs != 0.0) y += cs * own_w[k];
+                }
+            }
+            Ys[b * NYE + t] = y;
+        }
+    };
+
+    const long long work = static_cast<long long>(a.cnt[0]) * a.nstrips;
+    for (long long wi = blockIdx.x; wi < work; wi += gridDim.x) {
+        const int p = a.act[wi / a.nstrips];
+        const int strip = static_cast<int>(wi % a.nstrips);
+        const int j0 = strip * J;
+        const int jend = min(j0 + J, nv);
+        const int kk = a.k[p];
+        const int par = a.par[p];
+        const double inv = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
+        const double* Sin = (par ? a.S1 : a.S0) + static_cast<size_t>(p) * n;
+        const double* in = kk == 1 ? Sin : (par ? a.T1 : a.T0) + static_cast<size_t>(p) * n;
+        double* Tout = (par ? a.T0 : a.T1) + static_cast<size_t>(p) * n;
+        double* Sout = (par ? a.S0 : a.S1) + static_cast<size_t>(p) * n;
+        const int nsteps = (jend - j0) + 2 * KRV;
+
+        auto issue = [&](int s) {
+            const uint32_t g = gstep + s;
+            const int slot = g % kStages;
+            const int r = j0 - KRV + s;
+            const int ro = r - KRV;
+            uint32_t bytes = 0;
+            const bool has_in = r >= 0 && r < nv;
+            const bool has_s = s >= 2 * KRV && ro < jend;
+            if (has_in) bytes += nx * 8;
+            if (has_s) bytes += nx * 8;
+            if (bytes) {
+                mbar_expect_tx(&full[slot], bytes);
+                if (has_in) tma_row(rows + slot * RW + H, in + static_cast<size_t>(r) * nx, nx * 8, &full[slot]);
+                if (has_s) tma_row(srow + slot * 2 * NT, Sin + static_cast<size_t>(ro) * nx, nx * 8, &full[slot]);
+            } else {
+                mbar_arrive(&full[slot]);
+            }
+        };
+
+        __syncthreads(); // previous item fully consumed the ring and the Y rows
+        if (t == 0) {
+            for (int s = 0; s < kStages - 1 && s < nsteps; ++s) issue(s);
+        }
+        if (t < 6) c[t] = a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + t];
+        __syncthreads();
+        if (owner)
+            for (int k = 0; k < own_np; ++k) cq[k * NYE + t] = c[__ldg(a.op.pair_slot + own_q0 + k)];
+        load_w(j0);
+        __syncthreads();
+
+        double win[WROWS][2 * NP];
+#pragma unroll
+        for (int r = 0; r < WROWS; ++r)
+#pragma unroll
+            for (int q = 0; q < 2 * NP; ++q) win[r][q] = 0.0;
+        unsigned long long tb = 0, sb = 0;
+
+        for (int base = 0; base < nsteps; base += WROWS) {
+#pragma unroll
+            for (int ph = 0; ph < WROWS; ++ph) {
+                const int s = base + ph;
+                if (s < nsteps) {
+                    if (t == 0 && s + kStages - 1 < nsteps) issue(s + kStages - 1);
+                    const int jn = j0 - 2 * KRV + s + 1; // output row of the next step
+                    if (jn >= j0 && jn < jend) {
+                        fold_y(jn & 1);
+                        if (jn + 1 < jend) load_w(jn + 1);
+                    }
+                    const uint32_t g = gstep + s;
+                    const int slot = g % kStages;
+                    mbar_wait(&full[slot], (g / kStages) & 1);
+                    const int r = j0 - KRV + s;
+                    if (r >= 0 && r < nv) {
+                        const double2* src = reinterpret_cast<const double2*>(rows + slot * RW + i0 + AOFF);
+#pragma unroll
+                        for (int q = 0; q < NP; ++q) {
+                            const double2 v2 = src[q];
+                            win[ph][2 * q] = v2.x;
+                            win[ph][2 * q + 1] = v2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 2 * NP; ++q) win[ph][q] = 0.0;
+                    }
+                    const int jo = r - KRV; // output row of this step
+                    if (s >= 2 * KRV && jo < jend) {
+                        const double2 sv = reinterpret_cast<const double2*>(srow + slot * 2 * NT)[t];
+                        const double* yrow = Ys + (jo & 1) * NYE;
+                        double accA = 0.0, accB = 0.0;
+                        // ascending stencil offset == ascending DIA diagonal (sparse.cpp:412-423)
+                        if (wfast) {
+                            const double* y = yrow + 2 * NBM;
+#pragma unroll
+                            for (int dv = -KRV; dv <= KRV; ++dv) {
+                                const int rr = ((ph - KRV + dv) % WROWS + WROWS) % WROWS;
+#pragma unroll
+                                for (int dx = -KRX; dx <= KRX; ++dx) {
+                                    if (MaskInfo<MASK>::has(dx, dv)) {
+                                        const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
+                                        const int col = H + dx - AOFF;
+                                        const double w = y[e];
+                                        accA += w * win[rr][col];
+                                        accB += w * win[rr][col + 1];
+                                    }
+                                }
+                            }
+                        } else {
+                            const double* yA = yrow + clsA * NBM;
+                            const double* yB = yrow + clsB * NBM;
+#pragma unroll
+                            for (int dv = -KRV; dv <= KRV; ++dv) {
+                                const int rr = ((ph - KRV + dv) % WROWS + WROWS) % WROWS;
+#pragma unroll
+                                for (int dx = -KRX; dx <= KRX; ++dx) {
+                                    if (MaskInfo<MASK>::has(dx, dv)) {
+                                        const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
+                                        const int col = H + dx - AOFF;
+                                        accA += yA[e] * win[rr][col];
+                                        accB += yB[e] * win[rr][col + 1];
+                                    }
+                                }
+                            }
+                        }
+                        const size_t off = static_cast<size_t>(jo) * nx + i0;
+                        if (validA) {
+                            const double tA = accA * inv;
+                            const double sA = sv.x + tA;
+                            const double tB = accB * inv;
+                            const double sB = sv.y + tB;
+                            if (validB) {
+                                *reinterpret_cast<double2*>(Tout + off) = make_double2(tA, tB);
+                                *reinterpret_cast<double2*>(Sout + off) = make_double2(sA, sB);
+                                tb = umax64(tb, umax64(abs_bits(tA), abs_bits(tB)));
+                                sb = umax64(sb, umax64(abs_bits(sA), abs_bits(sB)));
+                            } else {
+                                Tout[off] = tA;
+                                Sout[off] = sA;
+                                tb = umax64(tb, abs_bits(tA));
+                                sb = umax64(sb, abs_bits(sA));
+                            }
+                        }
+                    }
+                    __syncthreads(); // ring slot and Y row consumed by every thread
+                }
+            }
+        }
+        gstep += nsteps;
+
+        tb = warp_umax(tb);
+        sb = warp_umax(sb);
+        if ((t & 31) == 0) {
+            red[0][t >> 5] = tb;
+            red[1][t >> 5] = sb;
+        }
+        __syncthreads();
+        if (t < 32) {
+            const int nw = (NT + 31) / 32;
+            unsigned long long t2 = t < nw ? red[0][t] : 0ULL;
+            unsigned long long s2 = t < nw ? red[1][t] : 0ULL;
+            t2 = warp_umax(t2);
+            s2 = warp_umax(s2);
+            if (t == 0) {
+                if (t2) atomicMax(&a.tn[p], t2);
+                if (s2) atomicMax(&a.sn[p], s2);
+            }
+        }
+    }
+}
+
+template <int NTMAX> struct NtClass;
+template <> struct NtClass<128> { static constexpr int minb = 4; };
+template <> struct NtClass<256> { static constexpr int minb = 2; };
+template <> struct NtClass<512> { static constexpr int minb = 1; };
+
+template <int V, int NTMAX>
+void launch_term_nt(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, size_t work) {
+    constexpr Variant v = kVariants[V];
+    auto kern = term_tma_kernel<v.rx, v.rv, v.mask, NTMAX, NtClass<NTMAX>::minb>;
+    static int configured_device = -1;
+    if (configured_device != ctx->device) {
+        S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured_device = ctx->device;
+    }
+    int blocks_per_sm = 1;
+    S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, nt, smem));
+    blocks_per_sm = std::max(1, blocks_per_sm);
+    const size_t cap = static_cast<size_t>(ctx->num_sms) * blocks_per_sm;
+    const int grid = static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
+    kern<<<grid, nt, smem, ctx->stream>>>(a);
+}
+
+template <int V>
+inline void launch_term_variant_unused(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, size_t work) {
+    if (nt <= 128)
+        launch_term_nt<V, 128>(ctx, a, nt, smem, work);
+    else if (nt <= 256)
+        launch_term_nt<V, 256>(ctx, a, nt, smem, work);
+    else
+        launch_term_nt<V, 512>(ctx, a, nt, smem, work);
+}
+
+} // namespace mg
+} // namespace s2b

@@ -1,0 +1,20 @@
+// term_tma_kernel instantiations for blocks of up to 512 threads.
+#include "term_kernel.cuh"
+
+namespace s2b {
+namespace mg {
+
+void launch_term_nt512(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work) {
+    switch (variant) {
+    case 1: launch_term_nt<1, 512>(ctx, a, nt, smem, work); break;
+    case 2: launch_term_nt<2, 512>(ctx, a, nt, smem, work); break;
+    case 3: launch_term_nt<3, 512>(ctx, a, nt, smem, work); break;
+    case 4: launch_term_nt<4, 512>(ctx, a, nt, smem, work); break;
+    case 5: launch_term_nt<5, 512>(ctx, a, nt, smem, work); break;
+    case 6: launch_term_nt<6, 512>(ctx, a, nt, smem, work); break;
+    default: fail(S2B_ERR_RUNTIME, "term kernel: unknown variant");
+    }
+}
+
+} // namespace mg
+} // namespace s2b
