@@ -487,13 +487,38 @@ s2b_operator* make_operator(s2b_context* ctx, const s2b_grid* grid, int order,
 
     // kernel variant: compressed weights, even nx (16-byte rows), nx <= 1024, mask fits
     op->variant = 0;
-    if (comp && nx % 2 == 0 && nx <= 1024) {
+    int max_pairs = 0;
+    for (int b = 0; b < kBoxBits; ++b) max_pairs = std::max(max_pairs, op->pair_begin[b + 1] - op->pair_begin[b]);
+    if (comp && nx % 2 == 0 && nx >= 6 && nx <= 1024 && max_pairs <= kPairSlots) {
         for (int v = 1; v < static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0])); ++v) {
             if ((op->union_mask & ~kVariants[v].mask) == 0) {
                 op->variant = v;
                 break;
             }
         }
+    }
+    if (op->variant) {
+        // entry-major weights for the TMA kernel: q = cls * NBM + e over the variant's mask
+        std::vector<int> e2bit;
+        for (int b = 0; b < kBoxBits; ++b)
+            if ((kVariants[op->variant].mask >> b) & 1) e2bit.push_back(b);
+        const size_t nbm = e2bit.size(), nye = kClasses * nbm;
+        std::vector<double> wt(nv * nye * kPairSlots, 0.0);
+        std::vector<int> eslot(nye * kPairSlots, -1);
+        for (int cls = 0; cls < kClasses; ++cls)
+            for (size_t e = 0; e < nbm; ++e) {
+                const size_t q = cls * nbm + e;
+                const int b = e2bit[e];
+                for (int pq = op->pair_begin[b], k = 0; pq < op->pair_begin[b + 1]; ++pq, ++k) {
+                    eslot[q * kPairSlots + k] = op->pair_slot[pq];
+                    for (size_t j = 0; j < nv; ++j)
+                        wt[(j * nye + q) * kPairSlots + k] = hw[(static_cast<size_t>(pq) * nv + j) * kClasses + cls];
+                }
+            }
+        op->d_wt.alloc(wt.size());
+        op->d_eslot.alloc(eslot.size());
+        S2B_CUDA(cudaMemcpy(op->d_wt.p, wt.data(), wt.size() * sizeof(double), cudaMemcpyHostToDevice));
+        S2B_CUDA(cudaMemcpy(op->d_eslot.p, eslot.data(), eslot.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     return op;
 }
@@ -615,6 +640,8 @@ TermArgs term_args(MagnusSession& s) {
     a.tn = s.tn.p;
     a.sn = s.sn.p;
     a.nstrips = static_cast<int>((s.op->nv + kStripRows - 1) / kStripRows);
+    a.wt = s.op->d_wt.p;
+    a.eslot = s.op->d_eslot.p;
     const uint64_t mask = kVariants[s.op->variant].mask;
     int e = 0;
     for (int b = 0; b < kBoxBits; ++b)
@@ -641,8 +668,9 @@ void launch_term(MagnusSession& s) {
         const int nt = static_cast<int>((std::max<size_t>((s.op->nx + 1) / 2, nye) + 31) / 32 * 32);
         const int H = kVariants[variant].rx <= 2 ? 2 : 4;
         const size_t rw = 2 * static_cast<size_t>(nt) + 2 * H;
-        const size_t smem = 128 + kStages * rw * 8 + kStages * 2 * static_cast<size_t>(nt) * 8 +
-                            (2 + 6) * static_cast<size_t>(nye) * 8;
+        const size_t smem = 128 + kStages * (s.op->nx + 2 * H) * 8 + kStages * s.op->nx * 8 +
+                            (2 + kPairSlots) * static_cast<size_t>(nye) * 8;
+        (void)rw;
         const size_t work = s.M * static_cast<size_t>(a.nstrips);
         if (nt <= 128)
             launch_term_nt128(s.ctx, variant, a, nt, smem, work);

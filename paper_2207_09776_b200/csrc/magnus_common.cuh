@@ -13,7 +13,7 @@ namespace mg {
 
 constexpr int kMaxTerms = 55;   // sparse.cpp:435
 constexpr int kStripRows = 32;  // output rows per work item (compressed kernel)
-constexpr int kStages = 6;      // TMA ring depth
+constexpr int kStages = 8;      // TMA ring depth (power of two)
 
 __host__ __device__ constexpr int box_bit(int dx, int dv) { return (dv + kBoxR) * kBoxW + (dx + kBoxR); }
 
@@ -62,7 +62,13 @@ struct TermArgs {
     unsigned long long* sn;
     int nstrips;
     int8_t e2bit[kBoxBits];
+    // entry-major weights of the kernel's mask: wt[(j * NYE + q) * kPairSlots + k] is the
+    // k-th source weight (slot order) of Y entry q = cls * NBM + e at row j, zero-padded;
+    // eslot[q * kPairSlots + k] is its CommutatorSet slot, -1 for padding.
+    const double* wt;
+    const int* eslot;
 };
+constexpr int kPairSlots = 6;
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

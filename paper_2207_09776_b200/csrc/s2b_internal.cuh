@@ -92,6 +92,8 @@ struct s2b_operator {
     std::vector<int> pair_slot;  // npairs
     int npairs = 0;
     s2b::DevBuf<int> d_pair_begin, d_pair_slot;
+    s2b::DevBuf<double> d_wt; // entry-major weights of the TMA kernel variant
+    s2b::DevBuf<int> d_eslot;
     // compressed: W[pair][j][cls]; full: W[pair][row]
     s2b::DevBuf<double> d_w;
     double dx_delta = 0.0, dv_delta = 0.0;

@@ -6,29 +6,40 @@
 namespace s2b {
 namespace mg {
 
+// One work item = (live path, strip of kStripRows output rows).
+//
+// Thread -> points: thread t < (nx-4)/2 owns the interior x-points 2t+2, 2t+3; the next two
+// threads own the x-boundary pairs {0, 1} and {nx-2, nx-1}, so every warp but the last reads
+// ONE interior Y set for both of its points.  Rows stream through a kStages-deep TMA ring
+// (stage s carries input row j0-KRV+s and accum row j0-2KRV+s); each thread keeps a
+// (2KRV+1)-row register window of its x-neighbourhood.  The Y values of the next output row
+// (5 x-classes x the mask's stencil points) are folded one step ahead by their owner threads
+// (thread q < NYE) from entry-major weights loaded one step earlier into registers.
 template <int KRX, int KRV, uint64_t MASK, int NTMAX, int MINB>
 __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     constexpr int H = KRX <= 2 ? 2 : 4;             // zero halo (doubles) on each side
-    constexpr int AOFF = (H - KRX) & ~1;            // first loaded smem index relative to 2t
-    constexpr int LAST = 1 + KRX + H;               // last needed smem index relative to 2t
+    constexpr int AOFF = (H - KRX) & ~1;            // first loaded smem index relative to p0
+    constexpr int LAST = 1 + KRX + H;               // last needed smem index relative to p0
     constexpr int NP = (LAST - AOFF) / 2 + 1;       // 16-byte pairs loaded per row
     constexpr int WROWS = 2 * KRV + 1;
     constexpr int NBM = MaskInfo<MASK>::count();
     constexpr int NYE = kClasses * NBM;             // Y entries of one row
     constexpr int J = kStripRows;
+    constexpr int KP = kPairSlots;
 
     const int nx = a.op.nx, nv = a.op.nv;
-    const size_t n = static_cast<size_t>(nx) * nv;
+    const int n = nx * nv;
     const int NT = blockDim.x;
-    const int RW = 2 * NT + 2 * H; // smem row width (doubles)
+    const int RW = nx + 2 * H; // smem row width (doubles)
     const int t = threadIdx.x;
-    const int i0 = 2 * t;
+    const int nint = (nx - 4) / 2; // threads owning interior pairs
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     double* rows = reinterpret_cast<double*>(smem_raw + 128); // kStages x RW
-    double* srow = rows + kStages * RW;                       // kStages x 2NT
-    double* Ys = srow + kStages * 2 * NT;                     // 2 x NYE
+    double* srow = rows + kStages * RW;                       // kStages x nx
+    double* Ys = srow + kStages * nx;                         // 2 x NYE
+    double* cq = Ys + 2 * NYE;                                // KP x NYE
     __shared__ double c[6];
     __shared__ unsigned long long red[2][32];
 
@@ -39,46 +50,42 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     }
     __syncthreads();
 
-    const int clsA = xclass(i0, nx), clsB = xclass(i0 + 1, nx);
-    const bool validA = i0 < nx, validB = i0 + 1 < nx;
-    const bool wfast = __all_sync(0xffffffffu, clsA == 2 && clsB == 2);
-    uint32_t gstep = 0; // running stage counter across work items (mbarrier phases)
+    // this thread's two x-points p0, p0+1 and their classes
+    const bool active = t < nint + 2;
+    const int p0 = t < nint ? 2 * t + 2 : (t == nint ? 0 : nx - 2);
+    const int clsA = t < nint ? 2 : (t == nint ? 0 : 3);
+    const int clsB = t < nint ? 2 : (t == nint ? 1 : 4);
+    const bool wfast = __all_sync(0xffffffffu, t < nint || !active);
 
-    // Y entry owned by this thread (q = t < NYE; the launch makes NT >= NYE): the row's fold
-    // over its source pairs (MagnusLogBuilder::fill order: slots ascending, from 0.0).  The
-    // weights of the next row are loaded one step ahead into registers; the pair
-    // coefficients of the current work item sit in shared memory (cq[k][q]).
-    constexpr int kMaxPairs = 6;
-    double* cq = Ys + 2 * NYE; // kMaxPairs x NYE
+    // Y entry owned by this thread (q = t < NYE; the launch makes NT >= NYE)
     const bool owner = t < NYE;
-    int own_cls = 0, own_q0 = 0, own_np = 0;
-    if (owner) {
-        const int bit = a.e2bit[t % NBM];
-        own_cls = t / NBM;
-        own_q0 = __ldg(a.op.pair_begin + bit);
-        own_np = __ldg(a.op.pair_begin + bit + 1) - own_q0;
-    }
-    double own_w[kMaxPairs];
+    double own_w[KP];
+    const double* wrow = a.wt + (owner ? t * KP : 0);
     auto load_w = [&](int j) {
+        if (owner) {
+            const double2* src = reinterpret_cast<const double2*>(wrow + static_cast<size_t>(j) * NYE * KP);
 #pragma unroll
-        for (int k = 0; k < kMaxPairs; ++k)
-            if (k < own_np)
-                own_w[k] = __ldg(a.op.w + (static_cast<size_t>(own_q0 + k) * nv + j) * kClasses + own_cls);
+            for (int k = 0; k < KP / 2; ++k) {
+                const double2 v = __ldg(src + k);
+                own_w[2 * k] = v.x;
+                own_w[2 * k + 1] = v.y;
+            }
+        }
     };
+    // MagnusLogBuilder::fill fold: slots ascending from 0.0, zero coefficients skipped
     auto fold_y = [&](int b) {
         if (owner) {
             double y = 0.0;
 #pragma unroll
-            for (int k = 0; k < kMaxPairs; ++k) {
-                if (k < own_np) {
-                    const double cs = cq[k * NYE + t];
-                    if (cs != 0.0) y += cs * own_w[k];
-                }
+            for (int k = 0; k < KP; ++k) {
+                const double cs = cq[k * NYE + t];
+                if (cs != 0.0) y += cs * own_w[k];
             }
             Ys[b * NYE + t] = y;
         }
     };
 
+    uint32_t gstep = 0; // running stage counter across work items (mbarrier phases)
     const long long work = static_cast<long long>(a.cnt[0]) * a.nstrips;
     for (long long wi = blockIdx.x; wi < work; wi += gridDim.x) {
         const int p = a.act[wi / a.nstrips];
@@ -88,15 +95,15 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
         const int kk = a.k[p];
         const int par = a.par[p];
         const double inv = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
-        const double* Sin = (par ? a.S1 : a.S0) + static_cast<size_t>(p) * n;
-        const double* in = kk == 1 ? Sin : (par ? a.T1 : a.T0) + static_cast<size_t>(p) * n;
-        double* Tout = (par ? a.T0 : a.T1) + static_cast<size_t>(p) * n;
-        double* Sout = (par ? a.S0 : a.S1) + static_cast<size_t>(p) * n;
+        const size_t pbase = static_cast<size_t>(p) * n;
+        const double* Sin = (par ? a.S1 : a.S0) + pbase;
+        const double* in = kk == 1 ? Sin : (par ? a.T1 : a.T0) + pbase;
+        double* Tout = (par ? a.T0 : a.T1) + pbase;
+        double* Sout = (par ? a.S0 : a.S1) + pbase;
         const int nsteps = (jend - j0) + 2 * KRV;
 
         auto issue = [&](int s) {
-            const uint32_t g = gstep + s;
-            const int slot = g % kStages;
+            const uint32_t slot = (gstep + s) & (kStages - 1);
             const int r = j0 - KRV + s;
             const int ro = r - KRV;
             uint32_t bytes = 0;
@@ -106,8 +113,8 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
             if (has_s) bytes += nx * 8;
             if (bytes) {
                 mbar_expect_tx(&full[slot], bytes);
-                if (has_in) tma_row(rows + slot * RW + H, in + static_cast<size_t>(r) * nx, nx * 8, &full[slot]);
-                if (has_s) tma_row(srow + slot * 2 * NT, Sin + static_cast<size_t>(ro) * nx, nx * 8, &full[slot]);
+                if (has_in) tma_row(rows + slot * RW + H, in + r * nx, nx * 8, &full[slot]);
+                if (has_s) tma_row(srow + slot * nx, Sin + ro * nx, nx * 8, &full[slot]);
             } else {
                 mbar_arrive(&full[slot]);
             }
@@ -119,8 +126,13 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
         }
         if (t < 6) c[t] = a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + t];
         __syncthreads();
-        if (owner)
-            for (int k = 0; k < own_np; ++k) cq[k * NYE + t] = c[__ldg(a.op.pair_slot + own_q0 + k)];
+        if (owner) {
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const int sl = __ldg(a.eslot + t * KP + k);
+                cq[k * NYE + t] = sl >= 0 ? c[sl] : 0.0;
+            }
+        }
         load_w(j0);
         __syncthreads();
 
@@ -143,11 +155,11 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                         if (jn + 1 < jend) load_w(jn + 1);
                     }
                     const uint32_t g = gstep + s;
-                    const int slot = g % kStages;
+                    const uint32_t slot = g & (kStages - 1);
                     mbar_wait(&full[slot], (g / kStages) & 1);
                     const int r = j0 - KRV + s;
                     if (r >= 0 && r < nv) {
-                        const double2* src = reinterpret_cast<const double2*>(rows + slot * RW + i0 + AOFF);
+                        const double2* src = reinterpret_cast<const double2*>(rows + slot * RW + p0 + AOFF);
 #pragma unroll
                         for (int q = 0; q < NP; ++q) {
                             const double2 v2 = src[q];
@@ -159,8 +171,8 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                         for (int q = 0; q < 2 * NP; ++q) win[ph][q] = 0.0;
                     }
                     const int jo = r - KRV; // output row of this step
-                    if (s >= 2 * KRV && jo < jend) {
-                        const double2 sv = reinterpret_cast<const double2*>(srow + slot * 2 * NT)[t];
+                    if (s >= 2 * KRV && jo < jend && active) {
+                        const double2 sv = *reinterpret_cast<const double2*>(srow + slot * nx + p0);
                         const double* yrow = Ys + (jo & 1) * NYE;
                         double accA = 0.0, accB = 0.0;
                         // ascending stencil offset == ascending DIA diagonal (sparse.cpp:412-423)
@@ -197,24 +209,15 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                                 }
                             }
                         }
-                        const size_t off = static_cast<size_t>(jo) * nx + i0;
-                        if (validA) {
-                            const double tA = accA * inv;
-                            const double sA = sv.x + tA;
-                            const double tB = accB * inv;
-                            const double sB = sv.y + tB;
-                            if (validB) {
-                                *reinterpret_cast<double2*>(Tout + off) = make_double2(tA, tB);
-                                *reinterpret_cast<double2*>(Sout + off) = make_double2(sA, sB);
-                                tb = umax64(tb, umax64(abs_bits(tA), abs_bits(tB)));
-                                sb = umax64(sb, umax64(abs_bits(sA), abs_bits(sB)));
-                            } else {
-                                Tout[off] = tA;
-                                Sout[off] = sA;
-                                tb = umax64(tb, abs_bits(tA));
-                                sb = umax64(sb, abs_bits(sA));
-                            }
-                        }
+                        const int off = jo * nx + p0;
+                        const double tA = accA * inv;
+                        const double sA = sv.x + tA;
+                        const double tB = accB * inv;
+                        const double sB = sv.y + tB;
+                        *reinterpret_cast<double2*>(Tout + off) = make_double2(tA, tB);
+                        *reinterpret_cast<double2*>(Sout + off) = make_double2(sA, sB);
+                        tb = umax64(tb, umax64(abs_bits(tA), abs_bits(tB)));
+                        sb = umax64(sb, umax64(abs_bits(sA), abs_bits(sB)));
                     }
                     __syncthreads(); // ring slot and Y row consumed by every thread
                 }
@@ -243,6 +246,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     }
 }
 
+// Block-size classes: (max threads, min resident blocks) -> register budget.
 template <int NTMAX> struct NtClass;
 template <> struct NtClass<128> { static constexpr int minb = 4; };
 template <> struct NtClass<256> { static constexpr int minb = 2; };
@@ -263,16 +267,6 @@ void launch_term_nt(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, si
     const size_t cap = static_cast<size_t>(ctx->num_sms) * blocks_per_sm;
     const int grid = static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
     kern<<<grid, nt, smem, ctx->stream>>>(a);
-}
-
-template <int V>
-inline void launch_term_variant_unused(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, size_t work) {
-    if (nt <= 128)
-        launch_term_nt<V, 128>(ctx, a, nt, smem, work);
-    else if (nt <= 256)
-        launch_term_nt<V, 256>(ctx, a, nt, smem, work);
-    else
-        launch_term_nt<V, 512>(ctx, a, nt, smem, work);
 }
 
 } // namespace mg
