@@ -669,7 +669,7 @@ void launch_term(MagnusSession& s) {
         const int H = kVariants[variant].rx <= 2 ? 2 : 4;
         const size_t rw = 2 * static_cast<size_t>(nt) + 2 * H;
         const size_t smem = 128 + kStages * (s.op->nx + 2 * H) * 8 + kStages * s.op->nx * 8 +
-                            (2 + kPairSlots) * static_cast<size_t>(nye) * 8;
+                            ((2 + kPairSlots) * static_cast<size_t>(nye) + 2) * 8;
         (void)rw;
         const size_t work = s.M * static_cast<size_t>(a.nstrips);
         if (nt <= 128)

@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     constexpr int WROWS = 2 * KRV + 1;
     constexpr int NBM = MaskInfo<MASK>::count();
     constexpr int NYE = kClasses * NBM;             // Y entries of one row
+    constexpr int YST = (NYE + 1) & ~1;             // Y row stride (16-byte aligned rows)
     constexpr int J = kStripRows;
     constexpr int KP = kPairSlots;
 
@@ -38,8 +39,9 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     double* rows = reinterpret_cast<double*>(smem_raw + 128); // kStages x RW
     double* srow = rows + kStages * RW;                       // kStages x nx
-    double* Ys = srow + kStages * nx;                         // 2 x NYE
-    double* cq = Ys + 2 * NYE;                                // KP x NYE
+    double* Ys = srow + kStages * nx;                         // 2 x YST
+    double* cq = Ys + 2 * YST;                                // KP x NYE
+    const uint32_t full_u = smem_u32(full), rows_u = smem_u32(rows), srow_u = smem_u32(srow);
     __shared__ double c[6];
     __shared__ unsigned long long red[2][32];
 
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                 const double cs = cq[k * NYE + t];
                 if (cs != 0.0) y += cs * own_w[k];
             }
-            Ys[b * NYE + t] = y;
+            Ys[b * YST + t] = y;
         }
     };
 
@@ -111,12 +113,13 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
             const bool has_s = s >= 2 * KRV && ro < jend;
             if (has_in) bytes += nx * 8;
             if (has_s) bytes += nx * 8;
+            const uint32_t bar = full_u + 8 * slot;
             if (bytes) {
-                mbar_expect_tx(&full[slot], bytes);
-                if (has_in) tma_row(rows + slot * RW + H, in + r * nx, nx * 8, &full[slot]);
-                if (has_s) tma_row(srow + slot * nx, Sin + ro * nx, nx * 8, &full[slot]);
+                mbar_expect_tx_u(bar, bytes);
+                if (has_in) tma_row_u(rows_u + 8 * (slot * RW + H), in + r * nx, nx * 8, bar);
+                if (has_s) tma_row_u(srow_u + 8 * (slot * nx), Sin + ro * nx, nx * 8, bar);
             } else {
-                mbar_arrive(&full[slot]);
+                mbar_arrive_u(bar);
             }
         };
 
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                     }
                     const uint32_t g = gstep + s;
                     const uint32_t slot = g & (kStages - 1);
-                    mbar_wait(&full[slot], (g / kStages) & 1);
+                    mbar_wait_u(full_u + 8 * slot, (g / kStages) & 1);
                     const int r = j0 - KRV + s;
                     if (r >= 0 && r < nv) {
                         const double2* src = reinterpret_cast<const double2*>(rows + slot * RW + p0 + AOFF);
@@ -173,11 +176,12 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                     const int jo = r - KRV; // output row of this step
                     if (s >= 2 * KRV && jo < jend && active) {
                         const double2 sv = *reinterpret_cast<const double2*>(srow + slot * nx + p0);
-                        const double* yrow = Ys + (jo & 1) * NYE;
+                        const double* yrow = Ys + (jo & 1) * YST;
                         double accA = 0.0, accB = 0.0;
                         // ascending stencil offset == ascending DIA diagonal (sparse.cpp:412-423)
                         if (wfast) {
-                            const double* y = yrow + 2 * NBM;
+                            // interior Y row: one 16-byte broadcast load per two entries
+                            const double2* y2 = reinterpret_cast<const double2*>(yrow + 2 * NBM);
 #pragma unroll
                             for (int dv = -KRV; dv <= KRV; ++dv) {
                                 const int rr = ((ph - KRV + dv) % WROWS + WROWS) % WROWS;
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                                     if (MaskInfo<MASK>::has(dx, dv)) {
                                         const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
                                         const int col = H + dx - AOFF;
-                                        const double w = y[e];
+                                        const double w = (e & 1) ? y2[e >> 1].y : y2[e >> 1].x;
                                         accA += w * win[rr][col];
                                         accB += w * win[rr][col + 1];
                                     }
