@@ -6,14 +6,14 @@ namespace mg {
 
 void launch_term_nt128(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work) {
     switch (variant) {
-    case 1: launch_term_nt<1, 128>(ctx, a, nt, smem, work); break;
-    case 2: launch_term_nt<2, 128>(ctx, a, nt, smem, work); break;
-    case 3: launch_term_nt<3, 128>(ctx, a, nt, smem, work); break;
-    case 4: launch_term_nt<4, 128>(ctx, a, nt, smem, work); break;
-    case 5: launch_term_nt<5, 128>(ctx, a, nt, smem, work); break;
-    case 6: launch_term_nt<6, 128>(ctx, a, nt, smem, work); break;
-    default: fail(S2B_ERR_RUNTIME, "term kernel: unknown variant");
+    case 1: launch_term_nt<1, 128>(ctx, a, nt, smem, work); return;
+    case 2: launch_term_nt<2, 128>(ctx, a, nt, smem, work); return;
+    case 3: launch_term_nt<3, 128>(ctx, a, nt, smem, work); return;
+    case 4: launch_term_nt<4, 128>(ctx, a, nt, smem, work); return;
+    case 5: launch_term_nt<5, 128>(ctx, a, nt, smem, work); return;
+    case 6: launch_term_nt<6, 128>(ctx, a, nt, smem, work); return;
     }
+    fail(S2B_ERR_RUNTIME, "term kernel: unknown variant");
 }
 
 } // namespace mg
