@@ -210,6 +210,10 @@ int s2b_magnus_session_moments(s2b_magnus_session *s, double *moments, double *l
 int s2b_magnus_session_destroy(s2b_magnus_session *s);
 
 /* ---- ensembles -------------------------------------------------------------- */
+/* Upload a host SolutionEnsemble (states [M][n], status [M] 0 Ok; blown rows ignored). */
+int s2b_ensemble_create_host(s2b_context *ctx, const s2b_grid *grid, double t, uint64_t seed,
+                             size_t M, const double *states, const uint8_t *status,
+                             s2b_ensemble **out);
 /* info: [0] records, [1] M, [2] n, [3] nx, [4] nv */
 int s2b_ensemble_info(const s2b_ensemble *e, int64_t info[5], double *times);
 int s2b_ensemble_download(const s2b_ensemble *e, size_t record, double *states, uint8_t *status);
@@ -220,6 +224,9 @@ int s2b_ensemble_destroy(s2b_ensemble *e);
 /* ---- exact solution + norms -------------------------------------------------- */
 int s2b_exact_reference(s2b_context *ctx, const s2b_grid *grid, double t, double a,
                         double sigma, const s2b_paths *paths, s2b_ensemble **out);
+/* One closed-form field (exact_langevin_field, exact_langevin.hpp:36-41) into host out[n]. */
+int s2b_exact_field(s2b_context *ctx, const s2b_grid *grid, double t, double a, double sigma,
+                    double W, double IW, double *out);
 int s2b_errors(s2b_context *ctx, const s2b_ensemble *ref, size_t ref_record,
                const s2b_ensemble *app, size_t app_record, int kappa, s2b_error_stats *out,
                double *me_out);

@@ -230,6 +230,15 @@ struct ItoFunctionals {
 };
 ItoFunctionals lebesgue_functionals(const PathSegment& segment);
 
+// Test oracles of the reference (stochastics.hpp:75-91): pathwise residuals of the three
+// polynomial Ito identities, host-side.
+enum class ItoIdentity { A, B, C };
+struct ItoExponents {
+    int p = 0, p1 = 0, p2 = 0;
+    int q = 0, q1 = 0, q2 = 0;
+};
+double ito_identity_residual(ItoIdentity identity, const ItoExponents& e, const PathSegment& segment);
+
 // ---- solvers (reference magnus.hpp:13-108, euler.hpp:12-49) -------------------
 struct AdaptiveConfig {
     bool enabled = false;
@@ -261,6 +270,11 @@ struct SolutionEnsemble {
     std::size_t blowup_count() const;
 };
 
+// Magnus logarithm as an explicit CSR matrix (magnus.hpp:49-56), host-side, and one
+// propagator application exp(Y) u on the GPU (magnus.hpp:58-60).
+SparseMatrix magnus_log(int order, const CommutatorSet& comms, const ItoFunctionals& f);
+std::vector<double> magnus_step(const SparseMatrix& y, std::span<const double> u, double tol);
+
 std::vector<SolutionEnsemble> solve_iterated_magnus(const MagnusConfig& cfg,
                                                     const CommutatorSet& comms,
                                                     std::span<const double> phi,
@@ -287,6 +301,11 @@ struct PathFunctionalsForExact {
     double W = 0.0, IW = 0.0;
 };
 Field gaussian_datum(const GridSpec& grid);
+// Fundamental solution at the origin (exact_langevin.hpp:27-30), host scalar.
+double gamma0(double t, double x, double v, const LangevinParams& params);
+// Closed-form pathwise field (exact_langevin.hpp:36-41), evaluated on the GPU.
+Field exact_langevin_field(const GridSpec& grid, double t, const LangevinParams& params,
+                           const PathFunctionalsForExact& path);
 SolutionEnsemble exact_reference(const GridSpec& grid, double t, const LangevinParams& params,
                                  const BrownianBatch& batch);
 

@@ -97,12 +97,16 @@ SIGNATURES = {
     "s2b_magnus_session_finish": (C.c_int, [_VP, _P(_VP)]),
     "s2b_magnus_session_moments": (C.c_int, [_VP, _P(C.c_double), _P(C.c_double)]),
     "s2b_magnus_session_destroy": (C.c_int, [_VP]),
+    "s2b_ensemble_create_host": (C.c_int, [_VP, _P(Grid), C.c_double, C.c_uint64, C.c_size_t,
+                                           _P(C.c_double), _P(C.c_uint8), _P(_VP)]),
     "s2b_ensemble_info": (C.c_int, [_VP, _P(C.c_int64), _P(C.c_double)]),
     "s2b_ensemble_download": (C.c_int, [_VP, C.c_size_t, _P(C.c_double), _P(C.c_uint8)]),
     "s2b_ensemble_counters": (C.c_int, [_VP, _P(C.c_int64), _P(C.c_int64)]),
     "s2b_ensemble_destroy": (C.c_int, [_VP]),
     "s2b_exact_reference": (C.c_int, [_VP, _P(Grid), C.c_double, C.c_double, C.c_double, _VP,
                                       _P(_VP)]),
+    "s2b_exact_field": (C.c_int, [_VP, _P(Grid), C.c_double, C.c_double, C.c_double, C.c_double,
+                                  C.c_double, _P(C.c_double)]),
     "s2b_errors": (C.c_int, [_VP, _VP, C.c_size_t, _VP, C.c_size_t, C.c_int, _P(ErrorStats),
                              _P(C.c_double)]),
     "s2b_exact_errors": (C.c_int, [_VP, _VP, C.c_size_t, C.c_double, C.c_double, _VP, C.c_int,

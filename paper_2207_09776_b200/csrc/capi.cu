@@ -454,6 +454,40 @@ int s2b_magnus_session_destroy(s2b_magnus_session* s) {
     return guard([&] { session_destroy(S(s)); });
 }
 
+int s2b_ensemble_create_host(s2b_context* ctx, const s2b_grid* grid, double t, uint64_t seed, size_t M,
+                             const double* states, const uint8_t* status, s2b_ensemble** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(states, "states");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        auto* e = new s2b_ensemble();
+        try {
+            const size_t n = grid->nx * grid->nv;
+            e->ctx = ctx;
+            e->R = 1;
+            e->M = M;
+            e->nx = grid->nx;
+            e->nv = grid->nv;
+            e->seed = seed;
+            e->grid = *grid;
+            e->times.push_back(t);
+            e->states.emplace_back(M * n);
+            e->status.alloc(M);
+            S2B_CUDA(cudaMemcpy(e->states[0].p, states, M * n * sizeof(double), cudaMemcpyHostToDevice));
+            if (status)
+                S2B_CUDA(cudaMemcpy(e->status.p, status, M, cudaMemcpyHostToDevice));
+            else
+                S2B_CUDA(cudaMemset(e->status.p, 0, M));
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
 int s2b_ensemble_info(const s2b_ensemble* e, int64_t info[5], double* times) {
     return guard([&] {
         need(e, "ensemble");
@@ -511,6 +545,17 @@ int s2b_exact_reference(s2b_context* ctx, const s2b_grid* grid, double t, double
         need(out, "out");
         S2B_CUDA(cudaSetDevice(ctx->device));
         *out = exact_reference(ctx, grid, t, a, sigma, paths);
+    });
+}
+
+int s2b_exact_field(s2b_context* ctx, const s2b_grid* grid, double t, double a, double sigma, double W, double IW,
+                    double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        exact_field(ctx, grid, t, a, sigma, W, IW, out);
     });
 }
 

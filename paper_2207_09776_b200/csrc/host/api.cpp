@@ -1,0 +1,250 @@
+// GPU-backed half of the C++ drop-in: the reference's solver, exact-solution and norm
+// entry points (magnus.hpp:93-97, euler.hpp:46-49, exact_langevin.hpp:44-46,
+// analysis.hpp:35-50, sparse.hpp:153-155) with their exact signatures, implemented on the
+// C ABI (spde2d_b200.h).  Host types in, host types out; the data crosses to the GPU once
+// per call.  Errors come back as the reference's exception classes; numerical failure is
+// the per-path BlownUp status.  There is no CPU fallback: without a usable B200 every call
+// throws std::runtime_error.
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "spde2d_b200.h"
+#include "spde2d_b200.hpp"
+
+namespace spde2d {
+
+namespace {
+
+void check(int rc) {
+    if (rc == S2B_OK) return;
+    const std::string msg = s2b_last_error();
+    if (rc == S2B_ERR_CONFIG) throw ConfigError(msg);
+    if (rc == S2B_ERR_DIMENSION) throw DimensionError(msg);
+    throw std::runtime_error(msg);
+}
+
+// One context per process (device from S2B_DEVICE, default 0), created on first use.
+s2b_context* context() {
+    static std::once_flag once;
+    static s2b_context* ctx = nullptr;
+    std::call_once(once, [] {
+        const char* d = std::getenv("S2B_DEVICE");
+        check(s2b_context_create(d ? std::atoi(d) : 0, &ctx));
+    });
+    return ctx;
+}
+
+s2b_grid c_grid(const GridSpec& g) { return s2b_grid{g.x.a, g.x.b, g.x.n, g.v.a, g.v.b, g.v.n}; }
+
+s2b_csr c_csr(const SparseMatrix& m) {
+    return s2b_csr{m.rows(), m.row_ptr().data(), m.col_idx().data(), m.values().data()};
+}
+
+template <class T>
+std::unique_ptr<T, int (*)(T*)> own(T* p, int (*d)(T*)) {
+    return std::unique_ptr<T, int (*)(T*)>(p, d);
+}
+
+std::vector<double> flat_values(const BrownianBatch& b) {
+    std::vector<double> v(b.M * (b.steps + 1));
+    for (std::size_t m = 0; m < b.M; ++m) {
+        if (b.values[m].size() != b.steps + 1) throw DimensionError("BrownianBatch: ragged values");
+        std::memcpy(v.data() + m * (b.steps + 1), b.values[m].data(), (b.steps + 1) * sizeof(double));
+    }
+    return v;
+}
+
+s2b_paths* upload_paths(const BrownianBatch& b) {
+    const std::vector<double> v = flat_values(b);
+    s2b_paths* p = nullptr;
+    check(s2b_paths_create_host(context(), b.dt_leb, b.steps, b.M, b.seed, v.data(), &p));
+    return p;
+}
+
+// Device ensemble -> host SolutionEnsembles (blown paths get an empty state).
+std::vector<SolutionEnsemble> download(s2b_ensemble* e, const GridSpec& grid, std::uint64_t seed,
+                                       double seconds_per_path) {
+    int64_t info[5];
+    check(s2b_ensemble_info(e, info, nullptr));
+    std::vector<double> times(static_cast<std::size_t>(info[0]));
+    check(s2b_ensemble_info(e, info, times.data()));
+    const std::size_t R = info[0], M = info[1], n = info[2];
+    std::vector<SolutionEnsemble> out(R);
+    std::vector<double> states(M * n);
+    std::vector<std::uint8_t> status(M);
+    for (std::size_t r = 0; r < R; ++r) {
+        check(s2b_ensemble_download(e, r, states.data(), status.data()));
+        SolutionEnsemble& s = out[r];
+        s.grid = grid;
+        s.t = times[r];
+        s.seed = seed;
+        s.states.resize(M);
+        s.status.resize(M);
+        s.seconds.assign(M, seconds_per_path);
+        for (std::size_t m = 0; m < M; ++m) {
+            s.status[m] = status[m] ? TrajectoryStatus::BlownUp : TrajectoryStatus::Ok;
+            if (!status[m]) s.states[m].assign(states.begin() + m * n, states.begin() + (m + 1) * n);
+        }
+    }
+    return out;
+}
+
+s2b_ensemble* upload_ensemble(const SolutionEnsemble& e) {
+    const std::size_t M = e.trajectories(), n = e.grid.dim();
+    std::vector<double> states(M * n, 0.0);
+    std::vector<std::uint8_t> status(M);
+    for (std::size_t m = 0; m < M; ++m) {
+        status[m] = e.status[m] == TrajectoryStatus::Ok ? 0 : 1;
+        if (!status[m]) {
+            if (e.states[m].size() != n) throw DimensionError("SolutionEnsemble: state length mismatch");
+            std::memcpy(states.data() + m * n, e.states[m].data(), n * sizeof(double));
+        }
+    }
+    const s2b_grid g = c_grid(e.grid);
+    s2b_ensemble* out = nullptr;
+    check(s2b_ensemble_create_host(context(), &g, e.t, e.seed, M, states.data(), status.data(), &out));
+    return out;
+}
+
+double elapsed_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+} // namespace
+
+std::vector<SolutionEnsemble> solve_iterated_magnus(const MagnusConfig& cfg, const CommutatorSet& comms,
+                                                    std::span<const double> phi, const BrownianBatch& batch,
+                                                    double T, const GridSpec& grid) {
+    if (cfg.order < 1 || cfg.order > 3 || cfg.order > comms.order)
+        throw ConfigError("solve_iterated_magnus: unsupported order");
+    if (phi.size() != grid.dim() || comms.B.rows() != grid.dim())
+        throw DimensionError("solve_iterated_magnus: dimension mismatch");
+    const auto t0 = std::chrono::steady_clock::now();
+    const s2b_grid g = c_grid(grid);
+    const SparseMatrix empty;
+    // the operator is laid out for exactly the requested order (MagnusLogBuilder(comms, cfg.order))
+    const s2b_csr src[6] = {c_csr(comms.B), c_csr(comms.A),
+                            cfg.order >= 2 ? c_csr(comms.A2) : c_csr(empty),
+                            cfg.order >= 2 ? c_csr(comms.BA) : c_csr(empty),
+                            cfg.order >= 3 ? c_csr(comms.BAA) : c_csr(empty),
+                            cfg.order >= 3 ? c_csr(comms.BAB) : c_csr(empty)};
+    s2b_operator* op = nullptr;
+    check(s2b_operator_create(context(), &g, cfg.order, src, &op));
+    auto op_guard = own(op, s2b_operator_destroy);
+    auto paths = own(upload_paths(batch), s2b_paths_destroy);
+    const s2b_magnus_config c{cfg.order,       cfg.dt,           T, cfg.expmv_tol, cfg.expmv_theta,
+                              cfg.blowup_norm_cap, cfg.record_times.data(), cfg.record_times.size()};
+    s2b_ensemble* e = nullptr;
+    check(s2b_solve_magnus(context(), op, &c, phi.data(), paths.get(), &e, nullptr));
+    auto e_guard = own(e, s2b_ensemble_destroy);
+    // per-path wall time is not observable on the GPU: report the mean (CSV uses total/M)
+    return download(e, grid, batch.seed, elapsed_since(t0) / static_cast<double>(batch.M));
+}
+
+std::vector<SolutionEnsemble> solve_euler(const EulerConfig& cfg, const CoefficientFields& fields,
+                                          const GridSpec& grid, const Field& phi, const BrownianBatch& batch,
+                                          double T) {
+    if (phi.nx() != grid.x.n || phi.nv() != grid.v.n) throw DimensionError("solve_euler: datum shape mismatch");
+    const auto t0 = std::chrono::steady_clock::now();
+    const s2b_grid g = c_grid(grid);
+    const Field* all[9] = {&fields.h, &fields.fx, &fields.fv, &fields.gxx, &fields.gxv,
+                           &fields.gvv, &fields.sig, &fields.sigx, &fields.sigv};
+    const bool zero[9] = {fields.zero_h,   fields.zero_fx,  fields.zero_fv,  fields.zero_gxx, fields.zero_gxv,
+                          fields.zero_gvv, fields.zero_sig, fields.zero_sigx, fields.zero_sigv};
+    const double* f9[9];
+    for (int k = 0; k < 9; ++k) {
+        if (!zero[k] && (all[k]->nx() != grid.x.n || all[k]->nv() != grid.v.n))
+            throw DimensionError("coefficient field shape does not match the grid");
+        f9[k] = zero[k] ? nullptr : all[k]->data().data();
+    }
+    s2b_fields* f = nullptr;
+    check(s2b_fields_create(context(), &g, f9, &f));
+    auto f_guard = own(f, s2b_fields_destroy);
+    auto paths = own(upload_paths(batch), s2b_paths_destroy);
+    const s2b_euler_config c{cfg.dt, T, cfg.record_times.data(), cfg.record_times.size()};
+    s2b_ensemble* e = nullptr;
+    check(s2b_solve_euler(context(), f, &c, phi.data().data(), paths.get(), &e));
+    auto e_guard = own(e, s2b_ensemble_destroy);
+    return download(e, grid, batch.seed, elapsed_since(t0) / static_cast<double>(batch.M));
+}
+
+SolutionEnsemble exact_reference(const GridSpec& grid, double t, const LangevinParams& params,
+                                 const BrownianBatch& batch) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const s2b_grid g = c_grid(grid);
+    auto paths = own(upload_paths(batch), s2b_paths_destroy);
+    s2b_ensemble* e = nullptr;
+    check(s2b_exact_reference(context(), &g, t, params.a, params.sigma, paths.get(), &e));
+    auto e_guard = own(e, s2b_ensemble_destroy);
+    auto out = download(e, grid, batch.seed, elapsed_since(t0) / static_cast<double>(batch.M));
+    return std::move(out.front());
+}
+
+namespace {
+s2b_error_stats norms(const SolutionEnsemble& ref, const SolutionEnsemble& app, const CentralRegion& region,
+                      Field* me) {
+    if (ref.grid.x.n != app.grid.x.n || ref.grid.v.n != app.grid.v.n)
+        throw DimensionError("error norms: grids differ");
+    if (ref.trajectories() != app.trajectories()) throw DimensionError("error norms: trajectory counts differ");
+    if (ref.seed != app.seed) throw ConfigError("error norms: ensembles were built from different seeds");
+    auto r = own(upload_ensemble(ref), s2b_ensemble_destroy);
+    auto a = own(upload_ensemble(app), s2b_ensemble_destroy);
+    s2b_error_stats st{};
+    const std::size_t w = region.size();
+    std::vector<double> buf(w * w);
+    check(s2b_errors(context(), r.get(), 0, a.get(), 0, region.kappa, &st, buf.data()));
+    if (st.region_lo != region.lo || st.region_hi != region.hi)
+        throw ConfigError("error norms: region does not match central_region(d, kappa)");
+    if (me) {
+        *me = Field(w, w);
+        std::memcpy(me->data().data(), buf.data(), buf.size() * sizeof(double));
+    }
+    return st;
+}
+} // namespace
+
+MeanAbsError mean_abs_error(const SolutionEnsemble& ref, const SolutionEnsemble& app, const CentralRegion& region) {
+    MeanAbsError out;
+    const s2b_error_stats st = norms(ref, app, region, &out.me);
+    out.excluded = st.excluded;
+    return out;
+}
+
+RelError mean_rel_error(const SolutionEnsemble& ref, const SolutionEnsemble& app, const CentralRegion& region) {
+    const s2b_error_stats st = norms(ref, app, region, nullptr);
+    return RelError{st.err, st.blowups};
+}
+
+std::vector<double> magnus_step(const SparseMatrix& y, std::span<const double> u, double tol) {
+    return expmv(y, u, tol);
+}
+
+Field exact_langevin_field(const GridSpec& grid, double t, const LangevinParams& params,
+                           const PathFunctionalsForExact& path) {
+    const s2b_grid g = c_grid(grid);
+    Field f(grid.x.n, grid.v.n);
+    check(s2b_exact_field(context(), &g, t, params.a, params.sigma, path.W, path.IW, f.data().data()));
+    return f;
+}
+
+std::vector<double> expmv(const SparseMatrix& m, std::span<const double> v, double tol, double theta) {
+    if (m.rows() != m.cols()) throw DimensionError("expmv: matrix must be square");
+    if (v.size() != m.cols()) throw DimensionError("expmv: vector length mismatch");
+    const s2b_csr c = c_csr(m);
+    std::vector<double> y(v.size());
+    int rep[4];
+    check(s2b_expmv(context(), &c, v.data(), tol, theta, y.data(), rep));
+    if (rep[0] == 1) throw ExpmvError(ExpmvStatus::Overflow, std::numeric_limits<double>::infinity(),
+                                      "expmv: overflow (non-finite intermediate)");
+    if (rep[0] == 2)
+        throw ExpmvError(ExpmvStatus::ToleranceNotReached, 0.0, "expmv: tolerance not reached within term budget");
+    return y;
+}
+
+} // namespace spde2d

@@ -548,6 +548,96 @@ ItoFunctionals lebesgue_functionals(const PathSegment& seg) {
     return f;
 }
 
+// ---- Ito identity residuals (stochastics.cpp:143-227), test oracles ---------------
+namespace {
+double pw(double x, int k) {
+    double r = 1.0;
+    for (int i = 0; i < k; ++i) r *= x;
+    return r;
+}
+} // namespace
+
+double ito_identity_residual(ItoIdentity id, const ItoExponents& e, const PathSegment& seg) {
+    if (e.p < 0 || e.p1 < 0 || e.p2 < 0 || e.q < 0 || e.q1 < 0 || e.q2 < 0)
+        throw ConfigError("ito_identity_residual: exponents must be non-negative");
+    const std::size_t n = seg.steps();
+    if (n == 0) throw ConfigError("ito_identity_residual: empty segment");
+    const auto& p = *seg.path;
+    const double base = p[seg.k0], dt = seg.dt_leb, t = seg.length(), wt = seg.terminal();
+    auto W = [&](std::size_t j) { return p[seg.k0 + j] - base; };
+    auto dW = [&](std::size_t j) { return p[seg.k0 + j + 1] - p[seg.k0 + j]; };
+    if (id == ItoIdentity::A) {
+        // int s^p W^q dW = (t^p W_t^{q+1} - int [q(q+1)/2 s^p W^{q-1} + p W^{q+1} s^{p-1}] ds)/(q+1)
+        double lhs = 0.0, rem = 0.0;
+        const double cq = 0.5 * e.q * (e.q + 1);
+        for (std::size_t j = 0; j < n; ++j) {
+            const double s = static_cast<double>(j) * dt, w = W(j);
+            lhs += pw(s, e.p) * pw(w, e.q) * dW(j);
+            double g = 0.0;
+            if (e.q > 0) g += cq * pw(s, e.p) * pw(w, e.q - 1);
+            if (e.p > 0) g += e.p * pw(w, e.q + 1) * pw(s, e.p - 1);
+            rem += g;
+        }
+        return lhs - (pw(t, e.p) * pw(wt, e.q + 1) - rem * dt) / (e.q + 1);
+    }
+    if (id == ItoIdentity::B) {
+        // int s^{p1} (int r^{p2} W^q dr) ds = (t^{1+p1} int s^{p2} W^q - int s^{1+p1+p2} W^q)/(1+p1)
+        double lhs = 0.0, inner = 0.0, i1 = 0.0, i2 = 0.0;
+        for (std::size_t j = 0; j < n; ++j) {
+            const double s = static_cast<double>(j) * dt, w = W(j);
+            lhs += pw(s, e.p1) * inner;
+            inner += pw(s, e.p2) * pw(w, e.q) * dt;
+            i1 += pw(s, e.p2) * pw(w, e.q);
+            i2 += pw(s, 1 + e.p1 + e.p2) * pw(w, e.q);
+        }
+        lhs *= dt;
+        return lhs - (pw(t, 1 + e.p1) * i1 * dt - i2 * dt) / (1 + e.p1);
+    }
+    // C: int s^{p1} W^{q1} (int r^{p2} W^{q2} dr) dW with three Lebesgue remainders
+    double lhs = 0.0, inner = 0.0, i1 = 0.0, i2 = 0.0, i3 = 0.0, i4 = 0.0;
+    const double cq = 0.5 * e.q1 * (e.q1 + 1);
+    for (std::size_t j = 0; j < n; ++j) {
+        const double s = static_cast<double>(j) * dt, w = W(j);
+        lhs += pw(s, e.p1) * pw(w, e.q1) * inner * dW(j);
+        i1 += pw(s, e.p2) * pw(w, e.q2);
+        i2 += pw(s, e.p1 + e.p2) * pw(w, e.q1 + e.q2 + 1);
+        if (e.q1 > 0) i3 += pw(s, e.p1) * pw(w, e.q1 - 1) * inner;
+        if (e.p1 > 0) i4 += pw(s, e.p1 - 1) * pw(w, e.q1 + 1) * inner;
+        inner += pw(s, e.p2) * pw(w, e.q2) * dt;
+    }
+    double rhs = pw(t, e.p1) * pw(wt, e.q1 + 1) * i1 * dt - i2 * dt;
+    if (e.q1 > 0) rhs -= cq * i3 * dt;
+    if (e.p1 > 0) rhs -= e.p1 * i4 * dt;
+    return lhs - rhs / (e.q1 + 1);
+}
+
+// ---- magnus_log (magnus.cpp:26-40, 63-82): the logarithm as an explicit CSR ------------
+SparseMatrix magnus_log(int order, const CommutatorSet& comms, const ItoFunctionals& f) {
+    if (order < 1 || order > 3) throw ConfigError("magnus_log: order must be in {1, 2, 3}");
+    if (order > comms.order) throw ConfigError("magnus_log: commutator set does not cover this order");
+    const double h = f.h;
+    SparseMatrix y = sparse_add(sparse_scale(comms.B, h), sparse_scale(comms.A, f.W));
+    if (order >= 2) {
+        y = sparse_add(y, sparse_scale(comms.A2, -0.5 * h));
+        y = sparse_add(y, sparse_scale(comms.BA, f.IW - 0.5 * h * f.W));
+    }
+    if (order >= 3) {
+        y = sparse_add(y, sparse_scale(comms.BAA, 0.5 * f.IW2 - 0.5 * f.W * f.IW + h * f.W * f.W / 12.0));
+        y = sparse_add(y, sparse_scale(comms.BAB, f.IsW - 0.5 * h * f.IW - h * h * f.W / 12.0));
+    }
+    return y;
+}
+
+// ---- gamma0 (exact_langevin.cpp:20-27) --------------------------------------------
+double gamma0(double t, double x, double v, const LangevinParams& p) {
+    if (!(p.a > 0.0) || p.sigma < 0.0 || !(p.gap() > 0.0))
+        throw ConfigError("exact Langevin solution needs a > 0 and a - sigma^2 > 0");
+    if (!(t > 0.0)) throw ConfigError("gamma0: t must be positive");
+    const double c = p.gap();
+    const double quad = v * v / t - 3.0 * v * x / (t * t) + 3.0 * x * x / (t * t * t);
+    return std::numbers::sqrt3 / (std::numbers::pi * t * t * c) * std::exp(-(2.0 / c) * quad);
+}
+
 std::size_t SolutionEnsemble::blowup_count() const {
     return static_cast<std::size_t>(std::count(status.begin(), status.end(), TrajectoryStatus::BlownUp));
 }

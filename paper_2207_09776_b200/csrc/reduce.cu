@@ -265,6 +265,21 @@ s2b_ensemble* exact_reference(s2b_context* ctx, const s2b_grid* grid, double t, 
     return e;
 }
 
+void exact_field(s2b_context* ctx, const s2b_grid* grid, double t, double a, double sigma, double W, double IW,
+                 double* host_out) {
+    const ExactParams p = exact_params(*grid, t, a, sigma);
+    const size_t n = grid->nx * grid->nv;
+    DevBuf<double2> wiw(1);
+    DevBuf<double> out(n);
+    const double2 h = make_double2(W, IW);
+    S2B_CUDA(cudaMemcpyAsync(wiw.p, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+    exact_field_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 1024)), 256, 0, ctx->stream>>>(
+        p, wiw.p, out.p, 1);
+    S2B_LAUNCHED(ctx);
+    S2B_CUDA(cudaMemcpyAsync(host_out, out.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 void errors(s2b_context* ctx, const s2b_ensemble* ref, size_t ref_record, const s2b_ensemble* app,
             size_t app_record, int kappa, s2b_error_stats* out, double* me_out) {
     if (ref->nx != app->nx || ref->nv != app->nv) fail(S2B_ERR_DIMENSION, "error norms: grids differ");
