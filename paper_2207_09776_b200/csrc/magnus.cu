@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -564,6 +565,7 @@ struct MagnusSession {
     int* h_cnt = nullptr; // pinned
     int cur = 0;          // which act[] is the input list
     bool timing = false;
+    bool use_cluster = false; // cluster-resident engine (cluster_magnus.cu) for this operator
     std::vector<cudaEvent_t> ev;
     s2b_magnus_stats stats{};
 
@@ -726,6 +728,13 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
         s->n = n;
         s->nwin = s->plan.total_steps / s->plan.dt_steps;
         s->R = static_cast<int>(s->plan.record_steps.size());
+        {
+            // S2B_ENGINE=stream|cluster overrides the automatic choice (A/B measurements)
+            const char* eng = std::getenv("S2B_ENGINE");
+            const bool ok = op->variant != 0 &&
+                            cluster_engine_supported(op->variant, static_cast<int>(op->nx), static_cast<int>(op->nv));
+            s->use_cluster = ok && !(eng && std::strcmp(eng, "stream") == 0);
+        }
         s->phi.assign(phi, phi + n);
         const size_t M = s->M;
         for (int b = 0; b < 2; ++b) {
@@ -780,6 +789,9 @@ void session_reset(MagnusSession* s) {
     S2B_CUDA(cudaMemsetAsync(s->iv.p, 0, s->iv.bytes(), s->ctx->stream));
     S2B_CUDA(cudaMemsetAsync(s->rec_status.p, 1, s->rec_status.bytes(), s->ctx->stream));
     S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->terms.p, 0, s->terms.bytes(), s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->windows.p, 0, s->windows.bytes(), s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->segments.p, 0, s->segments.bytes(), s->ctx->stream));
     s->cur = 0;
     s->cur_window = 0;
     s->stats = s2b_magnus_stats{};
@@ -813,6 +825,55 @@ void session_advance(MagnusSession* s, size_t n_windows) {
     if (n_windows == 0 || static_cast<size_t>(s->cur_window) >= s->nwin) return;
     const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
     prepare_windows(s, s->cur_window, stop);
+    if (s->use_cluster) {
+        // cluster-resident engine: every live path runs windows [cur, stop) on chip
+        ClusterArgs a{};
+        a.wt = s->op->d_wt.p;
+        a.eslot = s->op->d_eslot.p;
+        a.nx = static_cast<int>(s->op->nx);
+        a.nv = static_cast<int>(s->op->nv);
+        a.ctab = s->ctab.p;
+        a.stab = s->stab.p;
+        a.nwin = static_cast<int>(s->nwin);
+        a.win0 = s->cur_window;
+        a.win1 = stop;
+        a.dt_steps = static_cast<int>(s->plan.dt_steps);
+        a.S0 = s->S[0].p;
+        a.S1 = s->S[1].p;
+        a.win = s->iv.p;
+        a.status = s->iv.p + 4 * s->M;
+        a.par = s->iv.p + 5 * s->M;
+        a.rec_next = s->iv.p + 6 * s->M;
+        a.terms = s->terms.p;
+        a.windows = s->windows.p;
+        a.segments = s->segments.p;
+        a.rec = s->rec_ptrs.p;
+        a.rec_status = s->rec_status.p;
+        a.rec_steps = s->rec_steps.p;
+        a.R = s->R;
+        a.tol = s->cfg.expmv_tol;
+        a.cap = s->cfg.blowup_norm_cap;
+        a.M = static_cast<int>(s->M);
+        a.work = s->cnt.p + 3;
+        S2B_CUDA(cudaMemsetAsync(s->cnt.p + 3, 0, sizeof(int), s->ctx->stream));
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (s->timing) {
+            S2B_CUDA(cudaEventCreate(&e0));
+            S2B_CUDA(cudaEventCreate(&e1));
+            S2B_CUDA(cudaEventRecord(e0, s->ctx->stream));
+        }
+        launch_cluster_magnus(s->ctx, s->op->variant, a);
+        s->stats.term_launches += 1;
+        if (s->timing) {
+            S2B_CUDA(cudaEventRecord(e1, s->ctx->stream));
+            s->ev.push_back(e0);
+            s->ev.push_back(e1);
+        }
+        S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        if (s->timing) collect_timing(*s);
+        s->cur_window = stop;
+        return;
+    }
     {
         // (re)activate every live path at the current window boundary; window 0 also
         // initialises the per-path state (parity, records, counters)

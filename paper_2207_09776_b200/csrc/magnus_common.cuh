@@ -188,5 +188,34 @@ void launch_term_nt128(s2b_context* ctx, int variant, const TermArgs& a, int nt,
 void launch_term_nt256(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
 void launch_term_nt512(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
 
+// Cluster-resident engine (cluster_magnus.cu): one 8-CTA cluster per path, all Taylor terms
+// of windows [win0, win1) on chip.
+struct ClusterArgs {
+    const double* wt;  // entry-major weights of the variant (as TermArgs::wt)
+    const int* eslot;
+    int nx, nv;
+    const double* ctab; // [M][nwin][6]
+    const int* stab;    // [M][nwin]
+    int nwin, win0, win1, dt_steps;
+    double* S0;
+    double* S1;
+    int* par;
+    int* status;
+    int* win;
+    int* rec_next;
+    long long* terms;
+    long long* windows;
+    long long* segments;
+    double* const* rec; // R-1 record buffers
+    uint8_t* rec_status;
+    const long long* rec_steps;
+    int R;
+    double tol, cap;
+    int M;
+    int* work; // path counter (zeroed before the launch)
+};
+bool cluster_engine_supported(int variant, int nx, int nv);
+void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterArgs& a);
+
 } // namespace mg
 } // namespace s2b
