@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "magnus_common.cuh"
 
@@ -23,10 +24,7 @@ namespace mg {
 
 namespace {
 
-constexpr int kCl = 8;            // CTAs per cluster
-constexpr int kBands = 4;         // row bands per CTA (one 128-thread group each)
 constexpr int kBandThreads = 128; // 2 x-points per thread -> nx <= 256
-constexpr int kClThreads = kBands * kBandThreads;
 
 template <uint64_t MASK, int KRX>
 struct ClLayout {
@@ -61,8 +59,12 @@ struct NormAcc {
     }
 };
 
-template <int KRX, int KRV, uint64_t MASK, int RPB>
-__global__ void __launch_bounds__(kClThreads, 1) cluster_magnus_kernel(ClusterArgs a) {
+// CL CTAs per cluster, BANDS 128-thread row bands per CTA, RPB rows per band.
+template <int KRX, int KRV, uint64_t MASK, int RPB, int CL, int BANDS>
+__global__ void __launch_bounds__(BANDS * kBandThreads, (BANDS <= 2 ? 2 : 1)) cluster_magnus_kernel(ClusterArgs a) {
+    constexpr int kCl = CL;
+    constexpr int kBands = BANDS;
+    constexpr int kClThreads = BANDS * kBandThreads;
     using L = ClLayout<MASK, KRX>;
     constexpr int H = L::H;
     constexpr int AOFF = (H - KRX) & ~1;
@@ -345,40 +347,60 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_magnus_kernel(ClusterAr
     }
 }
 
-template <int V, int RPB>
+template <int V, int RPB, int CL, int BANDS>
 void launch_vr(s2b_context* ctx, const ClusterArgs& a) {
     constexpr Variant v = kVariants[V];
-    auto kern = cluster_magnus_kernel<v.rx, v.rv, v.mask, RPB>;
-    const size_t smem = ClLayout<v.mask, v.rx>::smem_bytes(a.nx, RPB * kBands);
+    auto kern = cluster_magnus_kernel<v.rx, v.rv, v.mask, RPB, CL, BANDS>;
+    const size_t smem = ClLayout<v.mask, v.rx>::smem_bytes(a.nx, RPB * BANDS);
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (CL > 8) S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(kClThreads);
+    cfg.blockDim = dim3(BANDS * kBandThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kCl;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(kCl);
+    cfg.gridDim = dim3(CL);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
     clusters = std::max(1, std::min(clusters, a.M));
-    cfg.gridDim = dim3(kCl * clusters);
+    cfg.gridDim = dim3(CL * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
+// Cluster shapes: 8 CTAs x 4 bands (one CTA per SM) is the default; S2B_CLUSTER=16 selects
+// 16 CTAs x 2 bands (two CTAs per SM, more SMs filled but a wider barrier per term) —
+// measured slower on B200 at 256^2 (8.3e8 vs 8.9e8 path*pt*windows/s).
+bool use_wide_cluster() {
+    static const bool wide = [] {
+        const char* e = std::getenv("S2B_CLUSTER");
+        return e && e[0] == '1' && e[1] == '6';
+    }();
+    return wide;
 }
 
 template <int V>
 void launch_v(s2b_context* ctx, const ClusterArgs& a) {
-    switch (a.nv / (kCl * kBands)) {
-    case 1: launch_vr<V, 1>(ctx, a); break;
-    case 2: launch_vr<V, 2>(ctx, a); break;
-    case 4: launch_vr<V, 4>(ctx, a); break;
-    case 8: launch_vr<V, 8>(ctx, a); break;
-    default: fail(S2B_ERR_RUNTIME, "cluster engine: unsupported nv");
+    if (use_wide_cluster() && a.nv % (16 * 2) == 0) {
+        switch (a.nv / (16 * 2)) {
+        case 1: launch_vr<V, 1, 16, 2>(ctx, a); return;
+        case 2: launch_vr<V, 2, 16, 2>(ctx, a); return;
+        case 4: launch_vr<V, 4, 16, 2>(ctx, a); return;
+        case 8: launch_vr<V, 8, 16, 2>(ctx, a); return;
+        }
     }
+    switch (a.nv / (8 * 4)) {
+    case 1: launch_vr<V, 1, 8, 4>(ctx, a); return;
+    case 2: launch_vr<V, 2, 8, 4>(ctx, a); return;
+    case 4: launch_vr<V, 4, 8, 4>(ctx, a); return;
+    case 8: launch_vr<V, 8, 8, 4>(ctx, a); return;
+    }
+    fail(S2B_ERR_RUNTIME, "cluster engine: unsupported nv");
 }
 
 } // namespace
@@ -386,9 +408,9 @@ void launch_v(s2b_context* ctx, const ClusterArgs& a) {
 bool cluster_engine_supported(int variant, int nx, int nv) {
     if (variant < 1 || variant > 4) return false;
     if (nx % 2 || nx < 6 || nx > 2 * kBandThreads) return false;
-    const int rpb = nv / (kCl * kBands);
-    if (nv % (kCl * kBands) || (rpb != 1 && rpb != 2 && rpb != 4 && rpb != 8)) return false;
-    const int rpc = rpb * kBands;
+    const int rpb = nv / 32; // 8 CTAs x 4 bands (or 16 x 2)
+    if (nv % 32 || (rpb != 1 && rpb != 2 && rpb != 4 && rpb != 8)) return false;
+    const int rpc = rpb * 4;
     size_t smem = 0;
     switch (variant) {
     case 1: smem = ClLayout<kMask5, 1>::smem_bytes(nx, rpc); break;
