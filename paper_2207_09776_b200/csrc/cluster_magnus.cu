@@ -60,7 +60,7 @@ struct NormAcc {
 };
 
 // CL CTAs per cluster, BANDS 128-thread row bands per CTA, RPB rows per band.
-template <int KRX, int KRV, uint64_t MASK, int RPB, int CL, int BANDS>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int RPB, int CL, int BANDS>
 __global__ void __launch_bounds__(BANDS * kBandThreads, (BANDS <= 2 ? 2 : 1)) cluster_magnus_kernel(ClusterArgs a) {
     constexpr int kCl = CL;
     constexpr int kBands = BANDS;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(BANDS * kBandThreads, (BANDS <= 2 ? 2 : 1)) cl
     const int p0 = lt < nint ? 2 * lt + 2 : (lt == nint ? 0 : nx - 2);
     const int clsA = lt < nint ? 2 : (lt == nint ? 0 : 3);
     const int clsB = lt < nint ? 2 : (lt == nint ? 1 : 4);
-    const bool wfast = __all_sync(0xffffffffu, lt < nint || !active);
+    const bool wfast = BM == 0 || __all_sync(0xffffffffu, lt < nint || !active);
     const int rb0 = band * RPB;
     const bool has_lo = rank > 0, has_hi = rank < kCl - 1;
 
@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(BANDS * kBandThreads, (BANDS <= 2 ? 2 : 1)) cl
                             } else {
                                 const double* yA = yrow + clsA * NBM;
                                 const double* yB = yrow + clsB * NBM;
+                            const double2* yi2 = reinterpret_cast<const double2*>(yrow + 2 * NBM);
 #pragma unroll
                                 for (int dv = -KRV; dv <= KRV; ++dv) {
                                     const int rr = ((ph - KRV + dv) % WROWS + WROWS) % WROWS;
@@ -249,8 +250,15 @@ __global__ void __launch_bounds__(BANDS * kBandThreads, (BANDS <= 2 ? 2 : 1)) cl
                                         if (MaskInfo<MASK>::has(dx, dv)) {
                                             const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
                                             const int col = H + dx - AOFF;
-                                            accA += yA[e] * win[rr][col];
-                                            accB += yB[e] * win[rr][col + 1];
+                                            double wA, wB;
+                                            if ((BM >> e) & 1) { // per-lane boundary value
+                                                wA = yA[e];
+                                                wB = yB[e];
+                                            } else { // interior value, broadcast
+                                                wA = wB = (e & 1) ? yi2[e >> 1].y : yi2[e >> 1].x;
+                                            }
+                                            accA += wA * win[rr][col];
+                                            accB += wB * win[rr][col + 1];
                                         }
                                     }
                                 }
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(BANDS * kBandThreads, (BANDS <= 2 ? 2 : 1)) cl
 template <int V, int RPB, int CL, int BANDS>
 void launch_vr(s2b_context* ctx, const ClusterArgs& a) {
     constexpr Variant v = kVariants[V];
-    auto kern = cluster_magnus_kernel<v.rx, v.rv, v.mask, RPB, CL, BANDS>;
+    auto kern = cluster_magnus_kernel<v.rx, v.rv, v.mask, v.bm, RPB, CL, BANDS>;
     const size_t smem = ClLayout<v.mask, v.rx>::smem_bytes(a.nx, RPB * BANDS);
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (CL > 8) S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -386,6 +394,8 @@ bool use_wide_cluster() {
 
 template <int V>
 void launch_v(s2b_context* ctx, const ClusterArgs& a) {
+    // the 16-CTA shape is instantiated only for the Langevin variants (compile time)
+    if constexpr (V >= 7)
     if (use_wide_cluster() && a.nv % (16 * 2) == 0) {
         switch (a.nv / (16 * 2)) {
         case 1: launch_vr<V, 1, 16, 2>(ctx, a); return;
@@ -406,7 +416,7 @@ void launch_v(s2b_context* ctx, const ClusterArgs& a) {
 } // namespace
 
 bool cluster_engine_supported(int variant, int nx, int nv) {
-    if (variant < 1 || variant > 4) return false;
+    if (variant < 1 || (variant > 4 && variant < 7) || variant > 9) return false;
     if (nx % 2 || nx < 6 || nx > 2 * kBandThreads) return false;
     const int rpb = nv / 32; // 8 CTAs x 4 bands (or 16 x 2)
     if (nv % 32 || (rpb != 1 && rpb != 2 && rpb != 4 && rpb != 8)) return false;
@@ -417,6 +427,9 @@ bool cluster_engine_supported(int variant, int nx, int nv) {
     case 2: smem = ClLayout<kMask11, 1>::smem_bytes(nx, rpc); break;
     case 3: smem = ClLayout<kMask19, 2>::smem_bytes(nx, rpc); break;
     case 4: smem = ClLayout<kBox22, 2>::smem_bytes(nx, rpc); break;
+    case 7: smem = ClLayout<kMask5, 1>::smem_bytes(nx, rpc); break;
+    case 8: smem = ClLayout<kMask11, 1>::smem_bytes(nx, rpc); break;
+    case 9: smem = ClLayout<kMask19, 2>::smem_bytes(nx, rpc); break;
     }
     return smem + 1024 <= 227 * 1024;
 }
@@ -427,6 +440,9 @@ void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterArgs& a) 
     case 2: launch_v<2>(ctx, a); break;
     case 3: launch_v<3>(ctx, a); break;
     case 4: launch_v<4>(ctx, a); break;
+    case 7: launch_v<7>(ctx, a); break;
+    case 8: launch_v<8>(ctx, a); break;
+    case 9: launch_v<9>(ctx, a); break;
     default: fail(S2B_ERR_RUNTIME, "cluster engine: unsupported variant");
     }
     S2B_LAUNCHED(ctx);

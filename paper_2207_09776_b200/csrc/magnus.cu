@@ -516,6 +516,34 @@ s2b_operator* make_operator(s2b_context* ctx, const s2b_grid* grid, int order,
                         wt[(j * nye + q) * kPairSlots + k] = hw[(static_cast<size_t>(pq) * nv + j) * kClasses + cls];
                 }
             }
+        // entries whose Y can differ between an x-boundary class and the interior, ignoring
+        // offsets that leave the grid from that class (their neighbour is zero padding, so
+        // the interior weight contributes the same +-0): the boundary warp loads only these
+        // per lane and broadcasts the interior value for the rest
+        const int cls_i[kClasses] = {0, 1, 2, static_cast<int>(nx) - 2, static_cast<int>(nx) - 1};
+        op->bmask = 0;
+        for (size_t e = 0; e < nbm; ++e) {
+            const int dx = e2bit[e] % kBoxW - kBoxR;
+            for (int cls : {0, 1, 3, 4}) {
+                const int i = cls_i[cls];
+                if (i + dx < 0 || i + dx >= static_cast<int>(nx)) continue; // leaves the grid
+                for (int k = 0; k < kPairSlots && !((op->bmask >> e) & 1); ++k)
+                    for (size_t j = 0; j < nv; ++j) {
+                        const double wb = wt[(j * nye + cls * nbm + e) * kPairSlots + k];
+                        const double wi = wt[(j * nye + 2 * nbm + e) * kPairSlots + k];
+                        if (std::memcmp(&wb, &wi, sizeof(double)) != 0) {
+                            op->bmask |= 1u << e;
+                            break;
+                        }
+                    }
+            }
+        }
+        // a specialised variant of the same mask whose compile-time boundary set covers bmask
+        // (same entry order, so wt/eslot stay valid)
+        for (int v = 1; v < kNumVariants; ++v)
+            if (kVariants[v].mask == kVariants[op->variant].mask && (op->bmask & ~kVariants[v].bm) == 0 &&
+                __builtin_popcount(kVariants[v].bm) < __builtin_popcount(kVariants[op->variant].bm))
+                op->variant = v;
         op->d_wt.alloc(wt.size());
         op->d_eslot.alloc(eslot.size());
         S2B_CUDA(cudaMemcpy(op->d_wt.p, wt.data(), wt.size() * sizeof(double), cudaMemcpyHostToDevice));

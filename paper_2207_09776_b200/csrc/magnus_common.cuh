@@ -167,19 +167,31 @@ constexpr uint64_t kBox22 = box_mask(2, 2);
 constexpr uint64_t kBox23 = box_mask(2, 3);
 constexpr uint64_t kBox33 = box_mask(3, 3);
 
+// bm: stencil entries (mask rank e) whose Y may differ on an x-boundary class at an in-grid
+// offset; the boundary warp loads those per lane and broadcasts the interior value for the
+// rest (bm == 0: boundary points use the interior Y outright).
 struct Variant {
     uint64_t mask;
     int rx, rv;
+    uint32_t bm;
 };
+constexpr uint32_t kBmAll = 0xFFFFFFFFu;
+// constant Langevin order 3: only (dx, dv) = (0, -1), (0, +1) differ at i = 0 and nx-1
+constexpr uint32_t kBm19c = (1u << MaskInfo<kMask19>::rank(box_bit(0, -1))) |
+                            (1u << MaskInfo<kMask19>::rank(box_bit(0, 1)));
 constexpr Variant kVariants[] = {
-    {0, 0, 0},        // 0: generic
-    {kMask5, 1, 1},   // 1
-    {kMask11, 1, 2},  // 2
-    {kMask19, 2, 2},  // 3
-    {kBox22, 2, 2},   // 4
-    {kBox23, 2, 3},   // 5
-    {kBox33, 3, 3},   // 6
+    {0, 0, 0, 0},             // 0: generic
+    {kMask5, 1, 1, kBmAll},   // 1
+    {kMask11, 1, 2, kBmAll},  // 2
+    {kMask19, 2, 2, kBmAll},  // 3
+    {kBox22, 2, 2, kBmAll},   // 4
+    {kBox23, 2, 3, kBmAll},   // 5
+    {kBox33, 3, 3, kBmAll},   // 6
+    {kMask5, 1, 1, 0},        // 7: Langevin order 1
+    {kMask11, 1, 2, 0},       // 8: Langevin order 2
+    {kMask19, 2, 2, kBm19c},  // 9: Langevin order 3 (constant coefficients)
 };
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 // Block-size classes: (max threads, min resident blocks) -> register budget.
 int tma_popcount(int variant);

@@ -94,6 +94,7 @@ struct s2b_operator {
     s2b::DevBuf<int> d_pair_begin, d_pair_slot;
     s2b::DevBuf<double> d_wt; // entry-major weights of the TMA kernel variant
     s2b::DevBuf<int> d_eslot;
+    uint32_t bmask = 0;       // Y entries that differ on x-boundary classes (in-grid offsets)
     // compressed: W[pair][j][cls]; full: W[pair][row]
     s2b::DevBuf<double> d_w;
     double dx_delta = 0.0, dv_delta = 0.0;

@@ -15,7 +15,7 @@ namespace mg {
 // (2KRV+1)-row register window of its x-neighbourhood.  The Y values of the next output row
 // (5 x-classes x the mask's stencil points) are folded one step ahead by their owner threads
 // (thread q < NYE) from entry-major weights loaded one step earlier into registers.
-template <int KRX, int KRV, uint64_t MASK, int NTMAX, int MINB>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NTMAX, int MINB>
 __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     constexpr int H = KRX <= 2 ? 2 : 4;             // zero halo (doubles) on each side
     constexpr int AOFF = (H - KRX) & ~1;            // first loaded smem index relative to p0
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     const int p0 = t < nint ? 2 * t + 2 : (t == nint ? 0 : nx - 2);
     const int clsA = t < nint ? 2 : (t == nint ? 0 : 3);
     const int clsB = t < nint ? 2 : (t == nint ? 1 : 4);
-    const bool wfast = __all_sync(0xffffffffu, t < nint || !active);
+    const bool wfast = BM == 0 || __all_sync(0xffffffffu, t < nint || !active);
 
     // Y entry owned by this thread (q = t < NYE; the launch makes NT >= NYE)
     const bool owner = t < NYE;
@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                         } else {
                             const double* yA = yrow + clsA * NBM;
                             const double* yB = yrow + clsB * NBM;
+                            const double2* yi2 = reinterpret_cast<const double2*>(yrow + 2 * NBM);
 #pragma unroll
                             for (int dv = -KRV; dv <= KRV; ++dv) {
                                 const int rr = ((ph - KRV + dv) % WROWS + WROWS) % WROWS;
@@ -207,8 +208,15 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                                     if (MaskInfo<MASK>::has(dx, dv)) {
                                         const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
                                         const int col = H + dx - AOFF;
-                                        accA += yA[e] * win[rr][col];
-                                        accB += yB[e] * win[rr][col + 1];
+                                        double wA, wB;
+                                        if ((BM >> e) & 1) { // per-lane boundary value
+                                            wA = yA[e];
+                                            wB = yB[e];
+                                        } else { // interior value, broadcast
+                                            wA = wB = (e & 1) ? yi2[e >> 1].y : yi2[e >> 1].x;
+                                        }
+                                        accA += wA * win[rr][col];
+                                        accB += wB * win[rr][col + 1];
                                     }
                                 }
                             }
@@ -259,7 +267,7 @@ template <> struct NtClass<512> { static constexpr int minb = 1; };
 template <int V, int NTMAX>
 void launch_term_nt(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, size_t work) {
     constexpr Variant v = kVariants[V];
-    auto kern = term_tma_kernel<v.rx, v.rv, v.mask, NTMAX, NtClass<NTMAX>::minb>;
+    auto kern = term_tma_kernel<v.rx, v.rv, v.mask, v.bm, NTMAX, NtClass<NTMAX>::minb>;
     static int configured_device = -1;
     if (configured_device != ctx->device) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

@@ -12,6 +12,9 @@ void launch_term_nt512(s2b_context* ctx, int variant, const TermArgs& a, int nt,
     case 4: launch_term_nt<4, 512>(ctx, a, nt, smem, work); return;
     case 5: launch_term_nt<5, 512>(ctx, a, nt, smem, work); return;
     case 6: launch_term_nt<6, 512>(ctx, a, nt, smem, work); return;
+    case 7: launch_term_nt<7, 512>(ctx, a, nt, smem, work); return;
+    case 8: launch_term_nt<8, 512>(ctx, a, nt, smem, work); return;
+    case 9: launch_term_nt<9, 512>(ctx, a, nt, smem, work); return;
     }
     fail(S2B_ERR_RUNTIME, "term kernel: unknown variant");
 }
