@@ -1,0 +1,429 @@
+// Cluster-resident Magnus engine, x-march layout (the default for the Langevin variants).
+//
+// Same cluster decomposition as cluster_magnus.cu (one 8-CTA cluster per path, CTA `rank`
+// owns rows [rank*RPC, (rank+1)*RPC), all Taylor terms of a window on chip), but the work
+// is laid out so that the generator Y costs nothing inside the term loop:
+//  * lane = row.  Thread (r, seg) owns row r of the CTA and the x-segment
+//    [seg*L, (seg+1)*L); it marches along x.  Y is x-invariant away from the two x-boundary
+//    columns on each side (the compressed operator), so the thread's row of Y lives in
+//    registers for the whole window (the y_j of MagnusLogBuilder::fill, magnus.cpp:141-160)
+//    and the march only loads the term: one value per stencil row per point, from a
+//    per-row register ring.
+//  * T and S are stored x-major ([x][row]): a warp's 32 lanes read 32 consecutive rows of
+//    one column (conflict-free), and every offset of the unrolled march is an immediate.
+//  * The KRV halo rows of the neighbours are pushed by the producer with DSMEM stores as
+//    each term is computed, so the one cluster barrier per term (needed anyway for the
+//    path-wide norms of expmv_into's stopping rule, sparse.cpp:463-492) also publishes the
+//    halos.
+//  * Path-wide maxima: 32-bit REDUX on the (hi, lo) words of the non-negative doubles,
+//    every warp re-derives the decision from the 8 CTA slots (no broadcast barrier).
+// The arithmetic per point is unchanged: Y.t summed from 0.0 in ascending (dv, dx) order
+// (== ascending DIA diagonal, sparse.cpp:412-423), t = acc * (1/(s*k)), S += t, no FMA.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "magnus_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace s2b {
+namespace mg {
+
+namespace {
+
+constexpr int kXmCl = 8;
+
+template <uint64_t MASK>
+struct RowExt {
+    static constexpr int lo(int dv) {
+        for (int dx = -kBoxR; dx <= kBoxR; ++dx)
+            if (MaskInfo<MASK>::has(dx, dv)) return dx;
+        return 1;
+    }
+    static constexpr int hi(int dv) {
+        for (int dx = kBoxR; dx >= -kBoxR; --dx)
+            if (MaskInfo<MASK>::has(dx, dv)) return dx;
+        return 0;
+    }
+    static constexpr int span(int dv) { return hi(dv) - lo(dv) + 1; }
+    static constexpr int off(int dv) {
+        int o = 0;
+        for (int d = -kBoxR; d < dv; ++d) o += span(d);
+        return o;
+    }
+    static constexpr int total() { return off(kBoxR + 1); }
+};
+
+__host__ __device__ constexpr int popc32(uint32_t v) { return v == 0 ? 0 : static_cast<int>(v & 1u) + popc32(v >> 1); }
+__host__ __device__ constexpr int bm_rank(uint32_t bm, int e) { return popc32(bm & ((1u << e) - 1u)); }
+
+template <uint64_t MASK, int KRX, int KRV, uint32_t BM, int NX, int RPC>
+struct XmLayout {
+    static constexpr int TR = RPC + 2 * KRV; // rows incl. halo
+    static constexpr int TX = NX + 2 * KRX;  // columns incl. zero x-halo
+    static constexpr int TBUF = TX * TR;
+    static constexpr int NBM = MaskInfo<MASK>::count();
+    static constexpr int NYE = kClasses * NBM;
+    static constexpr int NBB = popc32(BM);
+    static constexpr int SCR = RPC * (NX + 1); // row-major padded scratch (in T[1])
+    static constexpr size_t bytes() {
+        return 8 * (2 * static_cast<size_t>(TBUF) + static_cast<size_t>(NX) * RPC + 4 * static_cast<size_t>(NBB) * RPC);
+    }
+    static_assert(SCR <= TBUF, "transpose scratch must fit one term buffer");
+    static_assert(RPC * NYE <= TBUF, "Y fold scratch must fit one term buffer");
+};
+
+// max over a warp of non-negative doubles (or +NaN), as their bit patterns
+__device__ __forceinline__ unsigned long long warp_max_bits(unsigned long long b) {
+    const unsigned hi = static_cast<unsigned>(b >> 32), lo = static_cast<unsigned>(b);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return (static_cast<unsigned long long>(mh) << 32) | ml;
+}
+
+__device__ __forceinline__ unsigned long long dbits(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v));
+}
+
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT>
+__global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
+    using L = XmLayout<MASK, KRX, KRV, BM, NX, RPC>;
+    using RE = RowExt<MASK>;
+    constexpr int TR = L::TR, TX = L::TX, TBUF = L::TBUF;
+    constexpr int NBM = L::NBM, NYE = L::NYE, NBB = L::NBB;
+    constexpr int NSEG = NT / RPC;
+    constexpr int LX = NX / NSEG; // points per thread along x
+    constexpr int NW = NT / 32;
+    constexpr int KP = kPairSlots;
+    constexpr int NWIN = RE::total();
+    static_assert(NT % RPC == 0 && NX % NSEG == 0 && LX >= 4, "x-march shape");
+    static_assert(RPC >= 2 * KRV, "halo rows come from one neighbour");
+
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const int r = t % RPC;
+    const int seg = t / RPC;
+    const int x0 = seg * LX;
+    const int row0 = rank * RPC;
+    const int nx = NX;
+    const int n = NX * a.nv;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* T = reinterpret_cast<double*>(smem_raw); // [2][TX][TR]
+    double* S = T + 2 * TBUF;                        // [NX][RPC]
+    double* bY = S + NX * RPC;                       // [4][NBB][RPC] boundary-class Y
+    double* scr = T + TBUF;                          // scratch aliasing T[1]
+    __shared__ unsigned long long slots[2][kXmCl][2]; // CTA maxima of every rank, per parity
+    __shared__ unsigned long long red[NW][2];
+    __shared__ double c[6];
+    __shared__ int next_path;
+
+    for (int q = t; q < 2 * TBUF; q += NT) T[q] = 0.0;
+
+    const bool has_lo = rank > 0, has_hi = rank < kXmCl - 1;
+    // DSMEM halo push: rows r < KRV go to the lower neighbour's rows RPC + r, rows
+    // r >= RPC - KRV to the upper neighbour's rows r - RPC
+    double* rem = nullptr;
+    if (r < KRV && has_lo)
+        rem = cluster.map_shared_rank(T, rank - 1) + (x0 + KRX) * TR + (RPC + r + KRV);
+    else if (r >= RPC - KRV && has_hi)
+        rem = cluster.map_shared_rank(T, rank + 1) + (x0 + KRX) * TR + (r - RPC + KRV);
+    const bool do_rem = rem != nullptr;
+    unsigned long long* slot_dst = cluster.map_shared_rank(&slots[0][0][0], lane < kXmCl ? lane : 0);
+    int* next0 = cluster.map_shared_rank(&next_path, 0);
+
+    // own (row, x) element offsets
+    const int tb = (x0 + KRX) * TR + (r + KRV); // in a T buffer
+    const int sb = x0 * RPC + r;                // in S
+
+    // global <-> x-major S through the padded row-major scratch (coalesced both ways)
+    auto load_state = [&](const double* g) {
+        for (int q = t; q < RPC * NX; q += NT) scr[(q / NX) * (NX + 1) + q % NX] = g[q];
+        __syncthreads();
+        for (int q = t; q < RPC * NX; q += NT) S[q] = scr[(q % RPC) * (NX + 1) + q / RPC];
+        __syncthreads();
+    };
+    auto store_state = [&](double* g) {
+        for (int q = t; q < RPC * NX; q += NT) scr[(q % RPC) * (NX + 1) + q / RPC] = S[q];
+        __syncthreads();
+        for (int q = t; q < RPC * NX; q += NT) g[q] = scr[(q / NX) * (NX + 1) + q % NX];
+        __syncthreads();
+    };
+    // T[1] held scratch: restore its zero halo (x columns; outer rows of the edge CTAs)
+    auto clear_t1 = [&]() {
+        for (int q = t; q < TBUF; q += NT) scr[q] = 0.0;
+        __syncthreads();
+    };
+
+    uint32_t gterm = 0;
+
+    while (true) {
+        if (rank == 0 && t == 0) next_path = atomicAdd(a.work, 1);
+        cluster.sync();
+        const int p = *next0;
+        cluster.sync();
+        if (p >= a.M) break;
+        if (a.status[p] != 0) continue;
+
+        const int par = a.par[p];
+        double* gstate = (par ? a.S1 : a.S0) + static_cast<size_t>(p) * n + static_cast<size_t>(row0) * nx;
+        load_state(gstate);
+        clear_t1();
+
+        int w = a.win0, rec = a.rec_next[p];
+        long long terms = 0, windows = 0, segments = 0;
+        bool blown = false;
+        double sn_last = 0.0;
+
+        auto do_records = [&](int wdone) {
+            const long long step = static_cast<long long>(wdone + 1) * a.dt_steps;
+            while (rec < a.R && a.rec_steps[rec] == step) {
+                if (rec < a.R - 1) {
+                    store_state(a.rec[rec] + static_cast<size_t>(p) * n + static_cast<size_t>(row0) * nx);
+                    clear_t1();
+                }
+                if (rank == 0 && t == 0) a.rec_status[static_cast<size_t>(rec) * a.M + p] = 0;
+                ++rec;
+            }
+        };
+
+        while (w < a.win1 && !blown) {
+            const int sw = a.stab[static_cast<size_t>(p) * a.nwin + w];
+            if (sw == 0) { // norm == 0: exp(Y)u = u (sparse.cpp:449)
+                ++windows;
+                do_records(w);
+                ++w;
+                continue;
+            }
+            if (t < 6) c[t] = a.ctab[(static_cast<size_t>(p) * a.nwin + w) * 6 + t];
+            __syncthreads();
+            // fill's fold for this CTA's rows, slots ascending from 0.0, into scratch
+            for (int q = t; q < RPC * NYE; q += NT) {
+                const int rr = q / NYE, e = q - rr * NYE;
+                const double* wr = a.wt + (static_cast<size_t>(row0 + rr) * NYE + e) * KP;
+                double y = 0.0;
+#pragma unroll
+                for (int k = 0; k < KP; ++k) {
+                    const int sl = __ldg(a.eslot + e * KP + k);
+                    if (sl < 0) continue;
+                    const double cs = c[sl];
+                    if (cs != 0.0) y += cs * __ldg(wr + k);
+                }
+                scr[q] = y;
+            }
+            __syncthreads();
+            double y[NBM]; // interior (class 2) Y of row r
+#pragma unroll
+            for (int e = 0; e < NBM; ++e) y[e] = scr[r * NYE + 2 * NBM + e];
+            if constexpr (NBB > 0) {
+                for (int q = t; q < 4 * NBB * RPC; q += NT) {
+                    const int rr = q % RPC, eb = (q / RPC) % NBB, k4 = q / (RPC * NBB);
+                    const int cls = k4 < 2 ? k4 : k4 + 1;
+                    int e = 0;
+                    for (int m = 0, seen = 0; m < 32; ++m)
+                        if ((BM >> m) & 1) {
+                            if (seen == eb) {
+                                e = m;
+                                break;
+                            }
+                            ++seen;
+                        }
+                    bY[q] = scr[rr * NYE + cls * NBM + e];
+                }
+            }
+            __syncthreads();
+            clear_t1();
+
+            for (int sgi = 0; sgi < sw && !blown; ++sgi) {
+                // segment start: term = accum = y (sparse.cpp:452-453); halos to neighbours
+#pragma unroll
+                for (int i = 0; i < LX; ++i) {
+                    const double v = S[sb + i * RPC];
+                    T[tb + i * TR] = v;
+                    if (do_rem) rem[i * TR] = v;
+                }
+                int cur = 0;
+                cluster.sync();
+                double prev = __longlong_as_double(static_cast<long long>(kInfBits));
+                bool converged = false;
+                for (int k = 1; k <= kMaxTerms; ++k) {
+                    const double inv = 1.0 / (static_cast<double>(sw) * k);
+                    const double* tin = T + cur * TBUF + tb;
+                    double* tout = T + (cur ^ 1) * TBUF + tb;
+                    double* rout = rem + (cur ^ 1) * TBUF;
+                    double* sp = S + sb;
+                    double tm = 0.0, sm = 0.0;
+                    double win[NWIN > 0 ? NWIN : 1];
+                    // prime the per-row rings with columns lo .. hi-1
+#pragma unroll
+                    for (int dv = -KRV; dv <= KRV; ++dv) {
+                        if (RE::span(dv) > 0) {
+#pragma unroll
+                            for (int cc = 0; cc < RE::span(dv) - 1; ++cc)
+                                win[RE::off(dv) + cc] = tin[(RE::lo(dv) + cc) * TR + dv];
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < LX; ++i) {
+#pragma unroll
+                        for (int dv = -KRV; dv <= KRV; ++dv)
+                            if (RE::span(dv) > 0)
+                                win[RE::off(dv) + (i + RE::span(dv) - 1) % RE::span(dv)] =
+                                    tin[(i + RE::hi(dv)) * TR + dv];
+                        // x-class of this point (boundary only in the first / last segment)
+                        int bcls = -1;
+                        if constexpr (NBB > 0) {
+                            if (i < 2 && seg == 0) bcls = i;
+                            if (i >= LX - 2 && seg == NSEG - 1) bcls = 2 + (i - (LX - 2));
+                        }
+                        double acc = 0.0;
+#pragma unroll
+                        for (int dv = -KRV; dv <= KRV; ++dv) {
+#pragma unroll
+                            for (int dx = -KRX; dx <= KRX; ++dx) {
+                                if (MaskInfo<MASK>::has(dx, dv)) {
+                                    const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
+                                    double wv = y[e];
+                                    if constexpr (NBB > 0) {
+                                        if ((BM >> e) & 1) {
+                                            if (bcls >= 0) wv = bY[(bcls * NBB + bm_rank(BM, e)) * RPC + r];
+                                        }
+                                    }
+                                    const int slot = RE::off(dv) + (i + dx - RE::lo(dv)) % RE::span(dv);
+                                    acc += wv * win[slot];
+                                }
+                            }
+                        }
+                        const double tv = acc * inv;
+                        const double sv = sp[i * RPC] + tv;
+                        tout[i * TR] = tv;
+                        if (do_rem) rout[i * TR] = tv;
+                        sp[i * RPC] = sv;
+                        const double at = fabs(tv), as = fabs(sv);
+                        tm = at > tm ? at : tm;
+                        sm = (as > sm || sv != sv) ? as : sm; // NaN sticks
+                    }
+                    // path-wide max|t|, max|accum| (NaN-ranked): warps -> CTA -> every rank
+                    const unsigned long long wtb = warp_max_bits(dbits(tm));
+                    const unsigned long long wsb = warp_max_bits(dbits(sm));
+                    if (lane == 0) {
+                        red[warp][0] = wtb;
+                        red[warp][1] = wsb;
+                    }
+                    __syncthreads();
+                    const int kp = gterm & 1;
+                    if (warp == 0) {
+                        const unsigned long long ct = warp_max_bits(lane < NW ? red[lane][0] : 0ull);
+                        const unsigned long long cs = warp_max_bits(lane < NW ? red[lane][1] : 0ull);
+                        if (lane < kXmCl) {
+                            slot_dst[(kp * kXmCl + rank) * 2 + 0] = ct;
+                            slot_dst[(kp * kXmCl + rank) * 2 + 1] = cs;
+                        }
+                    }
+                    cluster.sync();
+                    const unsigned long long tball = warp_max_bits(lane < kXmCl ? slots[kp][lane][0] : 0ull);
+                    const unsigned long long sball = warp_max_bits(lane < kXmCl ? slots[kp][lane][1] : 0ull);
+                    int dec = 0;
+                    if (tball >= kInfBits || sball >= kInfBits) {
+                        dec = 2; // Overflow
+                    } else {
+                        const double tn = __longlong_as_double(static_cast<long long>(tball));
+                        const double sn = __longlong_as_double(static_cast<long long>(sball));
+                        const double gate = a.tol * sn;
+                        if (tn <= gate && prev <= gate) dec = 1;
+                        prev = tn;
+                        sn_last = sn;
+                    }
+                    ++gterm;
+                    ++terms;
+                    cur ^= 1;
+                    if (dec == 2) {
+                        blown = true;
+                        break;
+                    }
+                    if (dec == 1) {
+                        converged = true;
+                        break;
+                    }
+                }
+                if (!blown && !converged) blown = true; // ToleranceNotReached
+                if (!blown) ++segments;
+            }
+            if (blown) break;
+            // window-level cap (magnus.cpp:282-286)
+            if (sn_last > a.cap) {
+                blown = true;
+                break;
+            }
+            ++windows;
+            do_records(w);
+            ++w;
+        }
+        if (!blown) store_state(gstate);
+        if (rank == 0 && t == 0) {
+            a.terms[p] += terms;
+            a.windows[p] += windows;
+            a.segments[p] += segments;
+            a.rec_next[p] = rec;
+            a.win[p] = w;
+            a.status[p] = blown ? 2 : (w >= a.nwin ? 1 : 0);
+        }
+        // the next path reuses every buffer (and the neighbours push halos into ours)
+        cluster.sync();
+    }
+}
+
+template <int V, int NX, int RPC, int NT>
+void launch_xm(s2b_context* ctx, const ClusterArgs& a) {
+    constexpr Variant v = kVariants[V];
+    auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT>;
+    const size_t smem = XmLayout<v.mask, v.rx, v.rv, v.bm, NX, RPC>::bytes();
+    S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kXmCl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(kXmCl);
+    int clusters = 0;
+    S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
+    clusters = std::max(1, std::min(clusters, a.M));
+    cfg.gridDim = dim3(kXmCl * clusters);
+    S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
+bool xm_enabled() {
+    const char* e = std::getenv("S2B_XM");
+    return !(e && e[0] == '0');
+}
+
+} // namespace
+
+bool cluster_xm_supported(int variant, int nx, int nv) {
+    if (!xm_enabled()) return false;
+    if (variant < 7 || variant > 9) return false;
+    return nx == 256 && nv == 256;
+}
+
+void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterArgs& a) {
+    switch (variant) {
+    case 7: launch_xm<7, 256, 32, 512>(ctx, a); break;
+    case 8: launch_xm<8, 256, 32, 512>(ctx, a); break;
+    case 9: launch_xm<9, 256, 32, 512>(ctx, a); break;
+    default: fail(S2B_ERR_RUNTIME, "x-march cluster engine: unsupported variant");
+    }
+    S2B_LAUNCHED(ctx);
+}
+
+} // namespace mg
+} // namespace s2b

@@ -228,6 +228,9 @@ struct ClusterArgs {
 };
 bool cluster_engine_supported(int variant, int nx, int nv);
 void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterArgs& a);
+// x-march variant of the cluster engine (cluster_xm.cu); S2B_XM=0 disables it
+bool cluster_xm_supported(int variant, int nx, int nv);
+void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterArgs& a);
 
 } // namespace mg
 } // namespace s2b
