@@ -34,6 +34,14 @@ namespace mg {
 namespace {
 
 constexpr int kXmCl = 8;
+#ifndef S2B_XM_P
+#define S2B_XM_P 4
+#endif
+constexpr int kXmP = S2B_XM_P; // points in flight per thread (ILP of the stencil sums)
+#ifndef S2B_XM_NT
+#define S2B_XM_NT 256
+#endif
+constexpr int kXmNT = S2B_XM_NT; // threads per CTA
 
 template <uint64_t MASK>
 struct RowExt {
@@ -83,11 +91,21 @@ __device__ __forceinline__ unsigned long long warp_max_bits(unsigned long long b
     return (static_cast<unsigned long long>(mh) << 32) | ml;
 }
 
+// cluster barrier: release/acquire at cluster scope (covers the DSMEM halo stores)
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// |v| by clearing the sign bit (an integer op: no fp64 instruction)
+__device__ __forceinline__ double abs_of(double v) {
+    return __hiloint2double(__double2hiint(v) & 0x7fffffff, __double2loint(v));
+}
+
 __device__ __forceinline__ unsigned long long dbits(double v) {
     return static_cast<unsigned long long>(__double_as_longlong(v));
 }
 
-template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P>
 __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
     using L = XmLayout<MASK, KRX, KRV, BM, NX, RPC>;
     using RE = RowExt<MASK>;
@@ -98,6 +116,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
     constexpr int NW = NT / 32;
     constexpr int KP = kPairSlots;
     constexpr int NWIN = RE::total();
+    // ring geometry with P points in flight: span + P - 1 slots per stencil row
+#define RSPAN(dv) (RE::span(dv) + P - 1)
+#define ROFF(dv) (RE::off(dv) + ((dv) + KRV) * (P - 1))
+    static_assert(LX % P == 0, "points per thread must be a multiple of P");
     static_assert(NT % RPC == 0 && NX % NSEG == 0 && LX >= 4, "x-march shape");
     static_assert(RPC >= 2 * KRV, "halo rows come from one neighbour");
 
@@ -163,9 +185,9 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
 
     while (true) {
         if (rank == 0 && t == 0) next_path = atomicAdd(a.work, 1);
-        cluster.sync();
+        cluster_barrier();
         const int p = *next0;
-        cluster.sync();
+        cluster_barrier();
         if (p >= a.M) break;
         if (a.status[p] != 0) continue;
 
@@ -247,7 +269,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
                     if (do_rem) rem[i * TR] = v;
                 }
                 int cur = 0;
-                cluster.sync();
+                cluster_barrier();
                 double prev = __longlong_as_double(static_cast<long long>(kInfBits));
                 bool converged = false;
                 for (int k = 1; k <= kMaxTerms; ++k) {
@@ -256,57 +278,79 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
                     double* tout = T + (cur ^ 1) * TBUF + tb;
                     double* rout = rem + (cur ^ 1) * TBUF;
                     double* sp = S + sb;
-                    double tm = 0.0, sm = 0.0;
-                    double win[NWIN > 0 ? NWIN : 1];
-                    // prime the per-row rings with columns lo .. hi-1
+                    double tm = 0.0, sm = 0.0; // NaN-ignoring maxima of |t|, |accum|
+                    unsigned ex = 0;           // max exponent field of accum: all-ones = non-finite
+                    // per-row register rings over absolute columns c (slot (c - lo) mod R),
+                    // R = span + P - 1 so that P adjacent points are in flight
+                    double win[NWIN + (2 * KRV + 1) * (P - 1)];
 #pragma unroll
                     for (int dv = -KRV; dv <= KRV; ++dv) {
                         if (RE::span(dv) > 0) {
 #pragma unroll
                             for (int cc = 0; cc < RE::span(dv) - 1; ++cc)
-                                win[RE::off(dv) + cc] = tin[(RE::lo(dv) + cc) * TR + dv];
+                                win[ROFF(dv) + cc] = tin[(RE::lo(dv) + cc) * TR + dv];
                         }
                     }
 #pragma unroll
-                    for (int i = 0; i < LX; ++i) {
+                    for (int i0 = 0; i0 < LX; i0 += P) {
 #pragma unroll
                         for (int dv = -KRV; dv <= KRV; ++dv)
-                            if (RE::span(dv) > 0)
-                                win[RE::off(dv) + (i + RE::span(dv) - 1) % RE::span(dv)] =
-                                    tin[(i + RE::hi(dv)) * TR + dv];
-                        // x-class of this point (boundary only in the first / last segment)
-                        int bcls = -1;
-                        if constexpr (NBB > 0) {
-                            if (i < 2 && seg == 0) bcls = i;
-                            if (i >= LX - 2 && seg == NSEG - 1) bcls = 2 + (i - (LX - 2));
+                            if (RE::span(dv) > 0) {
+#pragma unroll
+                                for (int q = 0; q < P; ++q) {
+                                    const int col = i0 + q + RE::hi(dv);
+                                    win[ROFF(dv) + (col - RE::lo(dv)) % RSPAN(dv)] = tin[col * TR + dv];
+                                }
+                            }
+                        // x-class of each point (boundary only in the first / last segment)
+                        int bcls[P];
+#pragma unroll
+                        for (int q = 0; q < P; ++q) {
+                            const int i = i0 + q;
+                            bcls[q] = -1;
+                            if constexpr (NBB > 0) {
+                                if (i < 2 && seg == 0) bcls[q] = i;
+                                if (i >= LX - 2 && seg == NSEG - 1) bcls[q] = 2 + (i - (LX - 2));
+                            }
                         }
-                        double acc = 0.0;
+                        double acc[P];
+#pragma unroll
+                        for (int q = 0; q < P; ++q) acc[q] = 0.0;
 #pragma unroll
                         for (int dv = -KRV; dv <= KRV; ++dv) {
 #pragma unroll
                             for (int dx = -KRX; dx <= KRX; ++dx) {
                                 if (MaskInfo<MASK>::has(dx, dv)) {
                                     const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
-                                    double wv = y[e];
-                                    if constexpr (NBB > 0) {
-                                        if ((BM >> e) & 1) {
-                                            if (bcls >= 0) wv = bY[(bcls * NBB + bm_rank(BM, e)) * RPC + r];
+#pragma unroll
+                                    for (int q = 0; q < P; ++q) {
+                                        double wv = y[e];
+                                        if constexpr (NBB > 0) {
+                                            if ((BM >> e) & 1) {
+                                                if (bcls[q] >= 0)
+                                                    wv = bY[(bcls[q] * NBB + bm_rank(BM, e)) * RPC + r];
+                                            }
                                         }
+                                        const int col = i0 + q + dx;
+                                        acc[q] += wv * win[ROFF(dv) + (col - RE::lo(dv)) % RSPAN(dv)];
                                     }
-                                    const int slot = RE::off(dv) + (i + dx - RE::lo(dv)) % RE::span(dv);
-                                    acc += wv * win[slot];
                                 }
                             }
                         }
-                        const double tv = acc * inv;
-                        const double sv = sp[i * RPC] + tv;
-                        tout[i * TR] = tv;
-                        if (do_rem) rout[i * TR] = tv;
-                        sp[i * RPC] = sv;
-                        const double at = fabs(tv), as = fabs(sv);
-                        tm = at > tm ? at : tm;
-                        sm = (as > sm || sv != sv) ? as : sm; // NaN sticks
+#pragma unroll
+                        for (int q = 0; q < P; ++q) {
+                            const int i = i0 + q;
+                            const double tv = acc[q] * inv;
+                            const double sv = sp[i * RPC] + tv;
+                            tout[i * TR] = tv;
+                            if (do_rem) rout[i * TR] = tv;
+                            sp[i * RPC] = sv;
+                            if (fabs(tv) > tm) tm = abs_of(tv);
+                            if (fabs(sv) > sm) sm = abs_of(sv);
+                            ex = max(ex, static_cast<unsigned>(__double2hiint(sv)) & 0x7ff00000u);
+                        }
                     }
+                    if (ex == 0x7ff00000u) sm = __longlong_as_double(0x7FF8000000000000LL); // non-finite
                     // path-wide max|t|, max|accum| (NaN-ranked): warps -> CTA -> every rank
                     const unsigned long long wtb = warp_max_bits(dbits(tm));
                     const unsigned long long wsb = warp_max_bits(dbits(sm));
@@ -324,7 +368,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
                             slot_dst[(kp * kXmCl + rank) * 2 + 1] = cs;
                         }
                     }
-                    cluster.sync();
+                    cluster_barrier();
                     const unsigned long long tball = warp_max_bits(lane < kXmCl ? slots[kp][lane][0] : 0ull);
                     const unsigned long long sball = warp_max_bits(lane < kXmCl ? slots[kp][lane][1] : 0ull);
                     int dec = 0;
@@ -373,14 +417,14 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
             a.status[p] = blown ? 2 : (w >= a.nwin ? 1 : 0);
         }
         // the next path reuses every buffer (and the neighbours push halos into ours)
-        cluster.sync();
+        cluster_barrier();
     }
 }
 
 template <int V, int NX, int RPC, int NT>
 void launch_xm(s2b_context* ctx, const ClusterArgs& a) {
     constexpr Variant v = kVariants[V];
-    auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT>;
+    auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT, kXmP>;
     const size_t smem = XmLayout<v.mask, v.rx, v.rv, v.bm, NX, RPC>::bytes();
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
@@ -417,9 +461,9 @@ bool cluster_xm_supported(int variant, int nx, int nv) {
 
 void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterArgs& a) {
     switch (variant) {
-    case 7: launch_xm<7, 256, 32, 512>(ctx, a); break;
-    case 8: launch_xm<8, 256, 32, 512>(ctx, a); break;
-    case 9: launch_xm<9, 256, 32, 512>(ctx, a); break;
+    case 7: launch_xm<7, 256, 32, kXmNT>(ctx, a); break;
+    case 8: launch_xm<8, 256, 32, kXmNT>(ctx, a); break;
+    case 9: launch_xm<9, 256, 32, kXmNT>(ctx, a); break;
     default: fail(S2B_ERR_RUNTIME, "x-march cluster engine: unsupported variant");
     }
     S2B_LAUNCHED(ctx);
