@@ -31,7 +31,31 @@ sys.path.insert(0, ROOT)
 A_LANGEVIN = 1.1
 SIGMA = 1.0 / np.sqrt(10.0)
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "term_kernel_ncu.json")
+# Magnus engines (s2b_magnus_stats.engine) -> dominant kernel and its ncu summary in profiles/
+ENGINES = {
+    0: {"name": "stream", "kernel": "term_tma_kernel", "profile": "term_kernel_ncu.json",
+        "note": "streaming pass engine: term and accumulator round-trip HBM every Taylor term"},
+    1: {"name": "cluster-band", "kernel": "cluster_magnus_kernel", "profile": "cluster_kernel_ncu.json",
+        "note": "cluster-resident: the path stays in shared memory for the window; achieved is the "
+                "streaming-equivalent rate (can exceed HBM peak), traffic the real DRAM bytes"},
+    2: {"name": "cluster-xm", "kernel": "cluster_xm_kernel", "profile": "xm_kernel_ncu.json",
+        "note": "cluster-resident x-march: the path stays in shared memory for the window; achieved is "
+                "the streaming-equivalent rate (can exceed HBM peak), traffic the real DRAM bytes; the "
+                "binding limit is the fp64 pipe (compute_roofline)"},
+}
+
+
+def stencil_points(order):
+    """Union stencil of the constant Langevin family."""
+    return {1: 5, 2: 11, 3: 19}[order]
+
+
+def fp64_peak_tops():
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["dmul_dadd_tops"])
+    except Exception:
+        return None
 
 
 def parse():
@@ -237,23 +261,36 @@ def run_ours(args):
     ms_max = max_over_ranks(ms, dist, local)
     value = world * M * n * args.steps / (ms_max / 1e3)
 
-    # roofline of the dominant kernel (term_tma_kernel): algorithmic bytes per Taylor term
+    # roofline of the dominant kernel: algorithmic bytes per Taylor term (32 B per
+    # path*gridpoint*term, 24 B for the k=1 term of a segment), over that kernel's event time
     terms = st1["path_terms"] - st0["path_terms"]
     segs = st1["path_segments"] - st0["path_segments"]
     alg_bytes = n * (32.0 * (terms - segs) + 24.0 * segs)
     tk_ms = st1["term_kernel_ms"] - st0["term_kernel_ms"]
     tk_launches = st1["term_launches"] - st0["term_launches"]
+    engine = ENGINES.get(st1.get("engine", 0), ENGINES[0])
     peak, peak_kind = peaks()
     achieved = alg_bytes / (tk_ms / 1e3) / 1e9 if tk_ms > 0 else 0.0
     traffic = None
+    prof = {}
     try:
-        with open(PROFILE_SUMMARY) as f:
+        with open(os.path.join(ROOT, "profiles", engine["profile"])) as f:
             prof = json.load(f)
-        traffic = prof.get("dram_bytes_per_path_term")
-        if traffic is not None:
-            traffic = traffic * terms / max(tk_launches, 1)
+        if engine["name"] == "stream" and prof.get("dram_bytes_per_path_term") is not None:
+            traffic = prof["dram_bytes_per_path_term"] * terms / max(tk_launches, 1)
+        elif prof.get("dram_bytes_per_path_window") is not None:
+            traffic = prof["dram_bytes_per_path_window"] * M * args.steps / max(tk_launches, 1)
     except Exception:
         pass
+    # the on-chip engines are bound by the fp64 pipe, not HBM: report that ceiling beside it
+    # (DMUL + DADD per stencil point, no FMA for bitwise parity; +1 DMUL, +1 DADD per point)
+    fp64_ops = n * terms * (2.0 * stencil_points(args.order) + 2.0)
+    fp64_peak = fp64_peak_tops()
+    compute = {"bound": "fp64", "achieved": fp64_ops / (tk_ms / 1e3) / 1e12 if tk_ms > 0 else 0.0,
+               "peak": fp64_peak, "unit": "TFLOP/s (DMUL/DADD, non-FMA)",
+               "ops_model": f"{2 * stencil_points(args.order) + 2} fp64 ops per path*gridpoint*term",
+               "ncu_fp64_pipe_pct_of_active": prof.get("fp64_pipe_pct_of_active")}
+    compute["frac"] = compute["achieved"] / fp64_peak if fp64_peak else None
 
     # end-to-end through the C ABI with host buffers: per step the window's Brownian prefix
     # values go H2D from pinned memory, the window runs, the moment statistics come back D2H
@@ -310,9 +347,12 @@ def run_ours(args):
         "path_gridpoint_terms_per_s": world * n * terms / (ms_max / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "term_tma_kernel", "launches": tk_launches,
+                     "kernel": engine["kernel"], "engine": engine["name"], "launches": tk_launches,
                      "kernel_ms": tk_ms,
-                     "bytes_model": "32 B per path*gridpoint*term (24 B for the k=1 term of a segment)"},
+                     "bytes_model": "32 B per path*gridpoint*term (24 B for the k=1 term of a segment)",
+                     "traffic_source": f"profiles/{engine['profile']} (ncu dram__bytes, scaled per launch)",
+                     "note": engine["note"]},
+        "compute_roofline": compute,
         "gpu_launches": launches,
         "clocks": clk,
     }

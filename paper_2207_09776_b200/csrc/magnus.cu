@@ -942,6 +942,8 @@ void session_stats(const MagnusSession* s, s2b_magnus_stats* out) {
     out->path_terms = 0;
     out->path_windows = 0;
     out->path_segments = 0;
+    out->engine = !s->use_cluster ? 0
+                  : (cluster_xm_supported(s->op->variant, static_cast<int>(s->op->nx), static_cast<int>(s->op->nv)) ? 2 : 1);
     for (size_t m = 0; m < s->M; ++m) {
         out->path_terms += t[m];
         out->path_windows += w[m];
