@@ -1,0 +1,292 @@
+// Cluster-resident Euler-Maruyama (solve_euler, src/euler.cpp:95-182) for x-invariant
+// coefficient fields (the constant Langevin family) at 256 x 256.
+//
+// One 8-CTA cluster owns one path for ALL of its steps: the state never leaves shared
+// memory between steps.  CTA `rank` owns 32 rows; lane = row, each thread marches along
+// x over a 32-point segment with P points in flight, the row's coefficient values in
+// registers (x-invariant fields), the three stencil rows in per-row register rings.  The
+// state is double-buffered x-major ([x][row], conflict-free column reads, immediate
+// offsets); the one halo row on each side is pushed to the neighbour CTA with a DSMEM
+// store as it is computed, and one cluster barrier per step publishes it.
+//
+// Arithmetic: euler_step_into (euler.cpp:28-86) term by term, separately rounded
+// (-fmad=false): central differences, drift folded over the non-zero fields in the order
+// h, fx, fv, gxx, gxv, gvv with the 1/2 applied as (0.5*g) [per row here: the same
+// product], noise over sig, sigx, sigv, then (u + drift*dt) + noise*dW.
+// Blow-up: the reference stops a path at the first step whose max|u+| is infinite
+// (std::max ignores NaN): each thread keeps the first step at which it produced an
+// infinite value and folds it into a per-path atomicMin; the statuses are derived from it,
+// so no per-step reduction is needed (values computed after a blow-up are discarded).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
+#include "s2b_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace s2b {
+
+namespace {
+
+constexpr int kEmCl = 8;
+
+struct EmXmArgs {
+    const double* rowf; // [9][nv] row values of the x-invariant fields
+    double st[5];
+    double dt;
+    const double* values; // [M][vstride] Brownian prefix values
+    size_t vstride;
+    int step_leb;
+    int nsteps;
+    const double* phi;
+    double* const* rec; // R record buffers [M][n]
+    const int* rec_k;   // E-M step index after which record r is taken (ascending)
+    int R;
+    int* blow; // [M] first step with an infinite value (INT_MAX: none)
+    int M;
+    int nv;
+    int* work;
+};
+
+__device__ __forceinline__ void cl_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NX, int RPC, int NT, int P, int MASK>
+__global__ void __launch_bounds__(NT, 1) em_cluster_kernel(EmXmArgs a) {
+    constexpr bool GXV = (MASK & 16) != 0;
+    constexpr int TR = RPC + 2; // rows incl. one halo row each side
+    constexpr int TX = NX + 2;  // columns incl. one zero column each side
+    constexpr int TBUF = TX * TR;
+    constexpr int NSEG = NT / RPC;
+    constexpr int LX = NX / NSEG;
+    constexpr int WS = GXV ? 3 : 1; // ring span of rows j-1, j+1
+    constexpr int R0 = 3 + P - 1;   // ring slots of row j
+    constexpr int R1 = WS + P - 1;  // ring slots of rows j-1, j+1
+    static_assert(NT % RPC == 0 && NX % NSEG == 0 && LX % P == 0, "x-march shape");
+
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int t = threadIdx.x;
+    const int r = t % RPC;
+    const int seg = t / RPC;
+    const int x0 = seg * LX;
+    const int row0 = rank * RPC;
+    const int j = row0 + r;
+    const int n = NX * a.nv;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* U = reinterpret_cast<double*>(smem_raw); // [2][TX][TR]
+    __shared__ int next_path;
+
+    const bool has_lo = rank > 0, has_hi = rank < kEmCl - 1;
+    // halo push targets: row 0 -> lower neighbour's row RPC, row RPC-1 -> upper's row -1
+    double* rem = nullptr;
+    if (r == 0 && has_lo) rem = cluster.map_shared_rank(U, rank - 1) + (x0 + 1) * TR + (RPC + 1);
+    else if (r == RPC - 1 && has_hi) rem = cluster.map_shared_rank(U, rank + 1) + (x0 + 1) * TR + 0;
+    const bool do_rem = rem != nullptr;
+    int* next0 = cluster.map_shared_rank(&next_path, 0);
+    const int tb = (x0 + 1) * TR + (r + 1);
+
+    // this row's coefficients (x-invariant); 0.5*g formed as the reference forms it per point
+    const double fh = (MASK & 1) ? a.rowf[0 * a.nv + j] : 0.0;
+    const double ffx = (MASK & 2) ? a.rowf[1 * a.nv + j] : 0.0;
+    const double ffv = (MASK & 4) ? a.rowf[2 * a.nv + j] : 0.0;
+    const double hgxx = (MASK & 8) ? 0.5 * a.rowf[3 * a.nv + j] : 0.0;
+    const double fgxv = (MASK & 16) ? a.rowf[4 * a.nv + j] : 0.0;
+    const double hgvv = (MASK & 32) ? 0.5 * a.rowf[5 * a.nv + j] : 0.0;
+    const double fsig = (MASK & 64) ? a.rowf[6 * a.nv + j] : 0.0;
+    const double fsx = (MASK & 128) ? a.rowf[7 * a.nv + j] : 0.0;
+    const double fsv = (MASK & 256) ? a.rowf[8 * a.nv + j] : 0.0;
+    const double st0 = a.st[0], st1 = a.st[1], st2 = a.st[2], st3 = a.st[3], st4 = a.st[4];
+    const double dt = a.dt;
+
+    while (true) {
+        if (rank == 0 && t == 0) next_path = atomicAdd(a.work, 1);
+        cl_barrier();
+        const int p = *next0;
+        cl_barrier(); // everyone has read next_path; the previous path's pushes are done
+        if (p >= a.M) break;
+
+        // phi into buffer 0: own rows and the two halo rows (zero outside the grid), and
+        // zero x-halo columns in both buffers
+        for (int q = t; q < TR * NX; q += NT) {
+            const int rr = q / NX - 1, x = q % NX;
+            const int jj = row0 + rr;
+            U[(x + 1) * TR + rr + 1] = (jj >= 0 && jj < a.nv) ? a.phi[static_cast<size_t>(jj) * NX + x] : 0.0;
+        }
+        for (int q = t; q < 2 * 2 * TR; q += NT) {
+            const int b = q / (2 * TR), side = (q / TR) & 1, rr = q % TR;
+            U[b * TBUF + (side ? TX - 1 : 0) * TR + rr] = 0.0;
+        }
+        if (!has_lo || !has_hi) { // outer halo rows of buffer 1 stay zero
+            for (int x = t; x < TX; x += NT) {
+                if (!has_lo) U[TBUF + x * TR + 0] = 0.0;
+                if (!has_hi) U[TBUF + x * TR + RPC + 1] = 0.0;
+            }
+        }
+        __syncthreads();
+
+        const double* pv = a.values + static_cast<size_t>(p) * a.vstride;
+        double dWn = pv[a.step_leb] - pv[0];
+        int first = INT_MAX;
+        int rec = 0;
+        int cur = 0;
+        for (int k = 0; k < a.nsteps; ++k) {
+            const double dW = dWn;
+            if (k + 1 < a.nsteps) dWn = pv[static_cast<size_t>(k + 2) * a.step_leb] - pv[static_cast<size_t>(k + 1) * a.step_leb];
+            const double* uin = U + cur * TBUF + tb;
+            double* uout = U + (cur ^ 1) * TBUF + tb;
+            double* rout = rem + (cur ^ 1) * TBUF;
+            // rings over absolute columns c >= -1: row j slot (c+1) mod R0 (columns c-1..c+1
+            // live per point), rows j-1, j+1 slot (c - LO1) mod R1
+            constexpr int LO1 = GXV ? -1 : 0;
+            double w0[R0], wm[R1], wp[R1];
+            w0[0] = uin[-TR];
+            w0[1] = uin[0];
+            if constexpr (GXV) {
+                wm[0] = uin[-TR - 1];
+                wp[0] = uin[-TR + 1];
+                wm[1] = uin[-1];
+                wp[1] = uin[1];
+            }
+            bool inf_seen = false;
+#pragma unroll
+            for (int i0 = 0; i0 < LX; i0 += P) {
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int c = i0 + q;
+                    w0[(c + 2) % R0] = uin[(c + 1) * TR];
+                    const int ch = GXV ? c + 1 : c;
+                    wm[(ch - LO1) % R1] = uin[ch * TR - 1];
+                    wp[(ch - LO1) % R1] = uin[ch * TR + 1];
+                }
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int c = i0 + q;
+                    const double uc = w0[(c + 1) % R0];
+                    const double uxm = w0[c % R0];
+                    const double uxp = w0[(c + 2) % R0];
+                    const double uvm = wm[(c - LO1) % R1];
+                    const double uvp = wp[(c - LO1) % R1];
+                    const double dxu = (uxp - uxm) * st0;
+                    const double dvu = (uvp - uvm) * st2;
+                    double drift = 0.0;
+                    if (MASK & 1) drift += fh * uc;
+                    if (MASK & 2) drift += ffx * dxu;
+                    if (MASK & 4) drift += ffv * dvu;
+                    if (MASK & 8) {
+                        const double dxxu = (uxp - 2.0 * uc + uxm) * st1;
+                        drift += hgxx * dxxu;
+                    }
+                    if (MASK & 16) {
+                        const double upp = wp[(c + 1 - LO1) % R1], upm = wp[(c - 1 - LO1) % R1];
+                        const double ump = wm[(c + 1 - LO1) % R1], umm = wm[(c - 1 - LO1) % R1];
+                        const double dxvu = (upp - upm - ump + umm) * st4;
+                        drift += fgxv * dxvu;
+                    }
+                    if (MASK & 32) {
+                        const double dvvu = (uvp - 2.0 * uc + uvm) * st3;
+                        drift += hgvv * dvvu;
+                    }
+                    double noise = 0.0;
+                    if (MASK & 64) noise += fsig * uc;
+                    if (MASK & 128) noise += fsx * dxu;
+                    if (MASK & 256) noise += fsv * dvu;
+                    const double next = uc + drift * dt + noise * dW;
+                    uout[c * TR] = next;
+                    if (do_rem) rout[c * TR] = next;
+                    inf_seen |= fabs(next) == __longlong_as_double(0x7FF0000000000000LL);
+                }
+            }
+            if (inf_seen && first == INT_MAX) first = k;
+            cl_barrier();
+            cur ^= 1;
+            while (rec < a.R && a.rec_k[rec] == k) {
+                double* dst = a.rec[rec] + static_cast<size_t>(p) * n + static_cast<size_t>(row0) * NX;
+                const double* src = U + cur * TBUF;
+                for (int q = t; q < RPC * NX; q += NT) dst[q] = src[(q % NX + 1) * TR + q / NX + 1];
+                ++rec;
+            }
+        }
+        if (first != INT_MAX) atomicMin(a.blow + p, first);
+    }
+}
+
+template <int MASK>
+void launch_em(s2b_context* ctx, const EmXmArgs& a) {
+    constexpr int NX = 256, RPC = 32, NT = 256, P = 4;
+    auto kern = em_cluster_kernel<NX, RPC, NT, P, MASK>;
+    const size_t smem = 8 * 2 * static_cast<size_t>(NX + 2) * (RPC + 2);
+    S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kEmCl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(kEmCl);
+    int clusters = 0;
+    S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
+    clusters = std::max(1, std::min(clusters, a.M));
+    cfg.gridDim = dim3(kEmCl * clusters);
+    S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
+__global__ void em_cluster_status_kernel(const int* blow, const int* rec_k, int R, uint8_t* status, int M) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    for (int r = 0; r < R; ++r) status[static_cast<size_t>(r) * M + m] = blow[m] <= rec_k[r] ? 1 : 0;
+}
+
+} // namespace
+
+bool em_cluster_supported(const s2b_fields* f) {
+    const char* e = std::getenv("S2B_EMXM");
+    if (e && e[0] == '0') return false;
+    return f->xinv && f->nx == 256 && f->nv == 256 && f->mask == (2 | 32 | 256);
+}
+
+void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const double* d_phi,
+                      const s2b_paths* paths, int step_leb, int nsteps, const std::vector<int>& rec_k,
+                      double* const* d_rec, uint8_t* d_status) {
+    const int M = static_cast<int>(paths->M);
+    DevBuf<int> blow(M), work(1), drec_k(rec_k.size());
+    DevBuf<double*> drec(rec_k.size());
+    std::vector<int> init(M, INT_MAX);
+    S2B_CUDA(cudaMemcpyAsync(blow.p, init.data(), M * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(work.p, 0, sizeof(int), ctx->stream));
+    S2B_CUDA(cudaMemcpyAsync(drec_k.p, rec_k.data(), rec_k.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    S2B_CUDA(cudaMemcpyAsync(drec.p, d_rec, rec_k.size() * sizeof(double*), cudaMemcpyHostToDevice, ctx->stream));
+    EmXmArgs a{};
+    a.rowf = f->d_rowf.p;
+    std::copy(f->st, f->st + 5, a.st);
+    a.dt = dt;
+    a.values = paths->d_values.p;
+    a.vstride = paths->steps + 1;
+    a.step_leb = step_leb;
+    a.nsteps = nsteps;
+    a.phi = d_phi;
+    a.rec = drec.p;
+    a.rec_k = drec_k.p;
+    a.R = static_cast<int>(rec_k.size());
+    a.blow = blow.p;
+    a.M = M;
+    a.nv = static_cast<int>(f->nv);
+    a.work = work.p;
+    launch_em<2 | 32 | 256>(ctx, a);
+    S2B_LAUNCHED(ctx);
+    em_cluster_status_kernel<<<(M + 255) / 256, 256, 0, ctx->stream>>>(blow.p, drec_k.p, a.R, d_status, M);
+    S2B_LAUNCHED(ctx);
+    S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+} // namespace s2b

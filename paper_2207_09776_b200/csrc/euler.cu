@@ -10,6 +10,8 @@
 // dW is the difference of prefix values (euler.cpp:156), so E-M and Magnus consume
 // the same paths.
 #include <algorithm>
+#include <cstring>
+#include <vector>
 
 #include "s2b_internal.cuh"
 
@@ -116,6 +118,25 @@ s2b_fields* make_fields(s2b_context* ctx, const s2b_grid* grid, const double* co
         f->mask |= 1 << k;
         S2B_CUDA(cudaMemcpy(f->d_f.p + k * n, fields9[k], n * sizeof(double), cudaMemcpyHostToDevice));
     }
+    // x-invariant fields (the constant Langevin family): row values for the cluster kernel
+    f->xinv = true;
+    std::vector<double> rowf(9 * nv, 0.0);
+    for (int k = 0; k < 9 && f->xinv; ++k) {
+        if (!(f->mask >> k & 1)) continue;
+        for (size_t j = 0; j < nv && f->xinv; ++j) {
+            const double* row = fields9[k] + j * nx;
+            rowf[k * nv + j] = row[0];
+            for (size_t i = 1; i < nx; ++i)
+                if (std::memcmp(&row[i], &row[0], sizeof(double)) != 0) {
+                    f->xinv = false;
+                    break;
+                }
+        }
+    }
+    if (f->xinv) {
+        f->d_rowf.alloc(9 * nv);
+        S2B_CUDA(cudaMemcpy(f->d_rowf.p, rowf.data(), rowf.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     // EulerStencils::from_grid (euler.cpp:18-26)
     const double dx = (grid->bx - grid->ax) / static_cast<double>(nx + 1);
     const double dv = (grid->bv - grid->av) / static_cast<double>(nv + 1);
@@ -143,6 +164,22 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         e->grid = f->grid;
         for (size_t r : plan.record_steps) e->times.push_back(static_cast<double>(r) * paths->dt_leb);
         e->status.alloc(e->R * M);
+        const size_t nsteps = plan.total_steps / plan.dt_steps;
+        if (em_cluster_supported(f) && M > 0) {
+            // cluster-resident: every step of every path on chip, records written directly
+            std::vector<int> rec_k;
+            std::vector<double*> rp;
+            for (size_t r : plan.record_steps) {
+                rec_k.push_back(static_cast<int>(r / plan.dt_steps) - 1);
+                e->states.emplace_back(M * n);
+                rp.push_back(e->states.back().p);
+            }
+            DevBuf<double> dphi(n);
+            S2B_CUDA(cudaMemcpyAsync(dphi.p, phi, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            em_cluster_solve(ctx, f, cfg->dt, dphi.p, paths, static_cast<int>(plan.dt_steps),
+                             static_cast<int>(nsteps), rec_k, rp.data(), e->status.p);
+            return e;
+        }
         DevBuf<double> U[2] = {DevBuf<double>(M * n), DevBuf<double>(M * n)};
         DevBuf<int> blown(M);
         S2B_CUDA(cudaMemsetAsync(blown.p, 0, blown.bytes(), ctx->stream));
@@ -158,7 +195,6 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         a.vstride = paths->steps + 1;
         a.blown = blown.p;
         a.M = M;
-        const size_t nsteps = plan.total_steps / plan.dt_steps;
         const unsigned gx = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64));
         size_t rec = 0;
         int cur = 0;

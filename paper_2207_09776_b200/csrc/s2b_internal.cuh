@@ -108,6 +108,8 @@ struct s2b_fields {
     s2b::DevBuf<double> d_f; // 9 * n, zero fields left unset
     double st[5] = {0, 0, 0, 0, 0}; // inv2dx invdx2 inv2dv invdv2 inv4dxdv
     s2b_grid grid{};
+    bool xinv = false;          // every non-zero field constant along x (bitwise)
+    s2b::DevBuf<double> d_rowf; // [9][nv] row values when xinv
 };
 
 struct s2b_paths {
@@ -163,6 +165,11 @@ s2b_paths* make_paths_host(s2b_context* ctx, double dt_leb, size_t steps, size_t
 s2b_paths* make_paths_philox(s2b_context* ctx, double dt_leb, size_t steps, size_t M, uint64_t seed,
                              uint64_t path_offset);
 s2b_fields* make_fields(s2b_context* ctx, const s2b_grid* grid, const double* const* fields9);
+// cluster-resident E-M (em_cluster.cu)
+bool em_cluster_supported(const s2b_fields* f);
+void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const double* d_phi,
+                      const s2b_paths* paths, int step_leb, int nsteps, const std::vector<int>& rec_k,
+                      double* const* d_rec, uint8_t* d_status);
 s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler_config* cfg,
                           const double* phi, const s2b_paths* paths);
 s2b_ensemble* exact_reference(s2b_context* ctx, const s2b_grid* grid, double t, double a, double sigma,

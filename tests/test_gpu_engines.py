@@ -65,3 +65,47 @@ def test_engines_blowup_exits_256(ref, s2b, ctx, engine):
                               phi=phi)
     assert np.array_equal(ens[-1].status, wst[-1])
     assert np.array_equal(ens[-1].states(), want[-1], equal_nan=True)
+
+
+EM_ENGINES = {"em-cluster": {}, "em-stream": {"S2B_EMXM": "0"}}
+
+
+@pytest.fixture
+def em_engine(request, monkeypatch):
+    for k, v in EM_ENGINES[request.param].items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
+@pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
+def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine):
+    """solve_euler at 256^2 (constant Langevin: the cluster-resident kernel) vs the reference,
+    with a mid-run record."""
+    d, T, dt_leb, dt, M, seed = 256, 0.01, 1e-4, 1e-4, 3, 21
+    ops = ref.Ops("langevin-constant", d, order=1)
+    values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
+    want, wst, _ = ops.solve_euler(values, dt_leb, T, dt, record_times=[0.005], seed=seed)
+    g = s2b.GridSpec.square(d)
+    f = s2b.Fields.from_family(g, "langevin-constant", ctx=ctx)
+    paths = s2b.BrownianPaths.from_values(values, dt_leb, seed=seed, ctx=ctx)
+    ens = s2b.solve_euler(s2b.EulerConfig(dt=dt, record_times=[0.005]), f, g, ops.datum(), paths, T)
+    assert len(ens) == len(want)
+    for r, e in enumerate(ens):
+        assert np.array_equal(e.status, wst[r])
+        assert np.array_equal(e.states(), want[r])
+
+
+@pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
+def test_euler_engines_blowup_256(ref, s2b, ctx, em_engine):
+    """dt far beyond the stability bound: Ok (finite, huge) at t = 20, blown by T = 200."""
+    d, T, M, seed = 256, 200.0, 2, 9
+    values, _ = ref.simulate_brownian(T, 1.0, M, seed)
+    ops = ref.Ops("langevin-constant", d, order=1)
+    want, wst, _ = ops.solve_euler(values, 1.0, T, 1.0, record_times=[20.0], seed=seed)
+    g = s2b.GridSpec.square(d)
+    f = s2b.Fields.from_family(g, "langevin-constant", ctx=ctx)
+    paths = s2b.BrownianPaths.from_values(values, 1.0, seed=seed, ctx=ctx)
+    ens = s2b.solve_euler(s2b.EulerConfig(dt=1.0, record_times=[20.0]), f, g, ops.datum(), paths, T)
+    assert np.array_equal(ens[0].status, wst[0]) and np.array_equal(ens[-1].status, wst[-1])
+    assert ens[-1].blowup_count() == M
+    assert np.array_equal(ens[0].states(), want[0])
