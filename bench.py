@@ -33,6 +33,9 @@ SIGMA = 1.0 / np.sqrt(10.0)
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # Magnus engines (s2b_magnus_stats.engine) -> dominant kernel and its ncu summary in profiles/
 ENGINES = {
+    3: {"name": "cluster-xmi", "kernel": "cluster_xmi_kernel", "profile": "xmi_kernel_ncu.json",
+        "note": "cluster-resident in-place x-march (16-CTA clusters, accumulator in L2): achieved is the "
+                "streaming-equivalent rate, traffic the real DRAM bytes; bound by the fp64 pipe"},
     0: {"name": "stream", "kernel": "term_tma_kernel", "profile": "term_kernel_ncu.json",
         "note": "streaming pass engine: term and accumulator round-trip HBM every Taylor term"},
     1: {"name": "cluster-band", "kernel": "cluster_magnus_kernel", "profile": "cluster_kernel_ncu.json",

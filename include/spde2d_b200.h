@@ -111,7 +111,7 @@ typedef struct {
     double term_kernel_ms; /* summed CUDA-event time of those launches (if timing enabled) */
     double gridpoints;     /* nx*nv */
     int64_t path_segments; /* sum over paths of Taylor segments (one k=1 term each) */
-    int32_t engine;        /* 0 streaming passes, 1 cluster row-band, 2 cluster x-march */
+    int32_t engine;        /* 0 streaming passes, 1 cluster row-band, 2 cluster x-march, 3 in-place x-march */
 } s2b_magnus_stats;
 
 const char *s2b_last_error(void);

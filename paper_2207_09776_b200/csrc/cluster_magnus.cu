@@ -416,7 +416,7 @@ void launch_v(s2b_context* ctx, const ClusterArgs& a) {
 } // namespace
 
 bool cluster_engine_supported(int variant, int nx, int nv) {
-    if (cluster_xm_supported(variant, nx, nv)) return true;
+    if (cluster_xm_supported(variant, nx, nv) || cluster_xmi_supported(variant, nx, nv)) return true;
     if (variant < 1 || (variant > 4 && variant < 7) || variant > 9) return false;
     if (nx % 2 || nx < 6 || nx > 2 * kBandThreads) return false;
     const int rpb = nv / 32; // 8 CTAs x 4 bands (or 16 x 2)
@@ -438,6 +438,10 @@ bool cluster_engine_supported(int variant, int nx, int nv) {
 void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterArgs& a) {
     if (cluster_xm_supported(variant, a.nx, a.nv)) {
         launch_cluster_xm(ctx, variant, a);
+        return;
+    }
+    if (cluster_xmi_supported(variant, a.nx, a.nv)) {
+        launch_cluster_xmi(ctx, variant, a);
         return;
     }
     switch (variant) {

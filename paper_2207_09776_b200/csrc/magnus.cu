@@ -582,6 +582,8 @@ struct MagnusSession {
     DevBuf<int> iv;              // win seg k nseg status par rec_next  (7 x M)
     DevBuf<double> prev;
     DevBuf<long long> terms, windows, segments;
+    DevBuf<double> sx; // accumulator scratch of the in-place cluster engine
+    int sx_slots = 0;
     DevBuf<unsigned long long> tn, sn;
     DevBuf<int> act[2];
     DevBuf<int> cnt;
@@ -762,6 +764,8 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
             const bool ok = op->variant != 0 &&
                             cluster_engine_supported(op->variant, static_cast<int>(op->nx), static_cast<int>(op->nv));
             s->use_cluster = ok && !(eng && std::strcmp(eng, "stream") == 0);
+            if (s->use_cluster && cluster_xmi_supported(op->variant, static_cast<int>(op->nx), static_cast<int>(op->nv)))
+                s->sx.alloc(cluster_xmi_scratch(static_cast<int>(op->nx), static_cast<int>(op->nv), &s->sx_slots));
         }
         s->phi.assign(phi, phi + n);
         const size_t M = s->M;
@@ -883,6 +887,8 @@ void session_advance(MagnusSession* s, size_t n_windows) {
         a.cap = s->cfg.blowup_norm_cap;
         a.M = static_cast<int>(s->M);
         a.work = s->cnt.p + 3;
+        a.sx = s->sx.p;
+        a.sx_slots = s->sx_slots;
         S2B_CUDA(cudaMemsetAsync(s->cnt.p + 3, 0, sizeof(int), s->ctx->stream));
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (s->timing) {
@@ -942,8 +948,12 @@ void session_stats(const MagnusSession* s, s2b_magnus_stats* out) {
     out->path_terms = 0;
     out->path_windows = 0;
     out->path_segments = 0;
-    out->engine = !s->use_cluster ? 0
-                  : (cluster_xm_supported(s->op->variant, static_cast<int>(s->op->nx), static_cast<int>(s->op->nv)) ? 2 : 1);
+    {
+        const int v = s->op->variant, nx = static_cast<int>(s->op->nx), nv = static_cast<int>(s->op->nv);
+        out->engine = !s->use_cluster ? 0
+                      : cluster_xm_supported(v, nx, nv) ? 2
+                      : cluster_xmi_supported(v, nx, nv) ? 3 : 1;
+    }
     for (size_t m = 0; m < s->M; ++m) {
         out->path_terms += t[m];
         out->path_windows += w[m];

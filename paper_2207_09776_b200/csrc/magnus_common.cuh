@@ -225,12 +225,19 @@ struct ClusterArgs {
     double tol, cap;
     int M;
     int* work; // path counter (zeroed before the launch)
+    double* sx; // accumulator scratch of the in-place engine: [slots][CL][nx][rows] (x-major)
+    int sx_slots;
 };
 bool cluster_engine_supported(int variant, int nx, int nv);
 void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterArgs& a);
 // x-march variant of the cluster engine (cluster_xm.cu); S2B_XM=0 disables it
 bool cluster_xm_supported(int variant, int nx, int nv);
 void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterArgs& a);
+// in-place x-march with the accumulator in L2 (cluster_xmi.cu): 16-CTA clusters at 512^2;
+// S2B_XMI=0 disables it.  sx_doubles: scratch the session must pass in ClusterArgs::sx.
+bool cluster_xmi_supported(int variant, int nx, int nv);
+size_t cluster_xmi_scratch(int nx, int nv, int* slots);
+void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterArgs& a);
 
 } // namespace mg
 } // namespace s2b

@@ -109,3 +109,38 @@ def test_euler_engines_blowup_256(ref, s2b, ctx, em_engine):
     assert np.array_equal(ens[0].status, wst[0]) and np.array_equal(ens[-1].status, wst[-1])
     assert ens[-1].blowup_count() == M
     assert np.array_equal(ens[0].states(), want[0])
+
+
+ENGINES_512 = {"xmi": {}, "stream": {"S2B_ENGINE": "stream"}}
+
+
+@pytest.fixture
+def engine512(request, monkeypatch):
+    for k, v in ENGINES_512[request.param].items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
+@pytest.mark.parametrize("engine512", list(ENGINES_512), indirect=True)
+@pytest.mark.parametrize("order", [2, 3])
+def test_engines_bitwise_512(ref, s2b, ctx, engine512, order):
+    """512^2: the in-place cluster engine (16-CTA clusters, accumulator in L2) and the
+    streaming engine against the reference, with a record snapshot."""
+    d, T, dt, dt_leb, M, seed = 512, 0.02, 0.01, 1e-3, 2, 51 + order
+    _, values, want, wst = _ref_run(ref, d, order, T, dt, dt_leb, M, seed, rec=[0.01])
+    ens, _, _, stats = gpu_magnus(s2b, ctx, "langevin-constant", d, order, values, dt_leb, T, dt,
+                                  rec=[0.01], seed=seed)
+    assert len(ens) == len(want)
+    for r, e in enumerate(ens):
+        assert np.array_equal(e.status, wst[r])
+        assert np.array_equal(e.states(), want[r], equal_nan=True)
+    assert stats["engine"] == (3 if engine512 == "xmi" else 0)
+
+
+@pytest.mark.parametrize("engine512", ["xmi"], indirect=True)
+def test_engines_blowup_exits_512(ref, s2b, ctx, engine512):
+    d, T, dt, dt_leb, M = 512, 0.02, 0.01, 1e-3, 2
+    _, values, want, wst = _ref_run(ref, d, 3, T, dt, dt_leb, M, 5, cap=1e-3)
+    ens, _, _, _ = gpu_magnus(s2b, ctx, "langevin-constant", d, 3, values, dt_leb, T, dt, seed=5,
+                              blowup_norm_cap=1e-3)
+    assert np.array_equal(ens[-1].status, wst[-1]) and ens[-1].blowup_count() == M
