@@ -82,6 +82,13 @@ typedef struct {
     size_t n_record;
 } s2b_magnus_config;
 
+/* AdaptiveConfig (magnus.hpp:14-17): step-size control of solve_adaptive_magnus. */
+typedef struct {
+    int enabled;      /* must be non-zero for s2b_solve_adaptive_magnus */
+    double tolerance; /* accepted order-2 / order-3 relative gap */
+    double shrink;    /* window shrink factor in (0, 1) */
+} s2b_adaptive_config;
+
 /* EulerConfig (euler.hpp:12-16) + the horizon T. */
 typedef struct {
     double dt;
@@ -189,6 +196,12 @@ int s2b_solve_magnus(s2b_context *ctx, const s2b_operator *op, const s2b_magnus_
                      s2b_magnus_stats *stats);
 int s2b_solve_euler(s2b_context *ctx, const s2b_fields *f, const s2b_euler_config *cfg,
                     const double *phi, const s2b_paths *paths, s2b_ensemble **out);
+/* solve_adaptive_magnus (magnus.cpp:306-404): orders 2 and 3 per window from one weight
+ * build, accept order 3 when the relative gap <= tolerance, else shrink and retry.
+ * cfg->order is ignored (the operator must carry order-3 commutators). */
+int s2b_solve_adaptive_magnus(s2b_context *ctx, const s2b_operator *op, const s2b_magnus_config *cfg,
+                              const s2b_adaptive_config *adaptive, const double *phi,
+                              const s2b_paths *paths, s2b_ensemble **out, s2b_magnus_stats *stats);
 
 /* Resident Magnus session: state stays in HBM, windows are advanced on demand. */
 int s2b_magnus_session_create(s2b_context *ctx, const s2b_operator *op,

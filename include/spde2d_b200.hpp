@@ -280,6 +280,14 @@ std::vector<SolutionEnsemble> solve_iterated_magnus(const MagnusConfig& cfg,
                                                     std::span<const double> phi,
                                                     const BrownianBatch& batch, double T,
                                                     const GridSpec& grid);
+// solve_adaptive_magnus (magnus.hpp:104-108): orders 2 and 3 per window from one logarithm
+// build; a window whose relative order-2/3 gap exceeds cfg.adaptive.tolerance shrinks by
+// cfg.adaptive.shrink and is retried.  Needs cfg.adaptive.enabled and order-3 commutators.
+std::vector<SolutionEnsemble> solve_adaptive_magnus(const MagnusConfig& cfg,
+                                                    const CommutatorSet& comms,
+                                                    std::span<const double> phi,
+                                                    const BrownianBatch& batch, double T,
+                                                    const GridSpec& grid);
 
 struct EulerConfig {
     double dt = 1e-4;

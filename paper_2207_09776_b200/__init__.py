@@ -349,6 +349,17 @@ class BrownianPaths:
 
 # ---------------------------------------------------------------- configs / ensembles
 @dataclass
+class AdaptiveConfig:
+    """AdaptiveConfig (magnus.hpp:14-17)."""
+    enabled: bool = False
+    tolerance: float = 1e-4
+    shrink: float = 0.5
+
+    def c(self):
+        return _capi.AdaptiveConfig(1 if self.enabled else 0, float(self.tolerance), float(self.shrink))
+
+
+@dataclass
 class MagnusConfig:
     """MagnusConfig (magnus.hpp:19-28); `threads` is accepted and ignored on the GPU."""
     order: int = 3
@@ -358,6 +369,7 @@ class MagnusConfig:
     blowup_norm_cap: float = 1e10
     threads: int = 0
     record_times: list = field(default_factory=list)
+    adaptive: AdaptiveConfig = field(default_factory=AdaptiveConfig)
 
     def c(self, T):
         rec = np.ascontiguousarray(self.record_times, np.float64)
@@ -457,6 +469,24 @@ def solve_iterated_magnus(cfg: MagnusConfig, comms: Operator, phi, batch: Browni
     st = _capi.MagnusStats()
     _check(lib().s2b_solve_magnus(comms.ctx.h, comms.h, C.byref(ccfg), _dptr(phi), batch.h,
                                   C.byref(h), C.byref(st)))
+    if stats is not None:
+        stats.update({k: getattr(st, k) for k, _ in _capi.MagnusStats._fields_})
+    return _ensembles(h, grid, batch.seed, comms.ctx)
+
+
+def solve_adaptive_magnus(cfg: MagnusConfig, comms: Operator, phi, batch: BrownianPaths, T,
+                          grid: GridSpec, stats: Optional[dict] = None):
+    """solve_adaptive_magnus (magnus.hpp:104-108): orders 2 and 3 per window, shrink-and-retry
+    on a relative gap above cfg.adaptive.tolerance; needs an order-3 operator."""
+    if len(phi) != grid.dim() or comms.grid.dim() != grid.dim():
+        raise DimensionError("solve_adaptive_magnus: dimension mismatch")
+    ccfg, keep = cfg.c(T)
+    acfg = cfg.adaptive.c()
+    phi = np.ascontiguousarray(phi, np.float64)
+    h = C.c_void_p()
+    st = _capi.MagnusStats()
+    _check(lib().s2b_solve_adaptive_magnus(comms.ctx.h, comms.h, C.byref(ccfg), C.byref(acfg), _dptr(phi),
+                                           batch.h, C.byref(h), C.byref(st)))
     if stats is not None:
         stats.update({k: getattr(st, k) for k, _ in _capi.MagnusStats._fields_})
     return _ensembles(h, grid, batch.seed, comms.ctx)

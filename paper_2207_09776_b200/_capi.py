@@ -33,6 +33,10 @@ class MagnusConfig(C.Structure):
                 ("n_record", C.c_size_t)]
 
 
+class AdaptiveConfig(C.Structure):
+    _fields_ = [("enabled", C.c_int), ("tolerance", C.c_double), ("shrink", C.c_double)]
+
+
 class EulerConfig(C.Structure):
     _fields_ = [("dt", C.c_double), ("T", C.c_double), ("record_times", C.POINTER(C.c_double)),
                 ("n_record", C.c_size_t)]
@@ -88,6 +92,8 @@ SIGNATURES = {
     "s2b_solve_magnus": (C.c_int, [_VP, _VP, _P(MagnusConfig), _P(C.c_double), _VP, _P(_VP),
                                    _P(MagnusStats)]),
     "s2b_solve_euler": (C.c_int, [_VP, _VP, _P(EulerConfig), _P(C.c_double), _VP, _P(_VP)]),
+    "s2b_solve_adaptive_magnus": (C.c_int, [_VP, _VP, _P(MagnusConfig), _P(AdaptiveConfig), _P(C.c_double),
+                                            _VP, _P(_VP), _P(MagnusStats)]),
     "s2b_magnus_session_create": (C.c_int, [_VP, _VP, _P(MagnusConfig), _P(C.c_double), _VP,
                                             _P(_VP)]),
     "s2b_magnus_session_advance": (C.c_int, [_VP, C.c_size_t]),

@@ -369,6 +369,21 @@ int s2b_solve_magnus(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_
     });
 }
 
+int s2b_solve_adaptive_magnus(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfg,
+                              const s2b_adaptive_config* adaptive, const double* phi, const s2b_paths* paths,
+                              s2b_ensemble** out, s2b_magnus_stats* stats) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(op, "op");
+        need(cfg, "cfg");
+        need(phi, "phi");
+        need(paths, "paths");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = solve_adaptive(ctx, op, cfg, adaptive, phi, paths, stats);
+    });
+}
+
 int s2b_solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler_config* cfg, const double* phi,
                     const s2b_paths* paths, s2b_ensemble** out) {
     return guard([&] {

@@ -147,6 +147,33 @@ std::vector<SolutionEnsemble> solve_iterated_magnus(const MagnusConfig& cfg, con
     return download(e, grid, batch.seed, elapsed_since(t0) / static_cast<double>(batch.M));
 }
 
+std::vector<SolutionEnsemble> solve_adaptive_magnus(const MagnusConfig& cfg, const CommutatorSet& comms,
+                                                    std::span<const double> phi, const BrownianBatch& batch,
+                                                    double T, const GridSpec& grid) {
+    if (!cfg.adaptive.enabled) throw ConfigError("solve_adaptive_magnus: adaptive flag not set");
+    if (!(cfg.adaptive.shrink > 0.0 && cfg.adaptive.shrink < 1.0))
+        throw ConfigError("solve_adaptive_magnus: shrink factor must lie in (0, 1)");
+    if (comms.order < 3) throw ConfigError("solve_adaptive_magnus: needs order-3 commutators");
+    if (phi.size() != grid.dim() || comms.B.rows() != grid.dim())
+        throw DimensionError("solve_adaptive_magnus: dimension mismatch");
+    const auto t0 = std::chrono::steady_clock::now();
+    const s2b_grid g = c_grid(grid);
+    // MagnusLogBuilder(comms, 3): the union pattern of all six sources
+    const s2b_csr src[6] = {c_csr(comms.B), c_csr(comms.A), c_csr(comms.A2),
+                            c_csr(comms.BA), c_csr(comms.BAA), c_csr(comms.BAB)};
+    s2b_operator* op = nullptr;
+    check(s2b_operator_create(context(), &g, 3, src, &op));
+    auto op_guard = own(op, s2b_operator_destroy);
+    auto paths = own(upload_paths(batch), s2b_paths_destroy);
+    const s2b_magnus_config c{3, cfg.dt, T, cfg.expmv_tol, cfg.expmv_theta, cfg.blowup_norm_cap,
+                              cfg.record_times.data(), cfg.record_times.size()};
+    const s2b_adaptive_config ad{1, cfg.adaptive.tolerance, cfg.adaptive.shrink};
+    s2b_ensemble* e = nullptr;
+    check(s2b_solve_adaptive_magnus(context(), op, &c, &ad, phi.data(), paths.get(), &e, nullptr));
+    auto e_guard = own(e, s2b_ensemble_destroy);
+    return download(e, grid, batch.seed, elapsed_since(t0) / static_cast<double>(batch.M));
+}
+
 std::vector<SolutionEnsemble> solve_euler(const EulerConfig& cfg, const CoefficientFields& fields,
                                           const GridSpec& grid, const Field& phi, const BrownianBatch& batch,
                                           double T) {

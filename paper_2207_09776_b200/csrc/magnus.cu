@@ -596,6 +596,7 @@ struct MagnusSession {
     int cur = 0;          // which act[] is the input list
     bool timing = false;
     bool use_cluster = false; // cluster-resident engine (cluster_magnus.cu) for this operator
+    bool external_prepare = false; // ctab/stab written by the caller (adaptive driver)
     std::vector<cudaEvent_t> ev;
     s2b_magnus_stats stats{};
 
@@ -856,7 +857,7 @@ void prepare_windows(MagnusSession* s, size_t w0, size_t w1) {
 void session_advance(MagnusSession* s, size_t n_windows) {
     if (n_windows == 0 || static_cast<size_t>(s->cur_window) >= s->nwin) return;
     const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
-    prepare_windows(s, s->cur_window, stop);
+    if (!s->external_prepare) prepare_windows(s, s->cur_window, stop);
     if (s->use_cluster) {
         // cluster-resident engine: every live path runs windows [cur, stop) on chip
         ClusterArgs a{};
@@ -1074,6 +1075,316 @@ void session_destroy(MagnusSession* s) {
     for (auto ev : s->ev) cudaEventDestroy(ev);
     if (s->h_cnt) cudaFreeHost(s->h_cnt);
     delete s;
+}
+
+// ---- solve_adaptive_magnus (magnus.cpp:306-404) ------------------------------------
+//
+// Per path: attempt the window [k0, k0+len) at orders 3 and 2 from one functional build,
+// accept the order-3 result when both expmv calls succeed and max|u3-u2| / max|u3| <= tau,
+// otherwise shrink len by `shrink` (below one Lebesgue step: blown).  Accepted windows never
+// cross a record time.  On the GPU every live path makes one attempt per round: the
+// attempt's six weights go into a one-window session (any Magnus engine), which runs twice
+// (Y3, then Y2 on the same input); a block per path reduces the gap and decides.  Paths
+// that finished or blew up sit the round out (status 2 -> skipped by every engine).
+namespace {
+
+__device__ void window_weights(const double* p, long long k0, long long L, double dt, double c3[6], double c2[6]) {
+    // lebesgue_functionals (stochastics.cpp:121-141) + log_coefficients (magnus.cpp:26-40)
+    const double base = p[k0];
+    double iw = 0.0, isw = 0.0, iw2 = 0.0;
+    for (long long j = 0; j < L; ++j) {
+        const double wv = p[k0 + j] - base;
+        const double sj = static_cast<double>(j) * dt;
+        iw += wv;
+        isw += sj * wv;
+        iw2 += wv * wv;
+    }
+    const double h = static_cast<double>(L) * dt;
+    const double W = p[k0 + L] - p[k0];
+    const double IW = iw * dt, IsW = isw * dt, IW2 = iw2 * dt;
+    c3[0] = c2[0] = h;
+    c3[1] = c2[1] = W;
+    c3[2] = c2[2] = -0.5 * h;
+    c3[3] = c2[3] = IW - 0.5 * h * W;
+    c3[4] = 0.5 * IW2 - 0.5 * W * IW + h * W * W / 12.0;
+    c3[5] = IsW - 0.5 * h * IW - h * h * W / 12.0;
+    c2[4] = c2[5] = 0.0;
+}
+
+struct AdArgs {
+    const double* values;
+    size_t vstride;
+    size_t M, n;
+    double dt_leb;
+    long long dt_steps, total;
+    const long long* rec_steps;
+    int R;
+    long long* k0;
+    long long* len;
+    int* fresh;
+    int* flags; // 0 live, 1 done, 2 blown
+    int* rec;   // next record
+    int* rec_lo;
+    int* rec_hi;
+    int* accept;
+    double* ctab3;
+    double* ctab2;
+    int* live;
+    double tau, shrink, cap;
+};
+
+__global__ void ad_prepare_kernel(AdArgs a) {
+    const size_t m = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (m >= a.M) return;
+    double* c3 = a.ctab3 + m * 6;
+    double* c2 = a.ctab2 + m * 6;
+    if (a.flags[m] != 0) {
+        for (int q = 0; q < 6; ++q) c3[q] = c2[q] = 0.0;
+        return;
+    }
+    if (a.fresh[m]) { // never step across the next record boundary
+        const long long to_rec = a.rec_steps[a.rec[m]] - a.k0[m];
+        a.len[m] = a.dt_steps < to_rec ? a.dt_steps : to_rec;
+        a.fresh[m] = 0;
+    }
+    double w3[6], w2[6];
+    window_weights(a.values + m * a.vstride, a.k0[m], a.len[m], a.dt_leb, w3, w2);
+    for (int q = 0; q < 6; ++q) {
+        c3[q] = w3[q];
+        c2[q] = w2[q];
+    }
+    atomicAdd(a.live, 1);
+}
+
+// session control block for one attempt run: every live path at window 0 of parity 0
+__global__ void ad_reset_kernel(int* iv, size_t M, const int* flags) {
+    const size_t m = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (m >= M) return;
+    for (int f = 0; f < 7; ++f) iv[f * M + m] = 0;
+    iv[4 * M + m] = flags[m] != 0 ? 2 : 0;
+}
+
+__global__ void ad_save_status_kernel(const int* status, int* out, size_t M) {
+    const size_t m = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (m < M) out[m] = status[m];
+}
+
+// gap = max|u3 - u2| / max|u3| (or the diff when max|u3| == 0) and the accept/shrink rule
+__global__ void ad_gap_kernel(AdArgs a, const double* __restrict__ u3, const double* __restrict__ S0,
+                              const double* __restrict__ S1, const int* __restrict__ par,
+                              const int* __restrict__ st3, const int* __restrict__ st2) {
+    __shared__ unsigned long long red[2][32];
+    for (size_t m = blockIdx.x; m < a.M; m += gridDim.x) {
+        if (a.flags[m] != 0) {
+            if (threadIdx.x == 0) a.accept[m] = 0;
+            continue;
+        }
+        bool ok = st3[m] != 2 && st2[m] != 2;
+        unsigned long long db = 0, sb = 0;
+        if (ok) { // both results finite (expmv Ok): the max is order independent on the bits
+            const double* x3 = u3 + m * a.n;
+            const double* x2 = (par[m] ? S1 : S0) + m * a.n;
+            for (size_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+                db = umax64(db, abs_bits(x3[i] - x2[i]));
+                sb = umax64(sb, abs_bits(x3[i]));
+            }
+        }
+        db = warp_umax(db);
+        sb = warp_umax(sb);
+        if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = db;
+            red[1][threadIdx.x >> 5] = sb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (unsigned q = 1; q < blockDim.x / 32; ++q) {
+                db = umax64(db, red[0][q]);
+                sb = umax64(sb, red[1][q]);
+            }
+            db = umax64(db, red[0][0]);
+            sb = umax64(sb, red[1][0]);
+            double gap = __longlong_as_double(static_cast<long long>(kInfBits));
+            const double diff = __longlong_as_double(static_cast<long long>(db));
+            const double scale = __longlong_as_double(static_cast<long long>(sb));
+            if (ok) {
+                gap = scale > 0.0 ? diff / scale : diff;
+                ok = isfinite(gap);
+            }
+            if (ok && gap <= a.tau) {
+                a.accept[m] = 1;
+                a.k0[m] += a.len[m];
+                a.fresh[m] = 1;
+                int r = a.rec[m];
+                a.rec_lo[m] = r;
+                if (!isfinite(scale) || scale > a.cap) {
+                    a.flags[m] = 2; // magnus.cpp:360-363
+                } else {
+                    while (r < a.R && a.rec_steps[r] == a.k0[m]) ++r;
+                    if (a.k0[m] >= a.total) a.flags[m] = 1;
+                }
+                a.rec_hi[m] = r;
+                a.rec[m] = r;
+            } else {
+                a.accept[m] = 0;
+                const long long shrunk = static_cast<long long>(static_cast<double>(a.len[m]) * a.shrink);
+                if (shrunk < 1) a.flags[m] = 2; // cannot refine below the Lebesgue grid
+                else a.len[m] = shrunk;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// accepted paths: u <- u3, and the record snapshots taken at the new k0
+__global__ void ad_commit_kernel(AdArgs a, const double* __restrict__ u3, double* __restrict__ U,
+                                 double* const* __restrict__ recs, uint8_t* __restrict__ rec_status) {
+    for (size_t m = blockIdx.y; m < a.M; m += gridDim.y) {
+        if (!a.accept[m]) continue;
+        const int lo = a.rec_lo[m], hi = a.rec_hi[m];
+        const double* src = u3 + m * a.n;
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < a.n;
+             i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+            const double v = src[i];
+            U[m * a.n + i] = v;
+            for (int r = lo; r < hi && r < a.R - 1; ++r) recs[r][m * a.n + i] = v;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            for (int r = lo; r < hi; ++r) rec_status[static_cast<size_t>(r) * a.M + m] = 0;
+    }
+}
+
+} // namespace
+
+s2b_ensemble* solve_adaptive(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfg,
+                             const s2b_adaptive_config* ad, const double* phi, const s2b_paths* paths,
+                             s2b_magnus_stats* stats) {
+    if (!ad || !ad->enabled) fail(S2B_ERR_CONFIG, "solve_adaptive_magnus: adaptive flag not set");
+    if (!(ad->shrink > 0.0 && ad->shrink < 1.0))
+        fail(S2B_ERR_CONFIG, "solve_adaptive_magnus: shrink factor must lie in (0, 1)");
+    if (op->order < 3) fail(S2B_ERR_CONFIG, "solve_adaptive_magnus: needs order-3 commutators");
+    const WindowPlan plan = plan_windows(cfg->dt, cfg->T, paths->dt_leb, paths->steps, cfg->record_times,
+                                         cfg->n_record, "solver");
+    const size_t M = paths->M, n = op->nx * op->nv;
+    const int R = static_cast<int>(plan.record_steps.size());
+    // the attempt runner: a one-window session (window = one Lebesgue step; the weights are
+    // supplied per attempt), no norm cap inside (the cap applies to accepted windows only)
+    s2b_magnus_config c1 = *cfg;
+    c1.order = 3;
+    c1.dt = paths->dt_leb;
+    c1.T = paths->dt_leb;
+    c1.blowup_norm_cap = HUGE_VAL;
+    c1.record_times = nullptr;
+    c1.n_record = 0;
+    MagnusSession* s = session_create(ctx, op, &c1, phi, paths);
+    auto* e = new s2b_ensemble();
+    try {
+        s->external_prepare = true;
+        e->ctx = ctx;
+        e->R = R;
+        e->M = M;
+        e->nx = op->nx;
+        e->nv = op->nv;
+        e->seed = paths->seed;
+        e->grid = op->grid;
+        for (size_t r : plan.record_steps) e->times.push_back(static_cast<double>(r) * paths->dt_leb);
+        e->status.alloc(static_cast<size_t>(R) * M);
+        S2B_CUDA(cudaMemsetAsync(e->status.p, 1, e->status.bytes(), ctx->stream));
+        for (int r = 0; r + 1 < R; ++r) e->states.emplace_back(M * n);
+        DevBuf<double> U(M * n), A(M * n), ctab2(M * 6);
+        broadcast_rows(ctx, U.p, phi, n, M);
+        DevBuf<long long> k0(M), len(M), rsteps(R);
+        DevBuf<int> fresh(M), flags(M), rec(M), rlo(M), rhi(M), acc(M), st3(M), live(1);
+        std::vector<int> ones(M, 1);
+        S2B_CUDA(cudaMemsetAsync(k0.p, 0, k0.bytes(), ctx->stream));
+        S2B_CUDA(cudaMemcpyAsync(fresh.p, ones.data(), M * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+        S2B_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes(), ctx->stream));
+        S2B_CUDA(cudaMemsetAsync(rec.p, 0, rec.bytes(), ctx->stream));
+        std::vector<long long> rs(plan.record_steps.begin(), plan.record_steps.end());
+        S2B_CUDA(cudaMemcpyAsync(rsteps.p, rs.data(), R * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+        std::vector<double*> rp;
+        for (auto& b : e->states) rp.push_back(b.p);
+        DevBuf<double*> drp(std::max<size_t>(1, rp.size()));
+        if (!rp.empty())
+            S2B_CUDA(cudaMemcpyAsync(drp.p, rp.data(), rp.size() * sizeof(double*), cudaMemcpyHostToDevice, ctx->stream));
+        AdArgs a{};
+        a.values = paths->d_values.p;
+        a.vstride = paths->steps + 1;
+        a.M = M;
+        a.n = n;
+        a.dt_leb = paths->dt_leb;
+        a.dt_steps = static_cast<long long>(plan.dt_steps);
+        a.total = static_cast<long long>(plan.total_steps);
+        a.rec_steps = rsteps.p;
+        a.R = R;
+        a.k0 = k0.p;
+        a.len = len.p;
+        a.fresh = fresh.p;
+        a.flags = flags.p;
+        a.rec = rec.p;
+        a.rec_lo = rlo.p;
+        a.rec_hi = rhi.p;
+        a.accept = acc.p;
+        a.ctab3 = s->ctab.p; // the session's window-0 weights
+        a.ctab2 = ctab2.p;
+        a.live = live.p;
+        a.tau = ad->tolerance;
+        a.shrink = ad->shrink;
+        a.cap = cfg->blowup_norm_cap;
+        const unsigned gm = static_cast<unsigned>((M + 255) / 256);
+        OpView ov{op->d_pair_begin.p, op->d_pair_slot.p, op->d_w.p, static_cast<int>(op->nx),
+                  static_cast<int>(op->nv), op->compressed};
+        auto norms = [&]() {
+            for (size_t m0 = 0; m0 < M; m0 += (1u << 30)) {
+                const size_t mc = std::min<size_t>(M - m0, 1u << 30);
+                norm_kernel<<<static_cast<unsigned>(mc), 256, 0, ctx->stream>>>(
+                    ov, s->bits.p, s->nbits, op->rx, s->ctab.p + m0 * 6, 1, 0, 1, cfg->expmv_theta,
+                    s->stab.p + m0, nullptr);
+                S2B_LAUNCHED(ctx);
+            }
+        };
+        auto run = [&]() {
+            S2B_CUDA(cudaMemcpyAsync(s->S[0].p, U.p, U.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
+            ad_reset_kernel<<<gm, 256, 0, ctx->stream>>>(s->iv.p, M, flags.p);
+            S2B_LAUNCHED(ctx);
+            S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), ctx->stream));
+            s->cur = 0;
+            s->cur_window = 0;
+            session_advance(s, 1);
+        };
+        const dim3 gg(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64)), static_cast<unsigned>(std::min<size_t>(M, 65535)));
+        int h_live = 0;
+        while (true) {
+            S2B_CUDA(cudaMemsetAsync(live.p, 0, sizeof(int), ctx->stream));
+            ad_prepare_kernel<<<gm, 256, 0, ctx->stream>>>(a);
+            S2B_LAUNCHED(ctx);
+            S2B_CUDA(cudaMemcpyAsync(&h_live, live.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (h_live == 0) break;
+            norms(); // order 3
+            run();
+            ad_save_status_kernel<<<gm, 256, 0, ctx->stream>>>(s->iv.p + 4 * M, st3.p, M);
+            S2B_LAUNCHED(ctx);
+            gather_kernel<<<gg, 256, 0, ctx->stream>>>(s->iv.p + 5 * M, s->S[0].p, s->S[1].p, A.p, n, M);
+            S2B_LAUNCHED(ctx);
+            S2B_CUDA(cudaMemcpyAsync(s->ctab.p, ctab2.p, M * 6 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+            norms(); // order 2
+            run();
+            ad_gap_kernel<<<static_cast<unsigned>(std::min<size_t>(M, 65535)), 256, 0, ctx->stream>>>(
+                a, A.p, s->S[0].p, s->S[1].p, s->iv.p + 5 * M, st3.p, s->iv.p + 4 * M);
+            S2B_LAUNCHED(ctx);
+            ad_commit_kernel<<<gg, 256, 0, ctx->stream>>>(a, A.p, U.p, drp.p, e->status.p);
+            S2B_LAUNCHED(ctx);
+        }
+        if (stats) session_stats(s, stats);
+        e->states.push_back(std::move(U));
+        S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        delete e;
+        session_destroy(s);
+        throw;
+    }
+    session_destroy(s);
+    return e;
 }
 
 } // namespace s2b
