@@ -15,6 +15,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <iosfwd>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -107,6 +108,10 @@ private:
     std::vector<std::int32_t> ci_;
     std::vector<double> val_;
 };
+
+// write_triplets (sparse.hpp:104): "row col value" lines (%zu %d %.17g) in CSR order.
+void write_triplets(const SparseMatrix& m, std::ostream& os);
+
 
 SparseMatrix tridiag(std::size_t n, double lo, double mid, double hi, double scale);
 SparseMatrix kron(const SparseMatrix& a, const SparseMatrix& b);
@@ -213,6 +218,8 @@ struct BrownianBatch {
     std::size_t index_of(double t) const;
 };
 BrownianBatch simulate_brownian(double T, double dt_leb, std::size_t M, std::uint64_t seed);
+// dump_path (stochastics.hpp:91): "t value" lines (%.12g %.17g) of path m, k = 0..steps.
+void dump_path(const BrownianBatch& batch, std::size_t m, std::ostream& os);
 
 struct PathSegment {
     const std::vector<double>* path = nullptr;

@@ -11,6 +11,8 @@
 #include <cmath>
 #include <limits>
 #include <numbers>
+#include <ostream>
+#include <cstdio>
 #include <string>
 
 #include "spde2d_b200.hpp"
@@ -486,6 +488,30 @@ double NormalStream::next() {
     cached_ = r * std::sin(ang);
     has_cached_ = true;
     return r * std::cos(ang);
+}
+
+// ---- text output used by the reference's experiment layer ---------------------------
+// dump_path (stochastics.cpp:229-237): one "t value" line per Lebesgue index.
+void dump_path(const BrownianBatch& batch, std::size_t m, std::ostream& os) {
+    if (m >= batch.M) throw ConfigError("dump_path: trajectory index out of range");
+    char line[96];
+    for (std::size_t k = 0; k <= batch.steps; ++k) {
+        std::snprintf(line, sizeof line, "%.12g %.17g\n", static_cast<double>(k) * batch.dt_leb, batch.values[m][k]);
+        os << line;
+    }
+}
+
+// write_triplets (sparse.cpp:352-363): "row col value" per stored entry, CSR order.
+void write_triplets(const SparseMatrix& m, std::ostream& os) {
+    const auto rp = m.row_ptr();
+    const auto ci = m.col_idx();
+    const auto v = m.values();
+    char line[96];
+    for (std::size_t r = 0; r < m.rows(); ++r)
+        for (std::size_t q = rp[r]; q < rp[r + 1]; ++q) {
+            std::snprintf(line, sizeof line, "%zu %d %.17g\n", r, ci[q], v[q]);
+            os << line;
+        }
 }
 
 BrownianBatch simulate_brownian(double T, double dt_leb, std::size_t M, std::uint64_t seed) {
