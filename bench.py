@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--d", type=int, default=256)
     ap.add_argument("--paths", type=int, default=16384, help="paths per GPU")
     ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--family", default="langevin-constant",
+                    choices=["langevin-constant", "langevin-variable"],
+                    help="coefficient family (cfg3 = langevin-variable)")
     ap.add_argument("--dt", type=float, default=0.01)
     ap.add_argument("--dt-leb", type=float, default=1e-4)
     ap.add_argument("--T", type=float, default=1.0)
@@ -167,7 +170,7 @@ def cpu_reference_leg(args, n_paths, windows, reps=1):
     """The reference C++ (oracle/_ref, OpenMP on every host core) on a bounded sample:
     `n_paths` paths over `windows` Magnus windows of the same workload."""
     from oracle import ref
-    ops = ref.Ops("langevin-constant", args.d, a=A_LANGEVIN, sigma=SIGMA, order=args.order)
+    ops = ref.Ops(args.family, args.d, a=A_LANGEVIN, sigma=SIGMA, order=args.order)
     T = windows * args.dt
     vals, _ = ref.simulate_brownian(T, args.dt_leb, n_paths, args.seed)
     threads = ref.max_threads()
@@ -217,7 +220,7 @@ def run_ours(args):
     grid = s2b.GridSpec.square(args.d)
     n = grid.dim()
     M = args.paths
-    op = s2b.Operator.from_family(grid, "langevin-constant", a=A_LANGEVIN, sigma=SIGMA,
+    op = s2b.Operator.from_family(grid, args.family, a=A_LANGEVIN, sigma=SIGMA,
                                   order=args.order, ctx=ctx)
     paths = s2b.BrownianPaths.philox(args.T, args.dt_leb, M, seed=args.seed,
                                      path_offset=rank * M, ctx=ctx)
@@ -340,10 +343,11 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Philox Brownian paths, Gaussian datum, Langevin a=1.1 sigma=1/sqrt(10))",
-        "config": {"workload": f"cfg2: constant-coefficient Langevin {args.d}x{args.d}, {M} paths/GPU, "
+        "config": {"workload": (f"cfg2: constant-coefficient Langevin" if args.family == "langevin-constant"
+                                else f"cfg3: variable-coefficient Langevin") + f" {args.d}x{args.d}, {M} paths/GPU, "
                                f"order-{args.order} iterated Magnus, dt={args.dt} ({nwin} windows), "
                                f"T={args.T}, dt_leb={args.dt_leb}, tol=1e-10, theta=1",
-                   "grid": args.d, "paths_per_gpu": M, "order": args.order, "dt": args.dt,
+                   "grid": args.d, "family": args.family, "paths_per_gpu": M, "order": args.order, "dt": args.dt,
                    "windows_per_step": 1, "parallelism": f"path-sharded x{world}",
                    "l2": "inputs larger than L2 (34 GB resident state per GPU)"},
         "path_terms_per_window": terms / max(1, M * args.steps),
@@ -384,7 +388,7 @@ def run_ours(args):
 
 def euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, world, M, n):
     """E-M at dt = dt_leb on the same paths: path*gridpoint*steps/s (16 B/pt/step roofline)."""
-    f = s2b.Fields.from_family(grid, "langevin-constant", a=A_LANGEVIN, sigma=SIGMA, ctx=ctx)
+    f = s2b.Fields.from_family(grid, args.family, a=A_LANGEVIN, sigma=SIGMA, ctx=ctx)
     steps = args.euler_steps
     T = steps * args.dt_leb
     cfg = s2b.EulerConfig(dt=args.dt_leb)
