@@ -216,6 +216,189 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_kernel(EmXmArgs a) {
     }
 }
 
+// In-place variant for grids whose double-buffered state exceeds a cluster (512^2: 4 MB per
+// path vs 3.6 MB in a 16-CTA cluster): one state buffer updated in place.  Within a warp a
+// column is read into the register rings before it is overwritten (program order); the
+// columns a warp reads from its neighbour segments (x0-1, x0+LX) are preloaded before a CTA
+// barrier; the halo rows from the neighbour CTAs are double-buffered by step parity (two
+// slot sets per side: row -1 at index 1 / 0, row RPC at RPC+2 / RPC+3).
+template <int NX, int RPC, int NT, int P, int MASK, int CL>
+__global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
+    static_assert((MASK & 16) == 0, "in-place E-M: no mixed derivative");
+    constexpr int TRI = RPC + 4;
+    constexpr int TX = NX + 2;
+    constexpr int TBUF = TX * TRI;
+    constexpr int NSEG = NT / RPC;
+    constexpr int LX = NX / NSEG;
+    constexpr int R0 = P + 2; // row j ring: columns c-1 .. c+P
+    static_assert(NT % RPC == 0 && NX % NSEG == 0 && LX % P == 0, "x-march shape");
+
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int t = threadIdx.x;
+    const int r = t % RPC;
+    const int seg = t / RPC;
+    const int x0 = seg * LX;
+    const int row0 = rank * RPC;
+    const int j = row0 + r;
+    const int n = NX * a.nv;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* U = reinterpret_cast<double*>(smem_raw); // [TX][TRI]
+    __shared__ int next_path;
+
+    auto ridx = [&](int row, int par) {
+        int i = 2 + row;
+        if (par) i += row < 0 ? -1 : (row >= RPC ? 1 : 0);
+        return i;
+    };
+    const bool has_lo = rank > 0, has_hi = rank < CL - 1;
+    const int cb = (x0 + 1) * TRI;
+    double* rem0 = nullptr;
+    double* rem1 = nullptr;
+    if (r == 0 && has_lo) {
+        double* nb = cluster.map_shared_rank(U, rank - 1);
+        rem0 = nb + cb + ridx(RPC, 0);
+        rem1 = nb + cb + ridx(RPC, 1);
+    } else if (r == RPC - 1 && has_hi) {
+        double* nb = cluster.map_shared_rank(U, rank + 1);
+        rem0 = nb + cb + ridx(-1, 0);
+        rem1 = nb + cb + ridx(-1, 1);
+    }
+    const bool do_rem = rem0 != nullptr;
+    int* next0 = cluster.map_shared_rank(&next_path, 0);
+    double* own = U + cb + 2 + r;
+
+    const double fh = (MASK & 1) ? a.rowf[0 * a.nv + j] : 0.0;
+    const double ffx = (MASK & 2) ? a.rowf[1 * a.nv + j] : 0.0;
+    const double ffv = (MASK & 4) ? a.rowf[2 * a.nv + j] : 0.0;
+    const double hgxx = (MASK & 8) ? 0.5 * a.rowf[3 * a.nv + j] : 0.0;
+    const double hgvv = (MASK & 32) ? 0.5 * a.rowf[5 * a.nv + j] : 0.0;
+    const double fsig = (MASK & 64) ? a.rowf[6 * a.nv + j] : 0.0;
+    const double fsx = (MASK & 128) ? a.rowf[7 * a.nv + j] : 0.0;
+    const double fsv = (MASK & 256) ? a.rowf[8 * a.nv + j] : 0.0;
+    const double st0 = a.st[0], st1 = a.st[1], st2 = a.st[2], st3 = a.st[3];
+    const double dt = a.dt;
+
+    for (int q = t; q < TBUF; q += NT) U[q] = 0.0; // zero x-halo columns and outer halo rows
+    int ip = 0;                                    // halo slot set of the current input
+
+    while (true) {
+        if (rank == 0 && t == 0) next_path = atomicAdd(a.work, 1);
+        cl_barrier();
+        const int p = *next0;
+        cl_barrier();
+        if (p >= a.M) break;
+
+        // phi: own rows and (where a neighbour exists) the halo rows of slot set ip
+        for (int q = t; q < (RPC + 2) * NX; q += NT) {
+            const int rr = q / NX - 1, x = q % NX;
+            const int jj = row0 + rr;
+            if (jj < 0 || jj >= a.nv) continue;
+            U[(x + 1) * TRI + ridx(rr, ip)] = a.phi[static_cast<size_t>(jj) * NX + x];
+        }
+        __syncthreads();
+
+        const double* pv = a.values + static_cast<size_t>(p) * a.vstride;
+        double dWn = pv[a.step_leb] - pv[0];
+        int first = INT_MAX;
+        int rec = 0;
+        for (int k = 0; k < a.nsteps; ++k) {
+            const double dW = dWn;
+            if (k + 1 < a.nsteps)
+                dWn = pv[static_cast<size_t>(k + 2) * a.step_leb] - pv[static_cast<size_t>(k + 1) * a.step_leb];
+            const double* rm = U + cb + ridx(r - 1, ip); // row j-1
+            const double* r0 = U + cb + 2 + r;           // row j
+            const double* rp = U + cb + ridx(r + 1, ip); // row j+1
+            double* rout = ip ? rem0 : rem1;             // neighbour slot set ip^1
+            // column x0-1 of row j and column x0+LX of row j: owned by the neighbour segments
+            double w0[R0], wm[P], wp[P];
+            w0[0] = r0[-TRI];
+            w0[1] = r0[0];
+            const double right = r0[LX * TRI];
+            __syncthreads();
+            bool inf_seen = false;
+#pragma unroll
+            for (int i0 = 0; i0 < LX; i0 += P) {
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int c = i0 + q;
+                    w0[(c + 2) % R0] = c + 1 < LX ? r0[(c + 1) * TRI] : right;
+                    wm[q] = rm[c * TRI];
+                    wp[q] = rp[c * TRI];
+                }
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int c = i0 + q;
+                    const double uc = w0[(c + 1) % R0];
+                    const double uxm = w0[c % R0];
+                    const double uxp = w0[(c + 2) % R0];
+                    const double uvm = wm[q];
+                    const double uvp = wp[q];
+                    const double dxu = (uxp - uxm) * st0;
+                    const double dvu = (uvp - uvm) * st2;
+                    double drift = 0.0;
+                    if (MASK & 1) drift += fh * uc;
+                    if (MASK & 2) drift += ffx * dxu;
+                    if (MASK & 4) drift += ffv * dvu;
+                    if (MASK & 8) {
+                        const double dxxu = (uxp - 2.0 * uc + uxm) * st1;
+                        drift += hgxx * dxxu;
+                    }
+                    if (MASK & 32) {
+                        const double dvvu = (uvp - 2.0 * uc + uvm) * st3;
+                        drift += hgvv * dvvu;
+                    }
+                    double noise = 0.0;
+                    if (MASK & 64) noise += fsig * uc;
+                    if (MASK & 128) noise += fsx * dxu;
+                    if (MASK & 256) noise += fsv * dvu;
+                    const double next = uc + drift * dt + noise * dW;
+                    own[c * TRI] = next;
+                    if (do_rem) rout[c * TRI] = next;
+                    inf_seen |= fabs(next) == __longlong_as_double(0x7FF0000000000000LL);
+                }
+            }
+            if (inf_seen && first == INT_MAX) first = k;
+            cl_barrier();
+            ip ^= 1;
+            while (rec < a.R && a.rec_k[rec] == k) {
+                double* dst = a.rec[rec] + static_cast<size_t>(p) * n + static_cast<size_t>(row0) * NX;
+                for (int q = t; q < RPC * NX; q += NT) dst[q] = U[(q % NX + 1) * TRI + 2 + q / NX];
+                ++rec;
+            }
+        }
+        if (first != INT_MAX) atomicMin(a.blow + p, first);
+        __syncthreads();
+    }
+}
+
+template <int MASK>
+void launch_em_ip(s2b_context* ctx, const EmXmArgs& a) {
+    constexpr int NX = 512, RPC = 32, NT = 256, P = 4, CL = 16;
+    auto kern = em_cluster_ip_kernel<NX, RPC, NT, P, MASK, CL>;
+    const size_t smem = 8 * static_cast<size_t>(NX + 2) * (RPC + 4);
+    S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(CL);
+    int clusters = 0;
+    S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
+    clusters = std::max(1, std::min(clusters, a.M));
+    cfg.gridDim = dim3(CL * clusters);
+    S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
 template <int MASK>
 void launch_em(s2b_context* ctx, const EmXmArgs& a) {
     constexpr int NX = 256, RPC = 32, NT = 256, P = 4;
@@ -252,7 +435,8 @@ __global__ void em_cluster_status_kernel(const int* blow, const int* rec_k, int 
 bool em_cluster_supported(const s2b_fields* f) {
     const char* e = std::getenv("S2B_EMXM");
     if (e && e[0] == '0') return false;
-    return f->xinv && f->nx == 256 && f->nv == 256 && f->mask == (2 | 32 | 256);
+    return f->xinv && ((f->nx == 256 && f->nv == 256) || (f->nx == 512 && f->nv == 512)) &&
+           f->mask == (2 | 32 | 256);
 }
 
 void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const double* d_phi,
@@ -282,7 +466,8 @@ void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const do
     a.M = M;
     a.nv = static_cast<int>(f->nv);
     a.work = work.p;
-    launch_em<2 | 32 | 256>(ctx, a);
+    if (f->nx == 512) launch_em_ip<2 | 32 | 256>(ctx, a);
+    else launch_em<2 | 32 | 256>(ctx, a);
     S2B_LAUNCHED(ctx);
     em_cluster_status_kernel<<<(M + 255) / 256, 256, 0, ctx->stream>>>(blow.p, drec_k.p, a.R, d_status, M);
     S2B_LAUNCHED(ctx);

@@ -78,10 +78,11 @@ def em_engine(request, monkeypatch):
 
 
 @pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
-def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine):
-    """solve_euler at 256^2 (constant Langevin: the cluster-resident kernel) vs the reference,
-    with a mid-run record."""
-    d, T, dt_leb, dt, M, seed = 256, 0.01, 1e-4, 1e-4, 3, 21
+@pytest.mark.parametrize("d", [256, 512])
+def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine, d):
+    """solve_euler at 256^2 / 512^2 (constant Langevin: the cluster-resident kernels, in place
+    at 512^2) vs the reference, with a mid-run record."""
+    T, dt_leb, dt, M, seed = 0.01, 1e-4, 1e-4, 3, 21
     ops = ref.Ops("langevin-constant", d, order=1)
     values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
     want, wst, _ = ops.solve_euler(values, dt_leb, T, dt, record_times=[0.005], seed=seed)
@@ -96,9 +97,10 @@ def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine):
 
 
 @pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
-def test_euler_engines_blowup_256(ref, s2b, ctx, em_engine):
+@pytest.mark.parametrize("d", [256, 512])
+def test_euler_engines_blowup_256(ref, s2b, ctx, em_engine, d):
     """dt far beyond the stability bound: Ok (finite, huge) at t = 20, blown by T = 200."""
-    d, T, M, seed = 256, 200.0, 2, 9
+    T, M, seed = 200.0, 2, 9
     values, _ = ref.simulate_brownian(T, 1.0, M, seed)
     ops = ref.Ops("langevin-constant", d, order=1)
     want, wst, _ = ops.solve_euler(values, 1.0, T, 1.0, record_times=[20.0], seed=seed)
