@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "magnus_common.cuh"
 
@@ -116,10 +117,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
     constexpr int NW = NT / 32;
     constexpr int KP = kPairSlots;
     constexpr int NWIN = RE::total();
-    // ring geometry with P points in flight: span + P - 1 slots per stencil row
-#define RSPAN(dv) (RE::span(dv) + P - 1)
-#define ROFF(dv) (RE::off(dv) + ((dv) + KRV) * (P - 1))
-    static_assert(LX % P == 0, "points per thread must be a multiple of P");
+    constexpr int RW = 8;                 // ring slots per stencil row (>= span + P - 1)
+    constexpr int XB = LX < 32 ? LX : 32; // columns per march block (multiple of RW and P)
+    static_assert(RE::span(0) + P - 1 <= RW && RE::span(1) + P - 1 <= RW && RE::span(2) + P - 1 <= RW, "ring size");
+    static_assert(LX % XB == 0 && XB % RW == 0 && XB % P == 0, "march blocks");
     static_assert(NT % RPC == 0 && NX % NSEG == 0 && LX >= 4, "x-march shape");
     static_assert(RPC >= 2 * KRV, "halo rows come from one neighbour");
 
@@ -280,76 +281,89 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
                     double* sp = S + sb;
                     double tm = 0.0, sm = 0.0; // NaN-ignoring maxima of |t|, |accum|
                     unsigned ex = 0;           // max exponent field of accum: all-ones = non-finite
-                    // per-row register rings over absolute columns c (slot (c - lo) mod R),
-                    // R = span + P - 1 so that P adjacent points are in flight
-                    double win[NWIN + (2 * KRV + 1) * (P - 1)];
+                    // per-row register rings of RW (power of two) slots over absolute columns c:
+                    // slot (c - lo) & (RW-1) is periodic in c, so the march is a loop over
+                    // blocks of XB columns (the last block, which may touch the zero x-halo of
+                    // the last segment, is a separate instance)
+                    double win[(2 * KRV + 1) * RW];
 #pragma unroll
                     for (int dv = -KRV; dv <= KRV; ++dv) {
                         if (RE::span(dv) > 0) {
 #pragma unroll
-                            for (int cc = 0; cc < RE::span(dv) - 1; ++cc)
-                                win[ROFF(dv) + cc] = tin[(RE::lo(dv) + cc) * TR + dv];
+                            for (int cc = 0; cc < RW; ++cc) // constant trip count: always unrolled
+                                if (cc < RE::span(dv) - 1) win[(dv + KRV) * RW + cc] = tin[(RE::lo(dv) + cc) * TR + dv];
                         }
                     }
+                    auto block = [&](const int cbase, auto last_tag) {
+                        constexpr bool LAST = decltype(last_tag)::value;
+                        const double* tinb = tin + cbase * TR;
+                        double* toutb = tout + cbase * TR;
+                        double* routb = rout + cbase * TR;
+                        double* spb = sp + cbase * RPC;
+                        const bool first_blk = cbase == 0;
+                        (void)first_blk;
 #pragma unroll
-                    for (int i0 = 0; i0 < LX; i0 += P) {
+                        for (int g = 0; g < XB; g += P) {
 #pragma unroll
-                        for (int dv = -KRV; dv <= KRV; ++dv)
-                            if (RE::span(dv) > 0) {
-#pragma unroll
-                                for (int q = 0; q < P; ++q) {
-                                    const int col = i0 + q + RE::hi(dv);
-                                    win[ROFF(dv) + (col - RE::lo(dv)) % RSPAN(dv)] = tin[col * TR + dv];
-                                }
-                            }
-                        // x-class of each point (boundary only in the first / last segment)
-                        int bcls[P];
-#pragma unroll
-                        for (int q = 0; q < P; ++q) {
-                            const int i = i0 + q;
-                            bcls[q] = -1;
-                            if constexpr (NBB > 0) {
-                                if (i < 2 && seg == 0) bcls[q] = i;
-                                if (i >= LX - 2 && seg == NSEG - 1) bcls[q] = 2 + (i - (LX - 2));
-                            }
-                        }
-                        double acc[P];
-#pragma unroll
-                        for (int q = 0; q < P; ++q) acc[q] = 0.0;
-#pragma unroll
-                        for (int dv = -KRV; dv <= KRV; ++dv) {
-#pragma unroll
-                            for (int dx = -KRX; dx <= KRX; ++dx) {
-                                if (MaskInfo<MASK>::has(dx, dv)) {
-                                    const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
+                            for (int dv = -KRV; dv <= KRV; ++dv)
+                                if (RE::span(dv) > 0) {
 #pragma unroll
                                     for (int q = 0; q < P; ++q) {
-                                        double wv = y[e];
-                                        if constexpr (NBB > 0) {
-                                            if ((BM >> e) & 1) {
-                                                if (bcls[q] >= 0)
-                                                    wv = bY[(bcls[q] * NBB + bm_rank(BM, e)) * RPC + r];
+                                        const int col = g + q + RE::hi(dv);
+                                        win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))] = tinb[col * TR + dv];
+                                    }
+                                }
+                            int bcls[P];
+#pragma unroll
+                            for (int q = 0; q < P; ++q) {
+                                const int i = g + q;
+                                bcls[q] = -1;
+                                if constexpr (NBB > 0) {
+                                    if (i < 2 && first_blk && seg == 0) bcls[q] = i;
+                                    if (LAST && i >= XB - 2 && seg == NSEG - 1) bcls[q] = 2 + (i - (XB - 2));
+                                }
+                            }
+                            double acc[P];
+#pragma unroll
+                            for (int q = 0; q < P; ++q) acc[q] = 0.0;
+#pragma unroll
+                            for (int dv = -KRV; dv <= KRV; ++dv) {
+#pragma unroll
+                                for (int dx = -KRX; dx <= KRX; ++dx) {
+                                    if (MaskInfo<MASK>::has(dx, dv)) {
+                                        const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
+#pragma unroll
+                                        for (int q = 0; q < P; ++q) {
+                                            double wv = y[e];
+                                            if constexpr (NBB > 0) {
+                                                if ((BM >> e) & 1) {
+                                                    if (bcls[q] >= 0)
+                                                        wv = bY[(bcls[q] * NBB + bm_rank(BM, e)) * RPC + r];
+                                                }
                                             }
+                                            const int col = g + q + dx;
+                                            acc[q] += wv * win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))];
                                         }
-                                        const int col = i0 + q + dx;
-                                        acc[q] += wv * win[ROFF(dv) + (col - RE::lo(dv)) % RSPAN(dv)];
                                     }
                                 }
                             }
-                        }
 #pragma unroll
-                        for (int q = 0; q < P; ++q) {
-                            const int i = i0 + q;
-                            const double tv = acc[q] * inv;
-                            const double sv = sp[i * RPC] + tv;
-                            tout[i * TR] = tv;
-                            if (do_rem) rout[i * TR] = tv;
-                            sp[i * RPC] = sv;
-                            if (fabs(tv) > tm) tm = abs_of(tv);
-                            if (fabs(sv) > sm) sm = abs_of(sv);
-                            ex = max(ex, static_cast<unsigned>(__double2hiint(sv)) & 0x7ff00000u);
+                            for (int q = 0; q < P; ++q) {
+                                const int i = g + q;
+                                const double tv = acc[q] * inv;
+                                const double sv = spb[i * RPC] + tv;
+                                toutb[i * TR] = tv;
+                                if (do_rem) routb[i * TR] = tv;
+                                spb[i * RPC] = sv;
+                                if (fabs(tv) > tm) tm = abs_of(tv);
+                                if (fabs(sv) > sm) sm = abs_of(sv);
+                                ex = max(ex, static_cast<unsigned>(__double2hiint(sv)) & 0x7ff00000u);
+                            }
                         }
-                    }
+                    };
+#pragma unroll 1
+                    for (int cbase = 0; cbase < LX - XB; cbase += XB) block(cbase, std::false_type{});
+                    block(LX - XB, std::true_type{});
                     if (ex == 0x7ff00000u) sm = __longlong_as_double(0x7FF8000000000000LL); // non-finite
                     // path-wide max|t|, max|accum| (NaN-ranked): warps -> CTA -> every rank
                     const unsigned long long wtb = warp_max_bits(dbits(tm));
