@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_kernel(EmXmArgs a) {
 // columns a warp reads from its neighbour segments (x0-1, x0+LX) are preloaded before a CTA
 // barrier; the halo rows from the neighbour CTAs are double-buffered by step parity (two
 // slot sets per side: row -1 at index 1 / 0, row RPC at RPC+2 / RPC+3).
-template <int NX, int RPC, int NT, int P, int MASK, int CL>
+template <int NX, int RPC, int NT, int P, int MASK, int CL, int NP>
 __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
     static_assert((MASK & 16) == 0, "in-place E-M: no mixed derivative");
     constexpr int TRI = RPC + 4;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
     const int n = NX * a.nv;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* U = reinterpret_cast<double*>(smem_raw); // [TX][TRI]
+    double* U = reinterpret_cast<double*>(smem_raw); // [NP][TX][TRI]: NP paths per cluster
     __shared__ int next_path;
 
     auto ridx = [&](int row, int par) {
@@ -267,7 +267,6 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
     }
     const bool do_rem = rem0 != nullptr;
     int* next0 = cluster.map_shared_rank(&next_path, 0);
-    double* own = U + cb + 2 + r;
 
     const double fh = (MASK & 1) ? a.rowf[0 * a.nv + j] : 0.0;
     const double ffx = (MASK & 2) ? a.rowf[1 * a.nv + j] : 0.0;
@@ -280,104 +279,132 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
     const double st0 = a.st[0], st1 = a.st[1], st2 = a.st[2], st3 = a.st[3];
     const double dt = a.dt;
 
-    for (int q = t; q < TBUF; q += NT) U[q] = 0.0; // zero x-halo columns and outer halo rows
-    int ip = 0;                                    // halo slot set of the current input
+    for (int q = t; q < NP * TBUF; q += NT) U[q] = 0.0; // zero x-halo columns and outer halo rows
+    int ip = 0;                                         // halo slot set of the current input
 
     while (true) {
-        if (rank == 0 && t == 0) next_path = atomicAdd(a.work, 1);
+        if (rank == 0 && t == 0) next_path = atomicAdd(a.work, NP);
         cl_barrier();
-        const int p = *next0;
+        const int pbase = *next0;
         cl_barrier();
-        if (p >= a.M) break;
+        if (pbase >= a.M) break;
+        const int np = a.M - pbase < NP ? a.M - pbase : NP; // paths this cluster carries now
 
         // phi: own rows and (where a neighbour exists) the halo rows of slot set ip
-        for (int q = t; q < (RPC + 2) * NX; q += NT) {
-            const int rr = q / NX - 1, x = q % NX;
+        for (int q = t; q < np * (RPC + 2) * NX; q += NT) {
+            const int pi = q / ((RPC + 2) * NX), qq = q % ((RPC + 2) * NX);
+            const int rr = qq / NX - 1, x = qq % NX;
             const int jj = row0 + rr;
             if (jj < 0 || jj >= a.nv) continue;
-            U[(x + 1) * TRI + ridx(rr, ip)] = a.phi[static_cast<size_t>(jj) * NX + x];
+            U[pi * TBUF + (x + 1) * TRI + ridx(rr, ip)] = a.phi[static_cast<size_t>(jj) * NX + x];
         }
         __syncthreads();
 
-        const double* pv = a.values + static_cast<size_t>(p) * a.vstride;
-        double dWn = pv[a.step_leb] - pv[0];
-        int first = INT_MAX;
+        const double* pv[NP];
+        double dWn[NP];
+        int first[NP];
+#pragma unroll
+        for (int pi = 0; pi < NP; ++pi) {
+            pv[pi] = a.values + static_cast<size_t>(pbase + (pi < np ? pi : 0)) * a.vstride;
+            dWn[pi] = pv[pi][a.step_leb] - pv[pi][0];
+            first[pi] = INT_MAX;
+        }
         int rec = 0;
         for (int k = 0; k < a.nsteps; ++k) {
-            const double dW = dWn;
-            if (k + 1 < a.nsteps)
-                dWn = pv[static_cast<size_t>(k + 2) * a.step_leb] - pv[static_cast<size_t>(k + 1) * a.step_leb];
-            const double* rm = U + cb + ridx(r - 1, ip); // row j-1
-            const double* r0 = U + cb + 2 + r;           // row j
-            const double* rp = U + cb + ridx(r + 1, ip); // row j+1
-            double* rout = ip ? rem0 : rem1;             // neighbour slot set ip^1
-            // column x0-1 of row j and column x0+LX of row j: owned by the neighbour segments
-            double w0[R0], wm[P], wp[P];
-            w0[0] = r0[-TRI];
-            w0[1] = r0[0];
-            const double right = r0[LX * TRI];
-            __syncthreads();
-            bool inf_seen = false;
+            double dW[NP];
 #pragma unroll
-            for (int i0 = 0; i0 < LX; i0 += P) {
-#pragma unroll
-                for (int q = 0; q < P; ++q) {
-                    const int c = i0 + q;
-                    w0[(c + 2) % R0] = c + 1 < LX ? r0[(c + 1) * TRI] : right;
-                    wm[q] = rm[c * TRI];
-                    wp[q] = rp[c * TRI];
-                }
-#pragma unroll
-                for (int q = 0; q < P; ++q) {
-                    const int c = i0 + q;
-                    const double uc = w0[(c + 1) % R0];
-                    const double uxm = w0[c % R0];
-                    const double uxp = w0[(c + 2) % R0];
-                    const double uvm = wm[q];
-                    const double uvp = wp[q];
-                    const double dxu = (uxp - uxm) * st0;
-                    const double dvu = (uvp - uvm) * st2;
-                    double drift = 0.0;
-                    if (MASK & 1) drift += fh * uc;
-                    if (MASK & 2) drift += ffx * dxu;
-                    if (MASK & 4) drift += ffv * dvu;
-                    if (MASK & 8) {
-                        const double dxxu = (uxp - 2.0 * uc + uxm) * st1;
-                        drift += hgxx * dxxu;
-                    }
-                    if (MASK & 32) {
-                        const double dvvu = (uvp - 2.0 * uc + uvm) * st3;
-                        drift += hgvv * dvvu;
-                    }
-                    double noise = 0.0;
-                    if (MASK & 64) noise += fsig * uc;
-                    if (MASK & 128) noise += fsx * dxu;
-                    if (MASK & 256) noise += fsv * dvu;
-                    const double next = uc + drift * dt + noise * dW;
-                    own[c * TRI] = next;
-                    if (do_rem) rout[c * TRI] = next;
-                    inf_seen |= fabs(next) == __longlong_as_double(0x7FF0000000000000LL);
-                }
+            for (int pi = 0; pi < NP; ++pi) {
+                dW[pi] = dWn[pi];
+                if (k + 1 < a.nsteps)
+                    dWn[pi] = pv[pi][static_cast<size_t>(k + 2) * a.step_leb] - pv[pi][static_cast<size_t>(k + 1) * a.step_leb];
             }
-            if (inf_seen && first == INT_MAX) first = k;
+            // columns x0-1 and x0+LX of row j belong to the neighbour segments: read them first
+            double lft[NP], cur0[NP], right[NP];
+#pragma unroll
+            for (int pi = 0; pi < NP; ++pi) {
+                const double* r0 = U + pi * TBUF + cb + 2 + r;
+                lft[pi] = r0[-TRI];
+                cur0[pi] = r0[0];
+                right[pi] = r0[LX * TRI];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int pi = 0; pi < NP; ++pi) {
+                if (pi >= np) break;
+                const double* rm = U + pi * TBUF + cb + ridx(r - 1, ip); // row j-1
+                const double* r0 = U + pi * TBUF + cb + 2 + r;           // row j
+                const double* rp = U + pi * TBUF + cb + ridx(r + 1, ip); // row j+1
+                double* own = U + pi * TBUF + cb + 2 + r;
+                double* rout = (ip ? rem0 : rem1) + pi * TBUF;           // neighbour slot set ip^1
+                double w0[R0], wm[P], wp[P];
+                w0[0] = lft[pi];
+                w0[1] = cur0[pi];
+                bool inf_seen = false;
+#pragma unroll
+                for (int i0 = 0; i0 < LX; i0 += P) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const int c = i0 + q;
+                        w0[(c + 2) % R0] = c + 1 < LX ? r0[(c + 1) * TRI] : right[pi];
+                        wm[q] = rm[c * TRI];
+                        wp[q] = rp[c * TRI];
+                    }
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const int c = i0 + q;
+                        const double uc = w0[(c + 1) % R0];
+                        const double uxm = w0[c % R0];
+                        const double uxp = w0[(c + 2) % R0];
+                        const double uvm = wm[q];
+                        const double uvp = wp[q];
+                        const double dxu = (uxp - uxm) * st0;
+                        const double dvu = (uvp - uvm) * st2;
+                        double drift = 0.0;
+                        if (MASK & 1) drift += fh * uc;
+                        if (MASK & 2) drift += ffx * dxu;
+                        if (MASK & 4) drift += ffv * dvu;
+                        if (MASK & 8) {
+                            const double dxxu = (uxp - 2.0 * uc + uxm) * st1;
+                            drift += hgxx * dxxu;
+                        }
+                        if (MASK & 32) {
+                            const double dvvu = (uvp - 2.0 * uc + uvm) * st3;
+                            drift += hgvv * dvvu;
+                        }
+                        double noise = 0.0;
+                        if (MASK & 64) noise += fsig * uc;
+                        if (MASK & 128) noise += fsx * dxu;
+                        if (MASK & 256) noise += fsv * dvu;
+                        const double next = uc + drift * dt + noise * dW[pi];
+                        own[c * TRI] = next;
+                        if (do_rem) rout[c * TRI] = next;
+                        inf_seen |= fabs(next) == __longlong_as_double(0x7FF0000000000000LL);
+                    }
+                }
+                if (inf_seen && first[pi] == INT_MAX) first[pi] = k;
+            }
             cl_barrier();
             ip ^= 1;
             while (rec < a.R && a.rec_k[rec] == k) {
-                double* dst = a.rec[rec] + static_cast<size_t>(p) * n + static_cast<size_t>(row0) * NX;
-                for (int q = t; q < RPC * NX; q += NT) dst[q] = U[(q % NX + 1) * TRI + 2 + q / NX];
+                for (int pi = 0; pi < np; ++pi) {
+                    double* dst = a.rec[rec] + static_cast<size_t>(pbase + pi) * n + static_cast<size_t>(row0) * NX;
+                    for (int q = t; q < RPC * NX; q += NT) dst[q] = U[pi * TBUF + (q % NX + 1) * TRI + 2 + q / NX];
+                }
                 ++rec;
             }
         }
-        if (first != INT_MAX) atomicMin(a.blow + p, first);
+#pragma unroll
+        for (int pi = 0; pi < NP; ++pi)
+            if (pi < np && first[pi] != INT_MAX) atomicMin(a.blow + pbase + pi, first[pi]);
         __syncthreads();
     }
 }
 
-template <int MASK>
+template <int MASK, int NX, int CL, int NP>
 void launch_em_ip(s2b_context* ctx, const EmXmArgs& a) {
-    constexpr int NX = 512, RPC = 32, NT = 256, P = 4, CL = 16;
-    auto kern = em_cluster_ip_kernel<NX, RPC, NT, P, MASK, CL>;
-    const size_t smem = 8 * static_cast<size_t>(NX + 2) * (RPC + 4);
+    constexpr int RPC = 32, NT = 256, P = 4;
+    auto kern = em_cluster_ip_kernel<NX, RPC, NT, P, MASK, CL, NP>;
+    const size_t smem = 8 * static_cast<size_t>(NP) * (NX + 2) * (RPC + 4);
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
@@ -432,6 +459,16 @@ __global__ void em_cluster_status_kernel(const int* blow, const int* rec_k, int 
 
 } // namespace
 
+// 256^2: S2B_EM_NP (3) paths per cluster in place (one barrier per step for all); S2B_EM2=0 selects
+// the double-buffered one-path kernel
+#ifndef S2B_EM_NP
+#define S2B_EM_NP 3
+#endif
+bool em_multi_path() {
+    const char* e = std::getenv("S2B_EM2");
+    return !(e && e[0] == '0');
+}
+
 bool em_cluster_supported(const s2b_fields* f) {
     const char* e = std::getenv("S2B_EMXM");
     if (e && e[0] == '0') return false;
@@ -466,7 +503,8 @@ void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const do
     a.M = M;
     a.nv = static_cast<int>(f->nv);
     a.work = work.p;
-    if (f->nx == 512) launch_em_ip<2 | 32 | 256>(ctx, a);
+    if (f->nx == 512) launch_em_ip<2 | 32 | 256, 512, 16, 1>(ctx, a);
+    else if (em_multi_path()) launch_em_ip<2 | 32 | 256, 256, 8, S2B_EM_NP>(ctx, a);
     else launch_em<2 | 32 | 256>(ctx, a);
     S2B_LAUNCHED(ctx);
     em_cluster_status_kernel<<<(M + 255) / 256, 256, 0, ctx->stream>>>(blow.p, drec_k.p, a.R, d_status, M);
