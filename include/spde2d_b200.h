@@ -196,6 +196,13 @@ int s2b_solve_magnus(s2b_context *ctx, const s2b_operator *op, const s2b_magnus_
                      s2b_magnus_stats *stats);
 int s2b_solve_euler(s2b_context *ctx, const s2b_fields *f, const s2b_euler_config *cfg,
                     const double *phi, const s2b_paths *paths, s2b_ensemble **out);
+/* A step-size sweep on shared paths (run_stepsize_sweep, experiment.cpp:486-551): ncfg
+ * configurations (typically the same order at several dt) solved in batched launches -- one
+ * persistent launch carries the paths of up to 8 configurations on the x-march engines.
+ * outs[i] / stats[i] (stats may be NULL) as s2b_solve_magnus would return for cfgs[i]. */
+int s2b_solve_magnus_sweep(s2b_context *ctx, const s2b_operator *op, const s2b_magnus_config *cfgs,
+                           size_t ncfg, const double *phi, const s2b_paths *paths, s2b_ensemble **outs,
+                           s2b_magnus_stats *stats);
 /* solve_adaptive_magnus (magnus.cpp:306-404): orders 2 and 3 per window from one weight
  * build, accept order 3 when the relative gap <= tolerance, else shrink and retry.
  * cfg->order is ignored (the operator must carry order-3 commutators). */

@@ -474,6 +474,24 @@ def solve_iterated_magnus(cfg: MagnusConfig, comms: Operator, phi, batch: Browni
     return _ensembles(h, grid, batch.seed, comms.ctx)
 
 
+def solve_iterated_magnus_sweep(cfgs: Sequence[MagnusConfig], comms: Operator, phi, batch: BrownianPaths, T,
+                                grid: GridSpec, stats: Optional[list] = None):
+    """Several MagnusConfigs (e.g. one order at several dt) on shared paths in batched launches
+    (run_stepsize_sweep, experiment.cpp:486-551).  Returns one ensemble list per config."""
+    if len(phi) != grid.dim() or comms.grid.dim() != grid.dim():
+        raise DimensionError("solve_iterated_magnus_sweep: dimension mismatch")
+    n = len(cfgs)
+    made = [c.c(T) for c in cfgs]
+    arr = (_capi.MagnusConfig * n)(*[m[0] for m in made])
+    phi = np.ascontiguousarray(phi, np.float64)
+    outs = (C.c_void_p * n)()
+    st = (_capi.MagnusStats * n)()
+    _check(lib().s2b_solve_magnus_sweep(comms.ctx.h, comms.h, arr, n, _dptr(phi), batch.h, outs, st))
+    if stats is not None:
+        stats.extend({k: getattr(x, k) for k, _ in _capi.MagnusStats._fields_} for x in st)
+    return [_ensembles(C.c_void_p(h), grid, batch.seed, comms.ctx) for h in outs]
+
+
 def solve_adaptive_magnus(cfg: MagnusConfig, comms: Operator, phi, batch: BrownianPaths, T,
                           grid: GridSpec, stats: Optional[dict] = None):
     """solve_adaptive_magnus (magnus.hpp:104-108): orders 2 and 3 per window, shrink-and-retry

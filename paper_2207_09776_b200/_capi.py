@@ -92,6 +92,8 @@ SIGNATURES = {
     "s2b_solve_magnus": (C.c_int, [_VP, _VP, _P(MagnusConfig), _P(C.c_double), _VP, _P(_VP),
                                    _P(MagnusStats)]),
     "s2b_solve_euler": (C.c_int, [_VP, _VP, _P(EulerConfig), _P(C.c_double), _VP, _P(_VP)]),
+    "s2b_solve_magnus_sweep": (C.c_int, [_VP, _VP, _P(MagnusConfig), C.c_size_t, _P(C.c_double), _VP, _P(_VP),
+                                         _P(MagnusStats)]),
     "s2b_solve_adaptive_magnus": (C.c_int, [_VP, _VP, _P(MagnusConfig), _P(AdaptiveConfig), _P(C.c_double),
                                             _VP, _P(_VP), _P(MagnusStats)]),
     "s2b_magnus_session_create": (C.c_int, [_VP, _VP, _P(MagnusConfig), _P(C.c_double), _VP,

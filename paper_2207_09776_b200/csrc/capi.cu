@@ -369,6 +369,32 @@ int s2b_solve_magnus(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_
     });
 }
 
+int s2b_solve_magnus_sweep(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfgs, size_t ncfg,
+                           const double* phi, const s2b_paths* paths, s2b_ensemble** outs, s2b_magnus_stats* stats) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(op, "op");
+        need(cfgs, "cfgs");
+        need(phi, "phi");
+        need(paths, "paths");
+        need(outs, "outs");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        std::vector<MagnusSession*> ss;
+        try {
+            for (size_t i = 0; i < ncfg; ++i) ss.push_back(session_create(ctx, op, &cfgs[i], phi, paths));
+            sessions_run_batched(ss.data(), static_cast<int>(ss.size()));
+            for (size_t i = 0; i < ncfg; ++i) {
+                if (stats) session_stats(ss[i], &stats[i]);
+                outs[i] = session_finish(ss[i]);
+            }
+        } catch (...) {
+            for (auto* s : ss) session_destroy(s);
+            throw;
+        }
+        for (auto* s : ss) session_destroy(s);
+    });
+}
+
 int s2b_solve_adaptive_magnus(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfg,
                               const s2b_adaptive_config* adaptive, const double* phi, const s2b_paths* paths,
                               s2b_ensemble** out, s2b_magnus_stats* stats) {

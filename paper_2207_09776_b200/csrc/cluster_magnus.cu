@@ -435,15 +435,21 @@ bool cluster_engine_supported(int variant, int nx, int nv) {
     return smem + 1024 <= 227 * 1024;
 }
 
-void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterArgs& a) {
+bool cluster_batch_supported(int variant, int nx, int nv) {
+    return cluster_xm_supported(variant, nx, nv) || cluster_xmi_supported(variant, nx, nv);
+}
+
+void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterBatch& b) {
+    const ClusterArgs& a = b.a[0];
     if (cluster_xm_supported(variant, a.nx, a.nv)) {
-        launch_cluster_xm(ctx, variant, a);
+        launch_cluster_xm(ctx, variant, b);
         return;
     }
     if (cluster_xmi_supported(variant, a.nx, a.nv)) {
-        launch_cluster_xmi(ctx, variant, a);
+        launch_cluster_xmi(ctx, variant, b);
         return;
     }
+    if (b.n != 1) fail(S2B_ERR_RUNTIME, "cluster engine: batched launch needs the x-march engines");
     switch (variant) {
     case 1: launch_v<1>(ctx, a); break;
     case 2: launch_v<2>(ctx, a); break;

@@ -107,7 +107,7 @@ __device__ __forceinline__ unsigned long long dbits(double v) {
 }
 
 template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P>
-__global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
+__global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
     using L = XmLayout<MASK, KRX, KRV, BM, NX, RPC>;
     using RE = RowExt<MASK>;
     constexpr int TR = L::TR, TX = L::TX, TBUF = L::TBUF;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
     const int x0 = seg * LX;
     const int row0 = rank * RPC;
     const int nx = NX;
-    const int n = NX * a.nv;
+    const int n = NX * B.a[0].nv;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* T = reinterpret_cast<double*>(smem_raw); // [2][TX][TR]
@@ -185,11 +185,15 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
     uint32_t gterm = 0;
 
     while (true) {
-        if (rank == 0 && t == 0) next_path = atomicAdd(a.work, 1);
+        if (rank == 0 && t == 0) next_path = atomicAdd(B.a[0].work, 1);
         cluster_barrier();
-        const int p = *next0;
+        const int vp = *next0;
         cluster_barrier();
-        if (p >= a.M) break;
+        if (vp >= B.total) break;
+        int sidx = 0; // the session this virtual path belongs to
+        while (sidx + 1 < B.n && vp >= B.prefix[sidx + 1]) ++sidx;
+        const ClusterArgs& a = B.a[sidx];
+        const int p = vp - B.prefix[sidx];
         if (a.status[p] != 0) continue;
 
         const int par = a.par[p];
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterArgs a) {
 }
 
 template <int V, int NX, int RPC, int NT>
-void launch_xm(s2b_context* ctx, const ClusterArgs& a) {
+void launch_xm(s2b_context* ctx, const ClusterBatch& a) {
     constexpr Variant v = kVariants[V];
     auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT, kXmP>;
     const size_t smem = XmLayout<v.mask, v.rx, v.rv, v.bm, NX, RPC>::bytes();
@@ -455,7 +459,7 @@ void launch_xm(s2b_context* ctx, const ClusterArgs& a) {
     cfg.gridDim = dim3(kXmCl);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-    clusters = std::max(1, std::min(clusters, a.M));
+    clusters = std::max(1, std::min(clusters, a.total));
     cfg.gridDim = dim3(kXmCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }
@@ -473,7 +477,7 @@ bool cluster_xm_supported(int variant, int nx, int nv) {
     return nx == 256 && nv == 256;
 }
 
-void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterArgs& a) {
+void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterBatch& a) {
     switch (variant) {
     case 7: launch_xm<7, 256, 32, kXmNT>(ctx, a); break;
     case 8: launch_xm<8, 256, 32, kXmNT>(ctx, a); break;

@@ -93,7 +93,7 @@ __device__ __forceinline__ void cluster_barrier_i() {
 }
 
 template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P, int CL>
-__global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterArgs a) {
+__global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterBatch B) {
     using L = XiLayout<MASK, KRX, KRV, BM, NX, RPC>;
     using RE = RowExtI<MASK>;
     constexpr int TRI = L::TRI, TBUF = L::TBUF;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterArgs a) {
     const int seg = t / RPC;
     const int x0 = seg * LX;
     const int row0 = rank * RPC;
-    const int n = NX * a.nv;
+    const int n = NX * B.a[0].nv;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* T = reinterpret_cast<double*>(smem_raw); // [TX][TRI]
@@ -157,18 +157,22 @@ __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterArgs a) {
     int* next0 = cluster.map_shared_rank(&next_path, 0);
     double* own = T + cb + 2 * KRV + r;
     const int slot_id = static_cast<int>(blockIdx.x) / CL;
-    double* SX = a.sx + (static_cast<size_t>(slot_id) * CL + rank) * NX * RPC; // [NX][RPC]
+    double* SX = B.a[0].sx + (static_cast<size_t>(slot_id) * CL + rank) * NX * RPC; // [NX][RPC]
     double* sxp = SX + static_cast<size_t>(x0) * RPC + r;
 
     uint32_t gterm = 0;
     int ip = 0; // halo slot set holding the current term's input rows
 
     while (true) {
-        if (rank == 0 && t == 0) next_path = atomicAdd(a.work, 1);
+        if (rank == 0 && t == 0) next_path = atomicAdd(B.a[0].work, 1);
         cluster_barrier_i();
-        const int p = *next0;
+        const int vp = *next0;
         cluster_barrier_i();
-        if (p >= a.M) break;
+        if (vp >= B.total) break;
+        int sidx = 0; // the session this virtual path belongs to
+        while (sidx + 1 < B.n && vp >= B.prefix[sidx + 1]) ++sidx;
+        const ClusterArgs& a = B.a[sidx];
+        const int p = vp - B.prefix[sidx];
         if (a.status[p] != 0) continue;
 
         const int par = a.par[p];
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterArgs a) {
 }
 
 template <int V, int NX, int RPC>
-void launch_xmi(s2b_context* ctx, const ClusterArgs& a) {
+void launch_xmi(s2b_context* ctx, const ClusterBatch& a) {
     constexpr Variant v = kVariants[V];
     auto kern = cluster_xmi_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, kXiNT, kXiP, kXiCl>;
     const size_t smem = XiLayout<v.mask, v.rx, v.rv, v.bm, NX, RPC>::bytes();
@@ -463,7 +467,7 @@ void launch_xmi(s2b_context* ctx, const ClusterArgs& a) {
     cfg.gridDim = dim3(kXiCl);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-    clusters = std::max(1, std::min({clusters, a.M, a.sx_slots}));
+    clusters = std::max(1, std::min({clusters, a.total, a.a[0].sx_slots}));
     cfg.gridDim = dim3(kXiCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }
@@ -486,7 +490,7 @@ size_t cluster_xmi_scratch(int nx, int nv, int* slots) {
     return static_cast<size_t>(*slots) * static_cast<size_t>(nx) * nv;
 }
 
-void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterArgs& a) {
+void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterBatch& a) {
     switch (variant) {
     case 7: launch_xmi<7, 512, 32>(ctx, a); break;
     case 8: launch_xmi<8, 512, 32>(ctx, a); break;

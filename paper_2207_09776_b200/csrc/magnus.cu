@@ -982,42 +982,93 @@ void prepare_windows(MagnusSession* s, size_t w0, size_t w1) {
     }
 }
 
+ClusterArgs cluster_args(MagnusSession* s, int stop) {
+    ClusterArgs a{};
+    a.wt = s->op->d_wt.p;
+    a.eslot = s->op->d_eslot.p;
+    a.nx = static_cast<int>(s->op->nx);
+    a.nv = static_cast<int>(s->op->nv);
+    a.ctab = s->ctab.p;
+    a.stab = s->stab.p;
+    a.nwin = static_cast<int>(s->nwin);
+    a.win0 = s->cur_window;
+    a.win1 = stop;
+    a.dt_steps = static_cast<int>(s->plan.dt_steps);
+    a.S0 = s->S[0].p;
+    a.S1 = s->S[1].p;
+    a.win = s->iv.p;
+    a.status = s->iv.p + 4 * s->M;
+    a.par = s->iv.p + 5 * s->M;
+    a.rec_next = s->iv.p + 6 * s->M;
+    a.terms = s->terms.p;
+    a.windows = s->windows.p;
+    a.segments = s->segments.p;
+    a.rec = s->rec_ptrs.p;
+    a.rec_status = s->rec_status.p;
+    a.rec_steps = s->rec_steps.p;
+    a.R = s->R;
+    a.tol = s->cfg.expmv_tol;
+    a.cap = s->cfg.blowup_norm_cap;
+    a.M = static_cast<int>(s->M);
+    a.work = s->cnt.p + 3;
+    a.sx = s->sx.p;
+    a.sx_slots = s->sx_slots;
+    return a;
+}
+
+// Advance several sessions to their ends in batched persistent launches (a step-size sweep
+// on shared paths: run_stepsize_sweep, experiment.cpp:486-551).  Sessions on the x-march
+// engines share one launch per kMaxBatch; any other engine runs its sessions one by one.
+void sessions_run_batched(MagnusSession* const* ss, int n) {
+    int i = 0;
+    while (i < n) {
+        MagnusSession* s0 = ss[i];
+        const int v = s0->op->variant, nx = static_cast<int>(s0->op->nx), nv = static_cast<int>(s0->op->nv);
+        if (!s0->use_cluster || !cluster_batch_supported(v, nx, nv)) {
+            session_advance(s0, s0->nwin);
+            ++i;
+            continue;
+        }
+        ClusterBatch cb{};
+        cb.n = 0;
+        cb.prefix[0] = 0;
+        int j = i;
+        for (; j < n && cb.n < kMaxBatch; ++j) {
+            MagnusSession* s = ss[j];
+            if (!s->use_cluster || s->op != s0->op || static_cast<size_t>(s->cur_window) >= s->nwin) break;
+            prepare_windows(s, s->cur_window, s->nwin);
+            cb.a[cb.n] = cluster_args(s, static_cast<int>(s->nwin));
+            cb.prefix[cb.n + 1] = cb.prefix[cb.n] + static_cast<int>(s->M);
+            ++cb.n;
+        }
+        if (cb.n == 0) { // session already finished (or a different operator): plain path
+            session_advance(s0, s0->nwin);
+            ++i;
+            continue;
+        }
+        cb.total = cb.prefix[cb.n];
+        S2B_CUDA(cudaMemsetAsync(cb.a[0].work, 0, sizeof(int), s0->ctx->stream));
+        launch_cluster_magnus(s0->ctx, v, cb);
+        S2B_CUDA(cudaStreamSynchronize(s0->ctx->stream));
+        for (int q = i; q < j; ++q) {
+            ss[q]->stats.term_launches += 1;
+            ss[q]->cur_window = static_cast<int>(ss[q]->nwin);
+        }
+        i = j;
+    }
+}
+
 void session_advance(MagnusSession* s, size_t n_windows) {
     if (n_windows == 0 || static_cast<size_t>(s->cur_window) >= s->nwin) return;
     const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
     if (!s->external_prepare) prepare_windows(s, s->cur_window, stop);
     if (s->use_cluster) {
         // cluster-resident engine: every live path runs windows [cur, stop) on chip
-        ClusterArgs a{};
-        a.wt = s->op->d_wt.p;
-        a.eslot = s->op->d_eslot.p;
-        a.nx = static_cast<int>(s->op->nx);
-        a.nv = static_cast<int>(s->op->nv);
-        a.ctab = s->ctab.p;
-        a.stab = s->stab.p;
-        a.nwin = static_cast<int>(s->nwin);
-        a.win0 = s->cur_window;
-        a.win1 = stop;
-        a.dt_steps = static_cast<int>(s->plan.dt_steps);
-        a.S0 = s->S[0].p;
-        a.S1 = s->S[1].p;
-        a.win = s->iv.p;
-        a.status = s->iv.p + 4 * s->M;
-        a.par = s->iv.p + 5 * s->M;
-        a.rec_next = s->iv.p + 6 * s->M;
-        a.terms = s->terms.p;
-        a.windows = s->windows.p;
-        a.segments = s->segments.p;
-        a.rec = s->rec_ptrs.p;
-        a.rec_status = s->rec_status.p;
-        a.rec_steps = s->rec_steps.p;
-        a.R = s->R;
-        a.tol = s->cfg.expmv_tol;
-        a.cap = s->cfg.blowup_norm_cap;
-        a.M = static_cast<int>(s->M);
-        a.work = s->cnt.p + 3;
-        a.sx = s->sx.p;
-        a.sx_slots = s->sx_slots;
+        ClusterBatch cb{};
+        cb.a[0] = cluster_args(s, stop);
+        cb.n = 1;
+        cb.prefix[0] = 0;
+        cb.prefix[1] = cb.total = static_cast<int>(s->M);
         S2B_CUDA(cudaMemsetAsync(s->cnt.p + 3, 0, sizeof(int), s->ctx->stream));
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (s->timing) {
@@ -1025,7 +1076,7 @@ void session_advance(MagnusSession* s, size_t n_windows) {
             S2B_CUDA(cudaEventCreate(&e1));
             S2B_CUDA(cudaEventRecord(e0, s->ctx->stream));
         }
-        launch_cluster_magnus(s->ctx, s->op->variant, a);
+        launch_cluster_magnus(s->ctx, s->op->variant, cb);
         s->stats.term_launches += 1;
         if (s->timing) {
             S2B_CUDA(cudaEventRecord(e1, s->ctx->stream));

@@ -228,16 +228,27 @@ struct ClusterArgs {
     double* sx; // accumulator scratch of the in-place engine: [slots][CL][nx][rows] (x-major)
     int sx_slots;
 };
+// Several sessions (e.g. a step-size sweep on shared paths) in ONE persistent launch: the
+// clusters draw virtual path ids from one counter (a[0].work); ids [prefix[s], prefix[s+1])
+// belong to session s.  The x-march engines support n > 1; the row-band one n == 1.
+constexpr int kMaxBatch = 8;
+struct ClusterBatch {
+    ClusterArgs a[kMaxBatch];
+    int prefix[kMaxBatch + 1];
+    int n;
+    int total;
+};
 bool cluster_engine_supported(int variant, int nx, int nv);
-void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterArgs& a);
+bool cluster_batch_supported(int variant, int nx, int nv); // n > 1 allowed
+void launch_cluster_magnus(s2b_context* ctx, int variant, const ClusterBatch& b);
 // x-march variant of the cluster engine (cluster_xm.cu); S2B_XM=0 disables it
 bool cluster_xm_supported(int variant, int nx, int nv);
-void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterArgs& a);
+void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterBatch& b);
 // in-place x-march with the accumulator in L2 (cluster_xmi.cu): 16-CTA clusters at 512^2;
 // S2B_XMI=0 disables it.  sx_doubles: scratch the session must pass in ClusterArgs::sx.
 bool cluster_xmi_supported(int variant, int nx, int nv);
 size_t cluster_xmi_scratch(int nx, int nv, int* slots);
-void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterArgs& a);
+void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterBatch& b);
 
 } // namespace mg
 } // namespace s2b

@@ -158,6 +158,7 @@ void session_stats(const MagnusSession* s, s2b_magnus_stats* out);
 void session_set_timing(MagnusSession* s, bool on);
 s2b_ensemble* session_snapshot(MagnusSession* s);
 s2b_ensemble* session_finish(MagnusSession* s);
+void sessions_run_batched(MagnusSession* const* ss, int n);
 s2b_ensemble* solve_adaptive(s2b_context* ctx, const s2b_operator* op, const s2b_magnus_config* cfg,
                              const s2b_adaptive_config* ad, const double* phi, const s2b_paths* paths,
                              s2b_magnus_stats* stats);
