@@ -1036,7 +1036,7 @@ void sessions_run_batched(MagnusSession* const* ss, int n) {
         for (; j < n && cb.n < kMaxBatch; ++j) {
             MagnusSession* s = ss[j];
             if (!s->use_cluster || s->op != s0->op || static_cast<size_t>(s->cur_window) >= s->nwin) break;
-            prepare_windows(s, s->cur_window, s->nwin);
+            if (!s->external_prepare) prepare_windows(s, s->cur_window, s->nwin);
             cb.a[cb.n] = cluster_args(s, static_cast<int>(s->nwin));
             cb.prefix[cb.n + 1] = cb.prefix[cb.n] + static_cast<int>(s->M);
             ++cb.n;
@@ -1454,10 +1454,14 @@ s2b_ensemble* solve_adaptive(s2b_context* ctx, const s2b_operator* op, const s2b
     c1.blowup_norm_cap = HUGE_VAL;
     c1.record_times = nullptr;
     c1.n_record = 0;
+    // s runs the order-3 attempts, s2 the order-2 ones: one batched launch carries both
     MagnusSession* s = session_create(ctx, op, &c1, phi, paths);
+    MagnusSession* s2 = nullptr;
     auto* e = new s2b_ensemble();
     try {
+        s2 = session_create(ctx, op, &c1, phi, paths);
         s->external_prepare = true;
+        s2->external_prepare = true;
         e->ctx = ctx;
         e->R = R;
         e->M = M;
@@ -1512,23 +1516,22 @@ s2b_ensemble* solve_adaptive(s2b_context* ctx, const s2b_operator* op, const s2b
         const unsigned gm = static_cast<unsigned>((M + 255) / 256);
         OpView ov{op->d_pair_begin.p, op->d_pair_slot.p, op->d_w.p, static_cast<int>(op->nx),
                   static_cast<int>(op->nv), op->compressed};
-        auto norms = [&]() {
+        auto norms = [&](MagnusSession* q) {
             for (size_t m0 = 0; m0 < M; m0 += (1u << 30)) {
                 const size_t mc = std::min<size_t>(M - m0, 1u << 30);
                 norm_kernel<<<static_cast<unsigned>(mc), 256, 0, ctx->stream>>>(
-                    ov, s->bits.p, s->nbits, op->rx, s->ctab.p + m0 * 6, 1, 0, 1, cfg->expmv_theta,
-                    s->stab.p + m0, nullptr);
+                    ov, q->bits.p, q->nbits, op->rx, q->ctab.p + m0 * 6, 1, 0, 1, cfg->expmv_theta,
+                    q->stab.p + m0, nullptr);
                 S2B_LAUNCHED(ctx);
             }
         };
-        auto run = [&]() {
-            S2B_CUDA(cudaMemcpyAsync(s->S[0].p, U.p, U.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
-            ad_reset_kernel<<<gm, 256, 0, ctx->stream>>>(s->iv.p, M, flags.p);
+        auto load = [&](MagnusSession* q) {
+            S2B_CUDA(cudaMemcpyAsync(q->S[0].p, U.p, U.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
+            ad_reset_kernel<<<gm, 256, 0, ctx->stream>>>(q->iv.p, M, flags.p);
             S2B_LAUNCHED(ctx);
-            S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), ctx->stream));
-            s->cur = 0;
-            s->cur_window = 0;
-            session_advance(s, 1);
+            S2B_CUDA(cudaMemsetAsync(q->cnt.p, 0, q->cnt.bytes(), ctx->stream));
+            q->cur = 0;
+            q->cur_window = 0;
         };
         const dim3 gg(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64)), static_cast<unsigned>(std::min<size_t>(M, 65535)));
         int h_live = 0;
@@ -1539,30 +1542,41 @@ s2b_ensemble* solve_adaptive(s2b_context* ctx, const s2b_operator* op, const s2b
             S2B_CUDA(cudaMemcpyAsync(&h_live, live.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
             S2B_CUDA(cudaStreamSynchronize(ctx->stream));
             if (h_live == 0) break;
-            norms(); // order 3
-            run();
+            S2B_CUDA(cudaMemcpyAsync(s2->ctab.p, ctab2.p, M * 6 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+            norms(s);  // order 3
+            norms(s2); // order 2
+            load(s);
+            load(s2);
+            MagnusSession* both[2] = {s, s2};
+            sessions_run_batched(both, 2);
             ad_save_status_kernel<<<gm, 256, 0, ctx->stream>>>(s->iv.p + 4 * M, st3.p, M);
             S2B_LAUNCHED(ctx);
             gather_kernel<<<gg, 256, 0, ctx->stream>>>(s->iv.p + 5 * M, s->S[0].p, s->S[1].p, A.p, n, M);
             S2B_LAUNCHED(ctx);
-            S2B_CUDA(cudaMemcpyAsync(s->ctab.p, ctab2.p, M * 6 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-            norms(); // order 2
-            run();
             ad_gap_kernel<<<static_cast<unsigned>(std::min<size_t>(M, 65535)), 256, 0, ctx->stream>>>(
-                a, A.p, s->S[0].p, s->S[1].p, s->iv.p + 5 * M, st3.p, s->iv.p + 4 * M);
+                a, A.p, s2->S[0].p, s2->S[1].p, s2->iv.p + 5 * M, st3.p, s2->iv.p + 4 * M);
             S2B_LAUNCHED(ctx);
             ad_commit_kernel<<<gg, 256, 0, ctx->stream>>>(a, A.p, U.p, drp.p, e->status.p);
             S2B_LAUNCHED(ctx);
         }
-        if (stats) session_stats(s, stats);
+        if (stats) {
+            session_stats(s, stats); // counters of the order-3 attempts plus the order-2 ones
+            s2b_magnus_stats st2{};
+            session_stats(s2, &st2);
+            stats->path_terms += st2.path_terms;
+            stats->path_segments += st2.path_segments;
+            stats->term_launches += st2.term_launches;
+        }
         e->states.push_back(std::move(U));
         S2B_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
         delete e;
         session_destroy(s);
+        session_destroy(s2);
         throw;
     }
     session_destroy(s);
+    session_destroy(s2);
     return e;
 }
 
