@@ -35,7 +35,8 @@ MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 ENGINES = {
     3: {"name": "cluster-xmi", "kernel": "cluster_xmi_kernel", "profile": "xmi_kernel_ncu.json",
         "note": "cluster-resident in-place x-march (16-CTA clusters, accumulator in L2): achieved is the "
-                "streaming-equivalent rate, traffic the real DRAM bytes; bound by the fp64 pipe"},
+                "streaming-equivalent rate, traffic the real DRAM bytes; bound by the fp64 pipe; by default "
+                "20% of the paths run on the streaming engine on the idle SMs (S2B_HYBRID)"},
     0: {"name": "stream", "kernel": "term_tma_kernel", "profile": "term_kernel_ncu.json",
         "note": "streaming pass engine: term and accumulator round-trip HBM every Taylor term"},
     1: {"name": "cluster-band", "kernel": "cluster_magnus_kernel", "profile": "cluster_kernel_ncu.json",
@@ -44,7 +45,8 @@ ENGINES = {
     2: {"name": "cluster-xm", "kernel": "cluster_xm_kernel", "profile": "xm_kernel_ncu.json",
         "note": "cluster-resident x-march: the path stays in shared memory for the window; achieved is "
                 "the streaming-equivalent rate (can exceed HBM peak), traffic the real DRAM bytes; the "
-                "binding limit is the fp64 pipe (compute_roofline)"},
+                "binding limit is the fp64 pipe (compute_roofline); by default 12% of the paths run on "
+                "the streaming engine concurrently, on the SMs the 8-CTA clusters leave idle (S2B_HYBRID)"},
 }
 
 
@@ -282,10 +284,16 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", engine["profile"])) as f:
             prof = json.load(f)
+        hyb = st1.get("hybrid_paths", 0) or 0  # paths on the streaming engine beside the clusters
+        stream_prof = {}
+        if hyb:
+            with open(os.path.join(ROOT, "profiles", ENGINES[0]["profile"])) as f:
+                stream_prof = json.load(f)
         if engine["name"] == "stream" and prof.get("dram_bytes_per_path_term") is not None:
             traffic = prof["dram_bytes_per_path_term"] * terms / max(tk_launches, 1)
         elif prof.get("dram_bytes_per_path_window") is not None:
-            traffic = prof["dram_bytes_per_path_window"] * M * args.steps / max(tk_launches, 1)
+            traffic = (prof["dram_bytes_per_path_window"] * (M - hyb) * args.steps
+                       + stream_prof.get("dram_bytes_per_path_term", 0.0) * terms * hyb / M) / max(tk_launches, 1)
     except Exception:
         pass
     # the on-chip engines are bound by the fp64 pipe, not HBM: report that ceiling beside it
@@ -357,7 +365,9 @@ def run_ours(args):
                      "kernel": engine["kernel"], "engine": engine["name"], "launches": tk_launches,
                      "kernel_ms": tk_ms,
                      "bytes_model": "32 B per path*gridpoint*term (24 B for the k=1 term of a segment)",
-                     "traffic_source": f"profiles/{engine['profile']} (ncu dram__bytes, scaled per launch)",
+                     "traffic_source": f"profiles/{engine['profile']} (ncu dram__bytes, scaled per launch)"
+                                       + (" + streaming-engine bytes of the hybrid slice" if st1.get("hybrid_paths") else ""),
+                     "hybrid_paths": st1.get("hybrid_paths", 0),
                      "note": engine["note"]},
         "compute_roofline": compute,
         "gpu_launches": launches,

@@ -119,6 +119,7 @@ typedef struct {
     double gridpoints;     /* nx*nv */
     int64_t path_segments; /* sum over paths of Taylor segments (one k=1 term each) */
     int32_t engine;        /* 0 streaming passes, 1 cluster row-band, 2 cluster x-march, 3 in-place x-march */
+    int64_t hybrid_paths;  /* paths the last cluster launch left to the streaming engine (idle SMs) */
 } s2b_magnus_stats;
 
 const char *s2b_last_error(void);

@@ -52,7 +52,7 @@ class MagnusStats(C.Structure):
     _fields_ = [("passes", C.c_int64), ("path_terms", C.c_int64), ("path_windows", C.c_int64),
                 ("term_launches", C.c_int64), ("term_kernel_ms", C.c_double),
                 ("gridpoints", C.c_double), ("path_segments", C.c_int64),
-                ("engine", C.c_int32)]
+                ("engine", C.c_int32), ("hybrid_paths", C.c_int64)]
 
 
 # Exported symbols with their ctypes signatures (restype int unless noted).

@@ -182,6 +182,7 @@ struct Ctl {
     int nwin;
     int dt_steps;
     int win_stop; // pause when reaching this window
+    int p_lo;     // paths below this index belong to another engine (hybrid runs)
     double tol;
     double cap;
     size_t M;
@@ -222,7 +223,7 @@ __device__ bool enter_window(const Ctl& c, int p, int w, int par) {
 
 __global__ void init_kernel(Ctl c, int first_window) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= static_cast<int>(c.M)) return;
+    if (p >= static_cast<int>(c.M) || p < c.p_lo) return;
     if (c.status[p] == 2) return; // blown paths stay blown
     c.tn[p] = 0;
     c.sn[p] = 0;
@@ -707,6 +708,9 @@ struct MagnusSession {
     DevBuf<long long> terms, windows, segments;
     DevBuf<double> sx; // accumulator scratch of the in-place cluster engine
     int sx_slots = 0;
+    DevBuf<int> cl_work;            // path counter of the cluster kernel in hybrid runs
+    DevBuf<double> mom_part, mom;   // moments: chunk partials, result
+    cudaStream_t stream2 = nullptr; // streaming passes beside the cluster kernel (hybrid)
     DevBuf<unsigned long long> tn, sn;
     DevBuf<int> act[2];
     DevBuf<int> cnt;
@@ -982,6 +986,52 @@ void prepare_windows(MagnusSession* s, size_t w0, size_t w1) {
     }
 }
 
+// The streaming pass engine over paths [p_lo, M): one Taylor term of every live path per
+// pass, per-path state machines in control_kernel (see the file header).
+void stream_loop(MagnusSession* s, int stop, int p_lo) {
+    {
+        // (re)activate every live path at the current window boundary; window 0 also
+        // initialises the per-path state (parity, records, counters)
+        Ctl c = s->ctl(stop);
+        c.p_lo = p_lo;
+        S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), s->ctx->stream));
+        init_kernel<<<static_cast<unsigned>((s->M + 127) / 128), 128, 0, s->ctx->stream>>>(c, s->cur_window);
+        S2B_LAUNCHED(s->ctx);
+        run_records(*s);
+        swap_lists(*s);
+    }
+    int chunk = 4;
+    while (true) {
+        S2B_CUDA(cudaMemcpyAsync(s->h_cnt, s->cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s->ctx->stream));
+        S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        if (s->timing) collect_timing(*s);
+        if (s->h_cnt[0] == 0) break;
+        for (int q = 0; q < chunk; ++q) {
+            launch_term(*s);
+            Ctl c = s->ctl(stop);
+            control_kernel<<<static_cast<unsigned>((s->M + 255) / 256), 256, 0, s->ctx->stream>>>(c);
+            S2B_LAUNCHED(s->ctx);
+            run_records(*s);
+            swap_lists(*s);
+            s->stats.passes += 1;
+        }
+        chunk = std::min(chunk * 2, 64);
+    }
+}
+
+// Hybrid split: the clusters of the x-march engines pack 15 x 8 (256^2) or 7 x 16 (512^2) per
+// B200, leaving 28 / 36 of the 148 SMs idle; the streaming engine runs a slice of the paths
+// concurrently on those SMs.  Measured best slices: 0.11-0.14 at 256^2 (+12%), 0.2 at 512^2
+// (+17%).  S2B_HYBRID overrides the slice (0 disables).
+double hybrid_fraction(const MagnusSession* s) {
+    const char* e = std::getenv("S2B_HYBRID");
+    if (e) return std::atof(e);
+    const int v = s->op->variant, nx = static_cast<int>(s->op->nx), nv = static_cast<int>(s->op->nv);
+    if (cluster_xm_supported(v, nx, nv)) return 0.12;
+    if (cluster_xmi_supported(v, nx, nv)) return 0.20;
+    return 0.0;
+}
+
 ClusterArgs cluster_args(MagnusSession* s, int stop) {
     ClusterArgs a{};
     a.wt = s->op->d_wt.p;
@@ -1062,6 +1112,68 @@ void session_advance(MagnusSession* s, size_t n_windows) {
     if (n_windows == 0 || static_cast<size_t>(s->cur_window) >= s->nwin) return;
     const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
     if (!s->external_prepare) prepare_windows(s, s->cur_window, stop);
+    const double hf = s->use_cluster ? hybrid_fraction(s) : 0.0;
+    const int Ms = (hf > 0.0 && hf < 1.0 && s->M >= 64 &&
+                    cluster_batch_supported(s->op->variant, static_cast<int>(s->op->nx), static_cast<int>(s->op->nv)))
+                       ? static_cast<int>(static_cast<double>(s->M) * hf) : 0;
+    if (s->use_cluster && Ms > 0) {
+        // hybrid: paths [0, M1) on the cluster engine (stream 1), [M1, M) on the streaming
+        // engine concurrently (stream 2, on the SMs the clusters leave idle)
+        const int M1 = static_cast<int>(s->M) - Ms;
+        s->stats.hybrid_paths = Ms;
+        if (!s->stream2) S2B_CUDA(cudaStreamCreateWithFlags(&s->stream2, cudaStreamNonBlocking));
+        if (!s->cl_work.p) s->cl_work.alloc(1);
+        cudaStream_t st1 = s->ctx->stream;
+        ClusterBatch cb{};
+        cb.a[0] = cluster_args(s, stop); // a.M stays the record-status stride; total bounds the run
+        cb.a[0].work = s->cl_work.p;
+        cb.n = 1;
+        cb.prefix[0] = 0;
+        cb.prefix[1] = cb.total = M1;
+        S2B_CUDA(cudaMemsetAsync(s->cl_work.p, 0, sizeof(int), st1));
+        cudaEvent_t prep, done, e0 = nullptr, e1 = nullptr;
+        S2B_CUDA(cudaEventCreateWithFlags(&prep, cudaEventDisableTiming));
+        S2B_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        S2B_CUDA(cudaEventRecord(prep, st1));
+        if (s->timing) {
+            S2B_CUDA(cudaEventCreate(&e0));
+            S2B_CUDA(cudaEventCreate(&e1));
+            S2B_CUDA(cudaEventRecord(e0, st1));
+        }
+        launch_cluster_magnus(s->ctx, s->op->variant, cb);
+        s->stats.term_launches += 1;
+        // the streaming passes: the same session state, a context view on stream 2
+        s2b_context c2 = *s->ctx;
+        c2.stream = s->stream2;
+        s2b_context* c1 = s->ctx;
+        const bool tim = s->timing;
+        S2B_CUDA(cudaStreamWaitEvent(s->stream2, prep, 0));
+        s->ctx = &c2;
+        s->timing = false;
+        try {
+            stream_loop(s, stop, M1);
+        } catch (...) {
+            s->ctx = c1;
+            s->timing = tim;
+            throw;
+        }
+        s->ctx = c1;
+        s->timing = tim;
+        c1->launches = c2.launches;
+        S2B_CUDA(cudaEventRecord(done, s->stream2));
+        S2B_CUDA(cudaStreamWaitEvent(st1, done, 0));
+        if (s->timing) {
+            S2B_CUDA(cudaEventRecord(e1, st1));
+            s->ev.push_back(e0);
+            s->ev.push_back(e1);
+        }
+        S2B_CUDA(cudaStreamSynchronize(st1));
+        cudaEventDestroy(prep);
+        cudaEventDestroy(done);
+        if (s->timing) collect_timing(*s);
+        s->cur_window = stop;
+        return;
+    }
     if (s->use_cluster) {
         // cluster-resident engine: every live path runs windows [cur, stop) on chip
         ClusterBatch cb{};
@@ -1088,33 +1200,7 @@ void session_advance(MagnusSession* s, size_t n_windows) {
         s->cur_window = stop;
         return;
     }
-    {
-        // (re)activate every live path at the current window boundary; window 0 also
-        // initialises the per-path state (parity, records, counters)
-        Ctl c = s->ctl(stop);
-        S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), s->ctx->stream));
-        init_kernel<<<static_cast<unsigned>((s->M + 127) / 128), 128, 0, s->ctx->stream>>>(c, s->cur_window);
-        S2B_LAUNCHED(s->ctx);
-        run_records(*s);
-        swap_lists(*s);
-    }
-    int chunk = 4;
-    while (true) {
-        S2B_CUDA(cudaMemcpyAsync(s->h_cnt, s->cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s->ctx->stream));
-        S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
-        if (s->timing) collect_timing(*s);
-        if (s->h_cnt[0] == 0) break;
-        for (int q = 0; q < chunk; ++q) {
-            launch_term(*s);
-            Ctl c = s->ctl(stop);
-            control_kernel<<<static_cast<unsigned>((s->M + 255) / 256), 256, 0, s->ctx->stream>>>(c);
-            S2B_LAUNCHED(s->ctx);
-            run_records(*s);
-            swap_lists(*s);
-            s->stats.passes += 1;
-        }
-        chunk = std::min(chunk * 2, 64);
-    }
+    stream_loop(s, stop, 0);
     s->cur_window = stop;
 }
 
@@ -1216,29 +1302,49 @@ s2b_ensemble* session_finish(MagnusSession* s) {
 namespace {
 // sum_m u_m and sum_m u_m^2 over live (not blown) paths, ascending m, reading each path's
 // current buffer; the statistic the multi-GPU path all-reduces.
+// Two levels, deterministic: chunks of kMomChunk paths per block (ascending m inside a chunk),
+// then the chunk partials summed in ascending chunk order.  One thread per point would walk
+// all M paths serially (latency-bound, and page-hopping 512 KB per step).
+constexpr int kMomChunk = 64;
 __global__ void session_moments_kernel(const int* __restrict__ par, const int* __restrict__ status,
                                        const double* __restrict__ S0, const double* __restrict__ S1,
-                                       size_t M, size_t n, double* __restrict__ mom) {
+                                       size_t M, size_t n, double* __restrict__ part) {
     const size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (r >= n) return;
+    const size_t m0 = static_cast<size_t>(blockIdx.y) * kMomChunk;
+    const size_t m1 = m0 + kMomChunk < M ? m0 + kMomChunk : M;
     double s1 = 0.0, s2 = 0.0;
-    for (size_t m = 0; m < M; ++m) {
-        if (status[m] == 2) continue;
+#pragma unroll 8
+    for (size_t m = m0; m < m1; ++m) {
         const double u = (par[m] ? S1 : S0)[m * n + r];
+        if (status[m] == 2) continue;
         s1 += u;
         s2 += u * u;
     }
-    mom[r] = s1;
-    mom[n + r] = s2;
+    part[blockIdx.y * 2 * n + r] = s1;
+    part[blockIdx.y * 2 * n + n + r] = s2;
+}
+__global__ void moments_finish_kernel(const double* __restrict__ part, size_t nch, size_t n, double* __restrict__ mom) {
+    const size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (r >= 2 * n) return;
+    double acc = 0.0;
+    for (size_t c = 0; c < nch; ++c) acc += part[c * 2 * n + r];
+    mom[r] = acc;
 }
 } // namespace
 
 void session_moments(MagnusSession* s, double* host_out, double* live_out) {
-    DevBuf<double> mom(2 * s->n);
-    session_moments_kernel<<<static_cast<unsigned>((s->n + 127) / 128), 128, 0, s->ctx->stream>>>(
-        s->iv.p + 5 * s->M, s->iv.p + 4 * s->M, s->S[0].p, s->S[1].p, s->M, s->n, mom.p);
+    const size_t nch = (s->M + kMomChunk - 1) / kMomChunk;
+    if (s->mom_part.n < nch * 2 * s->n) s->mom_part.alloc(nch * 2 * s->n);
+    if (s->mom.n < 2 * s->n) s->mom.alloc(2 * s->n);
+    dim3 g(static_cast<unsigned>((s->n + 255) / 256), static_cast<unsigned>(nch));
+    session_moments_kernel<<<g, 256, 0, s->ctx->stream>>>(s->iv.p + 5 * s->M, s->iv.p + 4 * s->M, s->S[0].p,
+                                                          s->S[1].p, s->M, s->n, s->mom_part.p);
     S2B_LAUNCHED(s->ctx);
-    S2B_CUDA(cudaMemcpyAsync(host_out, mom.p, mom.bytes(), cudaMemcpyDeviceToHost, s->ctx->stream));
+    moments_finish_kernel<<<static_cast<unsigned>((2 * s->n + 255) / 256), 256, 0, s->ctx->stream>>>(
+        s->mom_part.p, nch, s->n, s->mom.p);
+    S2B_LAUNCHED(s->ctx);
+    S2B_CUDA(cudaMemcpyAsync(host_out, s->mom.p, 2 * s->n * sizeof(double), cudaMemcpyDeviceToHost, s->ctx->stream));
     std::vector<int> st(s->M);
     S2B_CUDA(cudaMemcpyAsync(st.data(), s->iv.p + 4 * s->M, s->M * sizeof(int), cudaMemcpyDeviceToHost, s->ctx->stream));
     S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
@@ -1251,6 +1357,7 @@ void session_moments(MagnusSession* s, double* host_out, double* live_out) {
 
 void session_destroy(MagnusSession* s) {
     if (!s) return;
+    if (s->stream2) cudaStreamDestroy(s->stream2);
     for (auto ev : s->ev) cudaEventDestroy(ev);
     if (s->h_cnt) cudaFreeHost(s->h_cnt);
     delete s;

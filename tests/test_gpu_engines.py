@@ -146,3 +146,22 @@ def test_engines_blowup_exits_512(ref, s2b, ctx, engine512):
     ens, _, _, _ = gpu_magnus(s2b, ctx, "langevin-constant", d, 3, values, dt_leb, T, dt, seed=5,
                               blowup_norm_cap=1e-3)
     assert np.array_equal(ens[-1].status, wst[-1]) and ens[-1].blowup_count() == M
+
+
+@pytest.mark.parametrize("d", [256, 512])
+def test_hybrid_split_bitwise(s2b, ctx, monkeypatch, d):
+    """S2B_HYBRID: a slice of the paths runs on the streaming engine beside the cluster kernel
+    (on the SMs the clusters leave idle); every path's result is unchanged."""
+    T, dt, dt_leb, M = 0.02, 0.01, 1e-3, 96
+    g = s2b.GridSpec.square(d)
+    op = s2b.Operator.from_family(g, "langevin-constant", order=3, ctx=ctx)
+    paths = s2b.BrownianPaths.philox(T, dt_leb, M, seed=23, ctx=ctx)
+    phi = s2b.gaussian_datum(g)
+    cfg = s2b.MagnusConfig(order=3, dt=dt, record_times=[0.01])
+    monkeypatch.setenv("S2B_HYBRID", "0")
+    want = s2b.solve_iterated_magnus(cfg, op, phi, paths, T, g)
+    monkeypatch.setenv("S2B_HYBRID", "0.3")
+    got = s2b.solve_iterated_magnus(cfg, op, phi, paths, T, g)
+    for w, e in zip(want, got):
+        assert np.array_equal(w.status, e.status)
+        assert np.array_equal(w.states(), e.states(), equal_nan=True)
