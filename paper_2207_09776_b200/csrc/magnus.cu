@@ -1155,6 +1155,10 @@ void session_advance(MagnusSession* s, size_t n_windows) {
         } catch (...) {
             s->ctx = c1;
             s->timing = tim;
+            cudaStreamSynchronize(st1); // the cluster kernel still owns the session buffers
+            cudaStreamSynchronize(s->stream2);
+            cudaEventDestroy(prep);
+            cudaEventDestroy(done);
             throw;
         }
         s->ctx = c1;
