@@ -10,6 +10,7 @@
 // dW is the difference of prefix values (euler.cpp:156), so E-M and Magnus consume
 // the same paths.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -176,8 +177,10 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
             }
             DevBuf<double> dphi(n);
             S2B_CUDA(cudaMemcpyAsync(dphi.p, phi, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            bool nz = true; // no -0.0 in the datum (see em_cluster.cu)
+            for (size_t i = 0; i < n && nz; ++i) nz = !(phi[i] == 0.0 && std::signbit(phi[i]));
             em_cluster_solve(ctx, f, cfg->dt, dphi.p, paths, static_cast<int>(plan.dt_steps),
-                             static_cast<int>(nsteps), rec_k, rp.data(), e->status.p);
+                             static_cast<int>(nsteps), rec_k, rp.data(), e->status.p, nz);
             return e;
         }
         DevBuf<double> U[2] = {DevBuf<double>(M * n), DevBuf<double>(M * n)};

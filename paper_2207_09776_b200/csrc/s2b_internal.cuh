@@ -173,7 +173,7 @@ s2b_fields* make_fields(s2b_context* ctx, const s2b_grid* grid, const double* co
 bool em_cluster_supported(const s2b_fields* f);
 void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const double* d_phi,
                       const s2b_paths* paths, int step_leb, int nsteps, const std::vector<int>& rec_k,
-                      double* const* d_rec, uint8_t* d_status);
+                      double* const* d_rec, uint8_t* d_status, bool no_neg_zero);
 s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler_config* cfg,
                           const double* phi, const s2b_paths* paths);
 s2b_ensemble* exact_reference(s2b_context* ctx, const s2b_grid* grid, double t, double a, double sigma,

@@ -165,3 +165,23 @@ def test_hybrid_split_bitwise(s2b, ctx, monkeypatch, d):
     for w, e in zip(want, got):
         assert np.array_equal(w.status, e.status)
         assert np.array_equal(w.states(), e.states(), equal_nan=True)
+
+
+@pytest.mark.parametrize("em_engine", ["em-cluster"], indirect=True)
+@pytest.mark.parametrize("negzero", [False, True])
+def test_euler_cluster_bit_patterns(ref, s2b, ctx, em_engine, negzero):
+    """Bit patterns, not just values, including the sign of zeros: a datum without -0.0 takes
+    the shortened drift / noise folds (em_cluster.cu, NZ), one with -0.0 the literal ones."""
+    d, T, dt_leb, M, seed = 256, 0.005, 1e-4, 2, 77
+    ops = ref.Ops("langevin-constant", d, order=1)
+    phi = ops.datum().copy()
+    phi[::7] = 0.0  # zero rows of points whose stencil sums vanish
+    if negzero:
+        phi[::11] = -0.0
+    values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
+    want, wst, _ = ops.solve_euler(values, dt_leb, T, dt_leb, seed=seed, phi=phi)
+    g = s2b.GridSpec.square(d)
+    f = s2b.Fields.from_family(g, "langevin-constant", ctx=ctx)
+    paths = s2b.BrownianPaths.from_values(values, dt_leb, seed=seed, ctx=ctx)
+    got = s2b.solve_euler(s2b.EulerConfig(dt=dt_leb), f, g, phi, paths, T)[-1].states()
+    assert np.array_equal(got.view(np.uint64), want[-1].view(np.uint64))
