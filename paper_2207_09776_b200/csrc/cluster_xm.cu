@@ -106,7 +106,7 @@ __device__ __forceinline__ unsigned long long dbits(double v) {
     return static_cast<unsigned long long>(__double_as_longlong(v));
 }
 
-template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P, bool NZ>
 __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
     using L = XmLayout<MASK, KRX, KRV, BM, NX, RPC>;
     using RE = RowExt<MASK>;
@@ -346,7 +346,11 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
                                                 }
                                             }
                                             const int col = g + q + dx;
-                                            acc[q] += wv * win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))];
+                                            const double pr = wv * win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))];
+                                            // NZ: start at the first product, not 0.0 + it (only the
+                                            // sign of an all-zero sum differs; the accumulator and
+                                            // hence every state bit cannot, see DESIGN "Parity")
+                                            acc[q] = (NZ && e == 0) ? pr : acc[q] + pr;
                                         }
                                     }
                                 }
@@ -439,10 +443,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
     }
 }
 
-template <int V, int NX, int RPC, int NT>
+template <int V, int NX, int RPC, int NT, bool NZ>
 void launch_xm(s2b_context* ctx, const ClusterBatch& a) {
     constexpr Variant v = kVariants[V];
-    auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT, kXmP>;
+    auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT, kXmP, NZ>;
     const size_t smem = XmLayout<v.mask, v.rx, v.rv, v.bm, NX, RPC>::bytes();
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
@@ -478,10 +482,15 @@ bool cluster_xm_supported(int variant, int nx, int nv) {
 }
 
 void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterBatch& a) {
-    switch (variant) {
-    case 7: launch_xm<7, 256, 32, kXmNT>(ctx, a); break;
-    case 8: launch_xm<8, 256, 32, kXmNT>(ctx, a); break;
-    case 9: launch_xm<9, 256, 32, kXmNT>(ctx, a); break;
+    bool nz = true;
+    for (int i = 0; i < a.n; ++i) nz = nz && a.a[i].nz;
+    switch (variant * 2 + (nz ? 1 : 0)) {
+    case 14: launch_xm<7, 256, 32, kXmNT, false>(ctx, a); break;
+    case 15: launch_xm<7, 256, 32, kXmNT, true>(ctx, a); break;
+    case 16: launch_xm<8, 256, 32, kXmNT, false>(ctx, a); break;
+    case 17: launch_xm<8, 256, 32, kXmNT, true>(ctx, a); break;
+    case 18: launch_xm<9, 256, 32, kXmNT, false>(ctx, a); break;
+    case 19: launch_xm<9, 256, 32, kXmNT, true>(ctx, a); break;
     default: fail(S2B_ERR_RUNTIME, "x-march cluster engine: unsupported variant");
     }
     S2B_LAUNCHED(ctx);

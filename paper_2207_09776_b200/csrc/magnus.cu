@@ -710,6 +710,7 @@ struct MagnusSession {
     int sx_slots = 0;
     DevBuf<int> cl_work;            // path counter of the cluster kernel in hybrid runs
     DevBuf<double> mom_part, mom;   // moments: chunk partials, result
+    bool nz = false;                // the datum holds no -0.0
     cudaStream_t stream2 = nullptr; // streaming passes beside the cluster kernel (hybrid)
     DevBuf<unsigned long long> tn, sn;
     DevBuf<int> act[2];
@@ -901,6 +902,8 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
                 s->sx.alloc(cluster_xmi_scratch(static_cast<int>(op->nx), static_cast<int>(op->nv), &s->sx_slots));
         }
         s->phi.assign(phi, phi + n);
+        s->nz = true;
+        for (size_t i = 0; i < n && s->nz; ++i) s->nz = !(phi[i] == 0.0 && std::signbit(phi[i]));
         const size_t M = s->M;
         for (int b = 0; b < 2; ++b) {
             s->T[b].alloc(M * n);
@@ -1063,6 +1066,7 @@ ClusterArgs cluster_args(MagnusSession* s, int stop) {
     a.work = s->cnt.p + 3;
     a.sx = s->sx.p;
     a.sx_slots = s->sx_slots;
+    a.nz = s->nz ? 1 : 0;
     return a;
 }
 

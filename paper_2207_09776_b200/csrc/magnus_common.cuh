@@ -227,6 +227,7 @@ struct ClusterArgs {
     int* work; // path counter (zeroed before the launch)
     double* sx; // accumulator scratch of the in-place engine: [slots][CL][nx][rows] (x-major)
     int sx_slots;
+    int nz; // the datum holds no -0.0 (shortened stencil folds are then bit-identical)
 };
 // Several sessions (e.g. a step-size sweep on shared paths) in ONE persistent launch: the
 // clusters draw virtual path ids from one counter (a[0].work); ids [prefix[s], prefix[s+1])

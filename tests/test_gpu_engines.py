@@ -185,3 +185,21 @@ def test_euler_cluster_bit_patterns(ref, s2b, ctx, em_engine, negzero):
     paths = s2b.BrownianPaths.from_values(values, dt_leb, seed=seed, ctx=ctx)
     got = s2b.solve_euler(s2b.EulerConfig(dt=dt_leb), f, g, phi, paths, T)[-1].states()
     assert np.array_equal(got.view(np.uint64), want[-1].view(np.uint64))
+
+
+@pytest.mark.parametrize("negzero", [False, True])
+def test_xm_bit_patterns(ref, s2b, ctx, negzero):
+    """x-march Magnus: bit patterns (incl. zero signs) equal the reference's, with the
+    shortened stencil fold (datum without -0.0) and the literal one (datum with -0.0)."""
+    d, T, dt, dt_leb, M, seed = 256, 0.02, 0.01, 1e-3, 2, 91
+    ops = ref.Ops("langevin-constant", d, order=3)
+    phi = ops.datum().copy()
+    phi[::5] = 0.0
+    if negzero:
+        phi[::13] = -0.0
+    values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
+    want, wst, _ = ops.solve_magnus(values, dt_leb, T, dt, seed=seed, phi=phi)
+    ens, _, _, stats = gpu_magnus(s2b, ctx, "langevin-constant", d, 3, values, dt_leb, T, dt, seed=seed, phi=phi)
+    assert stats["engine"] == 2
+    assert np.array_equal(ens[-1].status, wst[-1])
+    assert np.array_equal(ens[-1].states().view(np.uint64), want[-1].view(np.uint64))
