@@ -34,7 +34,6 @@ namespace mg {
 
 namespace {
 
-constexpr int kXmCl = 8;
 #ifndef S2B_XM_P
 #define S2B_XM_P 4
 #endif
@@ -81,7 +80,6 @@ struct XmLayout {
         return 8 * (2 * static_cast<size_t>(TBUF) + static_cast<size_t>(NX) * RPC + 4 * static_cast<size_t>(NBB) * RPC);
     }
     static_assert(SCR <= TBUF, "transpose scratch must fit one term buffer");
-    static_assert(RPC * NYE <= TBUF, "Y fold scratch must fit one term buffer");
 };
 
 // max over a warp of non-negative doubles (or +NaN), as their bit patterns
@@ -106,8 +104,9 @@ __device__ __forceinline__ unsigned long long dbits(double v) {
     return static_cast<unsigned long long>(__double_as_longlong(v));
 }
 
-template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P, bool NZ>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P, bool NZ, int CL>
 __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
+    constexpr int kXmCl = CL; // CTAs per path
     using L = XmLayout<MASK, KRX, KRV, BM, NX, RPC>;
     using RE = RowExt<MASK>;
     constexpr int TR = L::TR, TX = L::TX, TBUF = L::TBUF;
@@ -140,6 +139,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
     double* S = T + 2 * TBUF;                        // [NX][RPC]
     double* bY = S + NX * RPC;                       // [4][NBB][RPC] boundary-class Y
     double* scr = T + TBUF;                          // scratch aliasing T[1]
+    // window-fold scratch: T[1], or both term buffers for a one-CTA path (no neighbour can
+    // push into T[0] then; re-zeroed after use)
+    double* yscr = CL == 1 ? T : scr;
+    static_assert(RPC * L::NYE <= (CL == 1 ? 2 : 1) * TBUF, "Y fold scratch must fit the term buffers");
     __shared__ unsigned long long slots[2][kXmCl][2]; // CTA maxima of every rank, per parity
     __shared__ unsigned long long red[NW][2];
     __shared__ double c[6];
@@ -240,12 +243,12 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
                     const double cs = c[sl];
                     if (cs != 0.0) y += cs * __ldg(wr + k);
                 }
-                scr[q] = y;
+                yscr[q] = y;
             }
             __syncthreads();
             double y[NBM]; // interior (class 2) Y of row r
 #pragma unroll
-            for (int e = 0; e < NBM; ++e) y[e] = scr[r * NYE + 2 * NBM + e];
+            for (int e = 0; e < NBM; ++e) y[e] = yscr[r * NYE + 2 * NBM + e];
             if constexpr (NBB > 0) {
                 for (int q = t; q < 4 * NBB * RPC; q += NT) {
                     const int rr = q % RPC, eb = (q / RPC) % NBB, k4 = q / (RPC * NBB);
@@ -259,10 +262,13 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
                             }
                             ++seen;
                         }
-                    bY[q] = scr[rr * NYE + cls * NBM + e];
+                    bY[q] = yscr[rr * NYE + cls * NBM + e];
                 }
             }
             __syncthreads();
+            if constexpr (CL == 1) {
+                for (int q = t; q < TBUF; q += NT) T[q] = 0.0;
+            }
             clear_t1();
 
             for (int sgi = 0; sgi < sw && !blown; ++sgi) {
@@ -443,10 +449,11 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
     }
 }
 
-template <int V, int NX, int RPC, int NT, bool NZ>
+template <int V, int NX, int RPC, int NT, bool NZ, int CL>
 void launch_xm(s2b_context* ctx, const ClusterBatch& a) {
     constexpr Variant v = kVariants[V];
-    auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT, kXmP, NZ>;
+    constexpr int kXmCl = CL;
+    auto kern = cluster_xm_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, NT, kXmP, NZ, CL>;
     const size_t smem = XmLayout<v.mask, v.rx, v.rv, v.bm, NX, RPC>::bytes();
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
@@ -475,22 +482,36 @@ bool xm_enabled() {
 
 } // namespace
 
+// grids: 256^2 as 8 CTAs x 32 rows (15 clusters fit), 128^2 as 4 x 32 (33 fit), 64^2 as one
+// CTA of 64 rows per path (148 fit)
 bool cluster_xm_supported(int variant, int nx, int nv) {
     if (!xm_enabled()) return false;
     if (variant < 7 || variant > 9) return false;
-    return nx == 256 && nv == 256;
+    return nx == nv && (nx == 256 || nx == 128 || nx == 64);
 }
+
+namespace {
+template <int V, bool NZ>
+void launch_xm_grid(s2b_context* ctx, const ClusterBatch& a) {
+    switch (a.a[0].nx) {
+    case 256: launch_xm<V, 256, 32, kXmNT, NZ, 8>(ctx, a); break;
+    case 128: launch_xm<V, 128, 32, kXmNT, NZ, 4>(ctx, a); break;
+    case 64: launch_xm<V, 64, 64, kXmNT, NZ, 1>(ctx, a); break;
+    default: fail(S2B_ERR_RUNTIME, "x-march cluster engine: unsupported grid");
+    }
+}
+} // namespace
 
 void launch_cluster_xm(s2b_context* ctx, int variant, const ClusterBatch& a) {
     bool nz = true;
     for (int i = 0; i < a.n; ++i) nz = nz && a.a[i].nz;
     switch (variant * 2 + (nz ? 1 : 0)) {
-    case 14: launch_xm<7, 256, 32, kXmNT, false>(ctx, a); break;
-    case 15: launch_xm<7, 256, 32, kXmNT, true>(ctx, a); break;
-    case 16: launch_xm<8, 256, 32, kXmNT, false>(ctx, a); break;
-    case 17: launch_xm<8, 256, 32, kXmNT, true>(ctx, a); break;
-    case 18: launch_xm<9, 256, 32, kXmNT, false>(ctx, a); break;
-    case 19: launch_xm<9, 256, 32, kXmNT, true>(ctx, a); break;
+    case 14: launch_xm_grid<7, false>(ctx, a); break;
+    case 15: launch_xm_grid<7, true>(ctx, a); break;
+    case 16: launch_xm_grid<8, false>(ctx, a); break;
+    case 17: launch_xm_grid<8, true>(ctx, a); break;
+    case 18: launch_xm_grid<9, false>(ctx, a); break;
+    case 19: launch_xm_grid<9, true>(ctx, a); break;
     default: fail(S2B_ERR_RUNTIME, "x-march cluster engine: unsupported variant");
     }
     S2B_LAUNCHED(ctx);

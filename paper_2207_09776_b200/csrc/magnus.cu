@@ -1030,7 +1030,7 @@ double hybrid_fraction(const MagnusSession* s) {
     const char* e = std::getenv("S2B_HYBRID");
     if (e) return std::atof(e);
     const int v = s->op->variant, nx = static_cast<int>(s->op->nx), nv = static_cast<int>(s->op->nv);
-    if (cluster_xm_supported(v, nx, nv)) return 0.12;
+    if (cluster_xm_supported(v, nx, nv)) return nx == 256 ? 0.12 : (nx == 128 ? 0.06 : 0.0); // 120 / 132 / 148 SMs busy
     if (cluster_xmi_supported(v, nx, nv)) return 0.20;
     return 0.0;
 }

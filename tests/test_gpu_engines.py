@@ -203,3 +203,16 @@ def test_xm_bit_patterns(ref, s2b, ctx, negzero):
     assert stats["engine"] == 2
     assert np.array_equal(ens[-1].status, wst[-1])
     assert np.array_equal(ens[-1].states().view(np.uint64), want[-1].view(np.uint64))
+
+
+@pytest.mark.parametrize("d,order", [(64, 2), (128, 3), (64, 3)])
+def test_xm_small_grids_bitwise(ref, s2b, ctx, d, order):
+    """x-march engine on 128^2 (4-CTA clusters) and 64^2 (one CTA per path) vs the reference."""
+    T, dt, dt_leb, M, seed = 0.2, 0.1, 1e-3, 3, 61 + d
+    _, values, want, wst = _ref_run(ref, d, order, T, dt, dt_leb, M, seed, rec=[0.1])
+    ens, _, _, stats = gpu_magnus(s2b, ctx, "langevin-constant", d, order, values, dt_leb, T, dt,
+                                  rec=[0.1], seed=seed)
+    assert stats["engine"] == 2
+    for r, e in enumerate(ens):
+        assert np.array_equal(e.status, wst[r])
+        assert np.array_equal(e.states(), want[r], equal_nan=True)
