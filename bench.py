@@ -63,6 +63,12 @@ def fp64_peak_tops():
         return None
 
 
+def workload_name(args):
+    fam = ("constant-coefficient Langevin" if args.family == "langevin-constant"
+           else "variable-coefficient Langevin")
+    return f"{args.preset}: {fam}"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -82,7 +88,31 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--euler-steps", type=int, default=200, help="E-M steps timed beside Magnus (0 = skip)")
-    return ap.parse_args()
+    ap.add_argument("--config", default=None, choices=sorted(PRESETS),
+                    help="BASELINE.json workload preset (cfg2 is the default workload); explicit flags win")
+    args = ap.parse_args()
+    args.preset = args.config or "cfg2"
+    if args.config:
+        given = {a.split("=")[0].lstrip("-").replace("-", "_") for a in sys.argv[1:] if a.startswith("--")}
+        for k, v in PRESETS[args.config].items():
+            if k not in given:
+                setattr(args, k, v)
+    return args
+
+
+# BASELINE.json configs as bench presets.  cfg5's 128k paths over 8 GPUs are 16384 per GPU, far
+# beyond one B200 at 1024^2 (4 state vectors x 8 MB per path): they run as independent waves of
+# 4096 resident paths (128 GB of state), and one timed step is one window of one wave — every
+# wave is the same work, so the wave's rate is the job's rate.  A full T = 1 is hours at 1024^2
+# (SURVEY 8(d)): the preset times a fixed handful of windows (dt = 5e-4, dt_leb = 1e-5).
+PRESETS = {
+    "cfg2": {"d": 256, "paths": 16384, "dt": 0.01, "dt_leb": 1e-4, "T": 1.0, "order": 3,
+             "family": "langevin-constant"},
+    "cfg3": {"d": 256, "paths": 16384, "dt": 0.01, "dt_leb": 1e-4, "T": 1.0, "order": 3,
+             "family": "langevin-variable"},
+    "cfg5": {"d": 1024, "paths": 4096, "dt": 5e-4, "dt_leb": 1e-5, "T": 0.005, "order": 3,
+             "family": "langevin-constant", "steps": 3, "warmup": 3, "euler_steps": 100},
+}
 
 
 def peaks():
@@ -201,7 +231,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference xoshiro256++ Brownian paths, Gaussian datum)",
-        "config": {"workload": f"cfg2 bounded sample: {M_cpu} paths x 1 window, {args.d}x{args.d}, "
+        "config": {"workload": f"{args.preset} bounded sample: {M_cpu} paths x 1 window, {args.d}x{args.d}, "
                                f"order {args.order}, dt={args.dt}, dt_leb={args.dt_leb}",
                    "grid": args.d, "paths": M_cpu, "order": args.order, "dt": args.dt},
         "cpu_baseline": {"value": value, "unit": "path*gridpoint*windows/s", "cores": threads,
@@ -337,7 +367,9 @@ def run_ours(args):
         e2e = {"value": world * M * n * args.steps / el, "unit": "path*gridpoint*windows/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
 
-    # Euler-Maruyama on the same grid/paths (dt = dt_leb), reported beside Magnus
+    # Euler-Maruyama on the same grid/paths (dt = dt_leb), reported beside Magnus; the Magnus
+    # session's state is released first (at 1024^2 both would not fit one GPU)
+    del sess
     em = None
     if args.euler_steps > 0:
         try:
@@ -351,8 +383,9 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Philox Brownian paths, Gaussian datum, Langevin a=1.1 sigma=1/sqrt(10))",
-        "config": {"workload": (f"cfg2: constant-coefficient Langevin" if args.family == "langevin-constant"
-                                else f"cfg3: variable-coefficient Langevin") + f" {args.d}x{args.d}, {M} paths/GPU, "
+        "config": {"workload": workload_name(args) + f" {args.d}x{args.d}, {M} paths/GPU"
+                               + (" (one wave of the 16384 per GPU that 128k paths over 8 GPUs give)"
+                                  if args.preset == "cfg5" else "") + ", "
                                f"order-{args.order} iterated Magnus, dt={args.dt} ({nwin} windows), "
                                f"T={args.T}, dt_leb={args.dt_leb}, tol=1e-10, theta=1",
                    "grid": args.d, "family": args.family, "paths_per_gpu": M, "order": args.order, "dt": args.dt,

@@ -10,8 +10,11 @@
 // dW is the difference of prefix values (euler.cpp:156), so E-M and Magnus consume
 // the same paths.
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "s2b_internal.cuh"
@@ -22,6 +25,7 @@ namespace {
 
 struct EmArgs {
     const double* f; // 9 * n (only mask fields valid)
+    const double* rowf; // [9][nv] row values when every field is x-invariant
     int mask;
     int nx, nv;
     double st[5];
@@ -88,6 +92,132 @@ __global__ void __launch_bounds__(256) em_step_kernel(EmArgs a) {
     }
     if (inf_seen) a.blown[m] = 1;
   }
+}
+
+// The reference's per-point update (euler.cpp:51-80) on register operands: the same
+// expressions, in the same order, as em_step_kernel (without g^xv, which needs diagonals).
+__device__ __forceinline__ double em_point(int mask, const double* fv, const double* st, double dt,
+                                           double dW, double uc, double uxm, double uxp, double uvm,
+                                           double uvp) {
+    const double dxu = (uxp - uxm) * st[0];
+    const double dvu = (uvp - uvm) * st[2];
+    double drift = 0.0;
+    if (mask & 1) drift += fv[0] * uc;
+    if (mask & 2) drift += fv[1] * dxu;
+    if (mask & 4) drift += fv[2] * dvu;
+    if (mask & 8) {
+        const double dxxu = (uxp - 2.0 * uc + uxm) * st[1];
+        drift += 0.5 * fv[3] * dxxu;
+    }
+    if (mask & 32) {
+        const double dvvu = (uvp - 2.0 * uc + uvm) * st[3];
+        drift += 0.5 * fv[5] * dvvu;
+    }
+    double noise = 0.0;
+    if (mask & 64) noise += fv[6] * uc;
+    if (mask & 128) noise += fv[7] * dxu;
+    if (mask & 256) noise += fv[8] * dvu;
+    return uc + drift * dt + noise * dW;
+}
+
+// Row-marching streaming step (any fields without g^xv, even nx <= 1024): a work item is
+// (group of P paths, strip of R rows); thread t owns x-points 2t, 2t+1 of every row (16-byte
+// loads and stores), marches down the strip with rows j-1, j, j+1 of each path in registers
+// and row j+2 in flight, and takes its x-neighbours from the adjacent lanes (warp-edge lanes
+// read the one value across the warp boundary from L1).  The P paths share every field load.
+// Items are ordered strip-fastest so neighbouring CTAs share halo rows in L2.
+template <int P, int D, int MASK, bool XINV>
+__global__ void __launch_bounds__(512) em_rows_kernel(EmArgs a, int R, int strips, int items) {
+    const int nx = a.nx, nv = a.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+    const int t = threadIdx.x, lane = t & 31;
+    const int x0 = 2 * t;
+    const bool act = x0 < nx;
+    const int mask = MASK >= 0 ? MASK : a.mask;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int g = item / strips;
+        const int j0 = (item - g * strips) * R, j1 = min(nv, j0 + R);
+        const double* u[P];
+        double* o[P];
+        double dW[P];
+        bool live[P];
+        bool any = false;
+        #pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const size_t m = static_cast<size_t>(g) * P + p;
+            live[p] = m < a.M && !a.blown[m];
+            any |= live[p];
+            const size_t mm = live[p] ? m : 0;
+            u[p] = a.in + mm * n;
+            o[p] = a.out + mm * n;
+            const double* pv = a.values + mm * a.vstride;
+            dW[p] = live[p] ? pv[a.k1] - pv[a.k0] : 0.0;
+        }
+        if (!any) continue; // the reference stops a blown path (euler.cpp:159-162)
+        auto ld = [&](int p, int j) -> double2 {
+            if (!act || !live[p] || j < 0 || j >= nv) return make_double2(0.0, 0.0);
+            return __ldg(reinterpret_cast<const double2*>(u[p] + static_cast<size_t>(j) * nx + x0));
+        };
+        // rows j-1, j, j+1 in registers, rows j+2 .. j+1+D in flight
+        double2 rm[P], rc[P], rp[P], rq[D][P];
+        #pragma unroll
+        for (int p = 0; p < P; ++p) {
+            rm[p] = ld(p, j0 - 1);
+            rc[p] = ld(p, j0);
+            rp[p] = ld(p, j0 + 1);
+            #pragma unroll
+            for (int q = 0; q < D - 1; ++q) rq[q][p] = ld(p, j0 + 2 + q);
+        }
+        bool inf_seen[P];
+        #pragma unroll
+        for (int p = 0; p < P; ++p) inf_seen[p] = false;
+        for (int j = j0; j < j1; ++j) {
+            #pragma unroll
+            for (int p = 0; p < P; ++p) rq[D - 1][p] = ld(p, j + 1 + D);
+            const size_t r = static_cast<size_t>(j) * nx + x0;
+            double fa[9], fb[9];
+            #pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                fa[k] = fb[k] = 0.0;
+                if (k != 4 && (mask >> k & 1)) {
+                    if (XINV) {
+                        fa[k] = fb[k] = __ldg(a.rowf + k * nv + j);
+                    } else if (act) {
+                        const double2 fk = __ldg(reinterpret_cast<const double2*>(a.f + k * n + r));
+                        fa[k] = fk.x;
+                        fb[k] = fk.y;
+                    }
+                }
+            }
+            #pragma unroll
+            for (int p = 0; p < P; ++p) {
+                double left = __shfl_up_sync(0xffffffffu, rc[p].y, 1);
+                double right = __shfl_down_sync(0xffffffffu, rc[p].x, 1);
+                if (lane == 0) left = (act && live[p] && x0 > 0) ? __ldg(u[p] + r - 1) : 0.0;
+                if (x0 + 2 >= nx) right = 0.0;
+                else if (lane == 31) right = live[p] ? __ldg(u[p] + r + 2) : 0.0;
+                if (!act || !live[p]) continue;
+                const double na = em_point(mask, fa, a.st, a.dt, dW[p], rc[p].x, left, rc[p].y,
+                                           rm[p].x, rp[p].x);
+                const double nb = em_point(mask, fb, a.st, a.dt, dW[p], rc[p].y, rc[p].x, right,
+                                           rm[p].y, rp[p].y);
+                *reinterpret_cast<double2*>(o[p] + r) = make_double2(na, nb);
+                const double inf = __longlong_as_double(0x7FF0000000000000LL);
+                inf_seen[p] |= (fabs(na) == inf) | (fabs(nb) == inf);
+            }
+            #pragma unroll
+            for (int p = 0; p < P; ++p) {
+                rm[p] = rc[p];
+                rc[p] = rp[p];
+                rp[p] = rq[0][p];
+                #pragma unroll
+                for (int q = 0; q < D - 1; ++q) rq[q][p] = rq[q + 1][p];
+            }
+        }
+        #pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (inf_seen[p]) a.blown[static_cast<size_t>(g) * P + p] = 1;
+    }
 }
 
 __global__ void em_record_status_kernel(const int* blown, uint8_t* status, size_t M) {
@@ -199,6 +329,37 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         a.blown = blown.p;
         a.M = M;
         const unsigned gx = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64));
+        // the row-marching kernel: even nx up to 1024 points, no g^xv (S2B_EMROWS=0: the old one)
+#ifndef S2B_EM_D
+#define S2B_EM_D 4
+#endif
+        constexpr int kP = 2, kR = 32, kD = S2B_EM_D; // paths per item, rows per strip, rows in flight
+        const char* er = std::getenv("S2B_EMROWS");
+        const bool rows = !(f->mask & 16) && f->nx % 2 == 0 && f->nx <= 1024 && !(er && er[0] == '0');
+        const int nt = static_cast<int>(((f->nx / 2 + 31) / 32) * 32);
+        const int strips = static_cast<int>((f->nv + kR - 1) / kR);
+        const size_t items_sz = ((M + kP - 1) / kP) * static_cast<size_t>(strips);
+        if (items_sz > static_cast<size_t>(INT_MAX)) fail(S2B_ERR_CONFIG, "solve_euler: too many paths");
+        const int items = static_cast<int>(items_sz);
+        a.rowf = f->d_rowf.p;
+        using RowsFn = void (*)(EmArgs, int, int, int);
+        auto pick = [&](auto dtag) -> RowsFn {
+            constexpr int D = decltype(dtag)::value;
+            return f->mask == (2 | 32 | 256) ? (f->xinv ? em_rows_kernel<kP, D, 2 | 32 | 256, true>
+                                                        : em_rows_kernel<kP, D, 2 | 32 | 256, false>)
+                                             : em_rows_kernel<kP, D, -1, false>;
+        };
+        const char* ed = std::getenv("S2B_EM_D"); // rows in flight (A/B runs)
+        const int dsel = ed ? std::atoi(ed) : kD;
+        RowsFn rows_fn = dsel == 2 ? pick(std::integral_constant<int, 2>{})
+                         : dsel == 6 ? pick(std::integral_constant<int, 6>{})
+                                     : pick(std::integral_constant<int, kD>{});
+        int rows_grid = 0;
+        if (rows) {
+            int per_sm = 0;
+            S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fn, nt, 0));
+            rows_grid = std::max(1, std::min(items, std::max(1, per_sm) * ctx->num_sms));
+        }
         size_t rec = 0;
         int cur = 0;
         for (size_t k = 0; k < nsteps; ++k) {
@@ -207,7 +368,9 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
             a.in = U[cur].p;
             a.out = U[cur ^ 1].p;
             dim3 grid(gx, static_cast<unsigned>(std::min<size_t>(M, 65535)));
-            if (f->mask & 16)
+            if (rows)
+                rows_fn<<<rows_grid, nt, 0, ctx->stream>>>(a, kR, strips, items);
+            else if (f->mask & 16)
                 em_step_kernel<true><<<grid, 256, 0, ctx->stream>>>(a);
             else
                 em_step_kernel<false><<<grid, 256, 0, ctx->stream>>>(a);
