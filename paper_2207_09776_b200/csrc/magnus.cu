@@ -574,6 +574,12 @@ s2b_operator* make_operator(s2b_context* ctx, const s2b_grid* grid, int order,
     }
     op->pair_begin[kBoxBits] = static_cast<int>(op->pair_slot.size());
     op->npairs = static_cast<int>(op->pair_slot.size());
+    for (size_t q = 0; q < pw.size() && op->wfinite; ++q)
+        for (double v : *pw[q])
+            if (!std::isfinite(v)) {
+                op->wfinite = false;
+                break;
+            }
 
     // x-invariance check: W(i, j) == W(class representative, j) bitwise for every pair
     bool comp = nx >= 5;
@@ -825,7 +831,9 @@ void launch_term(MagnusSession& s) {
         const int grid = grid_for(s.ctx, s.M * blocks_per_path, bs);
         constexpr int kGenK = S2B_GENK_K; // live paths per work item (shares every weight load)
         const int grid_k = grid_for(s.ctx, (s.M + kGenK - 1) / kGenK * blocks_per_path, bs);
-        if (generic_k_enabled())
+        if (term_var_supported(s.op))
+            launch_term_var(s.ctx, s.op, a, s.M);
+        else if (generic_k_enabled())
             term_generic_k_kernel<kGenK><<<grid_k, bs, 0, s.ctx->stream>>>(a, s.bits.p, s.nbits);
         else
             term_generic_kernel<<<grid, bs, 0, s.ctx->stream>>>(a, s.bits.p, s.nbits);

@@ -200,6 +200,11 @@ void launch_term_nt128(s2b_context* ctx, int variant, const TermArgs& a, int nt,
 void launch_term_nt256(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
 void launch_term_nt512(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
 
+// Streaming term kernel for uncompressed (x-dependent) weights with a Langevin union mask
+// (term_var.cu); S2B_TERMVAR=0 falls back to term_generic_k_kernel.
+bool term_var_supported(const s2b_operator* op);
+void launch_term_var(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, size_t live_max);
+
 // Cluster-resident engine (cluster_magnus.cu): one 8-CTA cluster per path, all Taylor terms
 // of windows [win0, win1) on chip.
 struct ClusterArgs {

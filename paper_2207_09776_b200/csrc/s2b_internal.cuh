@@ -91,6 +91,7 @@ struct s2b_operator {
     std::vector<int> pair_begin; // kBoxBits + 1
     std::vector<int> pair_slot;  // npairs
     int npairs = 0;
+    bool wfinite = true;      // every source weight finite (term_var's branch-free fold)
     s2b::DevBuf<int> d_pair_begin, d_pair_slot;
     s2b::DevBuf<double> d_wt; // entry-major weights of the TMA kernel variant
     s2b::DevBuf<int> d_eslot;
