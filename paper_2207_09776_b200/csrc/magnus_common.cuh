@@ -138,6 +138,14 @@ struct MaskInfo {
         return n;
     }
     static constexpr bool has(int dx, int dv) { return (MASK >> box_bit(dx, dv)) & 1; }
+    static constexpr int bit_of(int e) { // the e-th set bit
+        for (int b = 0; b < kBoxBits; ++b)
+            if ((MASK >> b) & 1) {
+                if (e == 0) return b;
+                --e;
+            }
+        return -1;
+    }
 };
 
 // One work item = (live path, strip of kStripRows output rows).  Threads own two adjacent

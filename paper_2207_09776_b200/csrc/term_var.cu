@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <initializer_list>
+#include <type_traits>
+#include <utility>
 
 #include "magnus_common.cuh"
 
@@ -32,6 +34,13 @@ constexpr int kVarNT = 256;  // threads per CTA
 constexpr int kVarRows = 32; // output rows per work item
 constexpr int kRing = 8;     // ring rows per path (power of two, >= 2*KRV + 2)
 
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    [&]<int... I>(std::integer_sequence<int, I...>) {
+        (f(std::integral_constant<int, I>{}), ...);
+    }(std::make_integer_sequence<int, N>{});
+}
+
 // PCNT: 3 bits per stencil entry (mask rank) = its number of source pairs
 template <uint64_t PCNT>
 struct Pc {
@@ -43,10 +52,17 @@ struct Pc {
     }
 };
 
-template <int K, uint64_t MASK, uint64_t PCNT, int KRX, int KRV, int XPT>
+// PS0, PS1: 3 bits per source pair (pairs 0-20, 21-41) = its CommutatorSet slot
+template <uint64_t PS0, uint64_t PS1>
+struct Ps {
+    static constexpr int slot(int q) { return static_cast<int>(((q < 21 ? PS0 >> (3 * q) : PS1 >> (3 * (q - 21)))) & 7); }
+};
+
+// TW: the weight rows stream through shared memory (TMA, double-buffered); otherwise (grids
+// whose two weight rows do not fit next to the ring) each point loads its weights from L2.
+template <int K, uint64_t MASK, uint64_t PCNT, uint64_t PS0, uint64_t PS1, int KRX, int KRV, int XPT, bool TW>
 __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int strips) {
     static_assert(2 * KRV + 2 <= kRing, "ring too short");
-    static_assert(K % 2 == 0, "pairs of paths share 16-byte coefficient loads");
     constexpr int NB = MaskInfo<MASK>::count();
     constexpr int NP = Pc<PCNT>::off(NB);
     const int nx = a.op.nx, nv = a.op.nv;
@@ -54,15 +70,29 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     const int RWS = nx + 2 * KRX; // ring row stride (zero x-halo on both sides)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
-    extern __shared__ __align__(16) double vsm[];
-    double* ring = vsm;                                         // [K][kRing][RWS]
-    double* cq = ring + static_cast<size_t>(K) * kRing * RWS;   // [NP][K] coefficient per pair
-    __shared__ int bslot[NP];                                   // pair -> CommutatorSet slot
+    extern __shared__ __align__(128) double vsm[];
+    double* wbuf = vsm;                                          // [2][NP][nx] weights of rows j, j+1
+    double* ring = wbuf + (TW ? 2 * static_cast<size_t>(NP) * nx : 0); // [K][kRing][RWS]
+    __shared__ __align__(8) uint64_t bar[2];
     __shared__ unsigned long long red[K][2][kVarNT / 32];
 
-    for (int q = t; q < NP; q += kVarNT) bslot[q] = a.op.pair_slot[q];
     for (int q = t; q < K * kRing * RWS; q += kVarNT) ring[q] = 0.0; // x-halos stay zero
+    if (TW && t == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
+    uint32_t ph = 0; // parity of the next wait on each weight buffer (bit b)
+    // one elected thread streams row jw's weights (NP rows of nx doubles) into buffer jw & 1
+    auto issue = [&](int jw) {
+        double* dst = wbuf + static_cast<size_t>(jw & 1) * NP * nx;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
+        mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * nx * 8));
+        for (int q = 0; q < NP; ++q)
+            tma_row(dst + static_cast<size_t>(q) * nx, a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx,
+                    static_cast<uint32_t>(nx * 8), &bar[jw & 1]);
+    };
 
     const int live = a.cnt[0];
     const int groups = (live + K - 1) / K;
@@ -77,6 +107,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
         double* Tout[K];
         double* Sout[K];
         double inv[K];
+        double c[K][6];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             pk[k] = g * K + k < live ? a.act[g * K + k] : -1;
@@ -87,13 +118,12 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
             in[k] = kk == 1 ? Sin[k] : (par ? a.T1 : a.T0) + static_cast<size_t>(p) * n;
             Tout[k] = (par ? a.T0 : a.T1) + static_cast<size_t>(p) * n;
             Sout[k] = (par ? a.S0 : a.S1) + static_cast<size_t>(p) * n;
+            const double* cp = a.ctab + (static_cast<size_t>(p) * a.nwin + a.win[p]) * 6;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) c[k][q] = pk[k] >= 0 ? cp[q] : 0.0;
         }
-        __syncthreads(); // the previous item is done with cq and the ring
-        for (int q = t; q < NP * K; q += kVarNT) {
-            const int pq = q / K, k = q - pq * K;
-            const int p = pk[k] >= 0 ? pk[k] : a.act[g * K];
-            cq[q] = pk[k] >= 0 ? a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + bslot[pq]] : 0.0;
-        }
+        __syncthreads(); // the previous item is done with the ring and both weight buffers
+        if (TW && t == 0) issue(j0);
         // ring rows j0-KRV .. j0+KRV (zero outside the grid)
         for (int jr = j0 - KRV; jr <= j0 + KRV; ++jr) {
 #pragma unroll
@@ -114,6 +144,8 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
         for (int k = 0; k < K; ++k) tb[k] = sb[k] = 0;
 
         for (int j = j0; j < j1; ++j) {
+            // the next row's weights (its buffer was last read in row j-1, before the barrier)
+            if (TW && t == 0 && j + 1 < j1) issue(j + 1);
             // prefetch: the ring's next row and this row's accumulator
             const int jn = j + KRV + 1;
             double nxt[K][XPT], sacc[K][XPT];
@@ -126,46 +158,49 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
                     nxt[k][u] = (ok && jn < nv) ? in[k][static_cast<size_t>(jn) * nx + i] : 0.0;
                     sacc[k][u] = ok ? Sin[k][static_cast<size_t>(j) * nx + i] : 0.0;
                 }
+            if (TW) {
+                mbar_wait(&bar[j & 1], (ph >> (j & 1)) & 1u);
+                ph ^= 1u << (j & 1);
+            }
+            const double* wr = wbuf + static_cast<size_t>(j & 1) * NP * nx;
 #pragma unroll
             for (int u = 0; u < XPT; ++u) {
                 const int i = t + u * kVarNT;
                 if (i >= nx) continue;
                 const size_t r = static_cast<size_t>(j) * nx + i;
-                double w[NP];
+                double wg[TW ? 1 : NP]; // the point's weights, all loads in flight at once
+                if constexpr (!TW) {
 #pragma unroll
-                for (int q = 0; q < NP; ++q) w[q] = __ldg(a.op.w + static_cast<size_t>(q) * n + r);
+                    for (int q = 0; q < NP; ++q) wg[q] = __ldg(a.op.w + static_cast<size_t>(q) * n + r);
+                }
                 double acc[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) acc[k] = 0.0;
+                // stencil entries in ascending bit order (== ascending (dv, dx)), all compile-time
+                static_for<NB>([&](auto E) {
+                    constexpr int e = decltype(E)::value;
+                    constexpr int b = MaskInfo<MASK>::bit_of(e);
+                    constexpr int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
+                    constexpr int q0 = Pc<PCNT>::off(e);
+                    double y[K];
 #pragma unroll
-                for (int dv = -KRV; dv <= KRV; ++dv) {
+                    for (int k = 0; k < K; ++k) y[k] = 0.0;
+                    static_for<Pc<PCNT>::cnt(e)>([&](auto C) {
+                        constexpr int q = q0 + decltype(C)::value;
+                        constexpr int sl = Ps<PS0, PS1>::slot(q);
+                        double w;
+                        if constexpr (TW) w = wr[q * nx + i];
+                        else w = wg[q];
 #pragma unroll
-                    for (int dx = -KRX; dx <= KRX; ++dx) {
-                        if (!MaskInfo<MASK>::has(dx, dv)) continue;
-                        const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
-                        const int q0 = Pc<PCNT>::off(e), nq = Pc<PCNT>::cnt(e);
-                        double y[K];
+                        for (int k = 0; k < K; ++k) y[k] += c[k][sl] * w;
+                    });
+                    const int jr = (j + dv) & (kRing - 1);
 #pragma unroll
-                        for (int k = 0; k < K; ++k) y[k] = 0.0;
-#pragma unroll
-                        for (int c = 0; c < 7; ++c) {
-                            if (c >= nq) break;
-                            const int q = q0 + c;
-#pragma unroll
-                            for (int k = 0; k < K; k += 2) {
-                                const double2 cs = *reinterpret_cast<const double2*>(cq + q * K + k);
-                                y[k] += cs.x * w[q];
-                                y[k + 1] += cs.y * w[q];
-                            }
-                        }
-                        const int jr = (j + dv) & (kRing - 1);
-#pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            const double x = ring[(static_cast<size_t>(k) * kRing + jr) * RWS + KRX + i + dx];
-                            acc[k] += y[k] * x;
-                        }
+                    for (int k = 0; k < K; ++k) {
+                        const double x = ring[(static_cast<size_t>(k) * kRing + jr) * RWS + KRX + i + dx];
+                        acc[k] += y[k] * x;
                     }
-                }
+                });
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     if (pk[k] < 0) continue;
@@ -238,13 +273,53 @@ uint64_t pcnt_from(const s2b_operator* op) {
         }
     return v;
 }
+// pair slots, 3 bits each: pairs [0, 21) in ps[0], [21, 42) in ps[1]
+bool pslots_from(const s2b_operator* op, uint64_t ps[2]) {
+    ps[0] = ps[1] = 0;
+    if (op->pair_slot.size() > 42) return false;
+    for (size_t q = 0; q < op->pair_slot.size(); ++q)
+        ps[q / 21] |= static_cast<uint64_t>(op->pair_slot[q]) << (3 * (q % 21));
+    return true;
+}
+constexpr uint64_t pslot_of(std::initializer_list<int> sl, int part) {
+    uint64_t v = 0;
+    int q = 0;
+    for (int x : sl) {
+        if (q / 21 == part) v |= static_cast<uint64_t>(x) << (3 * (q % 21));
+        ++q;
+    }
+    return v;
+}
+#define S2B_SL19V {4, 5, 2, 4, 5, 5, 3, 5, 0, 1, 4, 5, 3, 5, 5, 0, 4, 5, 0, 2, 3, 0, 4, 5, 5, 3, 5, 0, 1, 4, 5, 3, 5, 5, 4, 5, 2, 4, 5}
+#define S2B_SL19C {4, 5, 2, 4, 5, 5, 3, 0, 1, 4, 5, 3, 5, 0, 4, 0, 2, 3, 0, 4, 5, 3, 0, 1, 4, 5, 3, 5, 4, 5, 2, 4, 5}
+#define S2B_SL11 {2, 3, 0, 1, 3, 0, 0, 2, 3, 0, 3, 0, 1, 3, 2}
+#define S2B_SL5 {0, 1, 0, 0, 0, 0, 1}
+struct VarFam {
+    uint64_t mask, pc, ps0, ps1;
+};
+constexpr VarFam kFam19v{kMask19, kPc19var, pslot_of(S2B_SL19V, 0), pslot_of(S2B_SL19V, 1)};
+constexpr VarFam kFam19c{kMask19, kPc19con, pslot_of(S2B_SL19C, 0), pslot_of(S2B_SL19C, 1)};
+constexpr VarFam kFam11{kMask11, kPc11, pslot_of(S2B_SL11, 0), 0};
+constexpr VarFam kFam5{kMask5, kPc5, pslot_of(S2B_SL5, 0), 0};
 
-template <int K, uint64_t MASK, uint64_t PCNT, int KRX, int KRV>
+int fam_of(const s2b_operator* op) {
+    uint64_t ps[2];
+    if (!pslots_from(op, ps)) return -1;
+    const uint64_t pc = pcnt_from(op);
+    const VarFam fams[4] = {kFam19v, kFam19c, kFam11, kFam5};
+    for (int f = 0; f < 4; ++f)
+        if (op->union_mask == fams[f].mask && pc == fams[f].pc && ps[0] == fams[f].ps0 && ps[1] == fams[f].ps1)
+            return f;
+    return -1;
+}
+
+template <int K, VarFam F, int KRX, int KRV>
 void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
-    constexpr int NP = Pc<PCNT>::off(MaskInfo<MASK>::count());
+    constexpr int NP = Pc<F.pc>::off(MaskInfo<F.mask>::count());
     const int nx = a.op.nx, nv = a.op.nv;
     const int strips = (nv + kVarRows - 1) / kVarRows;
-    const size_t smem = (static_cast<size_t>(K) * kRing * (nx + 2 * KRX) + static_cast<size_t>(NP) * K) * 8;
+    const bool tw = nx <= kVarNT;
+    const size_t smem = ((tw ? 2 * static_cast<size_t>(NP) * nx : 0) + static_cast<size_t>(K) * kRing * (nx + 2 * KRX)) * 8;
     auto go = [&](auto kern) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
@@ -254,12 +329,17 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
         kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips);
     };
-    if (nx <= kVarNT)
-        go(term_var_kernel<K, MASK, PCNT, KRX, KRV, 1>);
+    if (tw)
+        go(term_var_kernel<K, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, 1, true>);
     else if (nx <= 2 * kVarNT)
-        go(term_var_kernel<K, MASK, PCNT, KRX, KRV, 2>);
+        go(term_var_kernel<K, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, 2, false>);
     else
-        go(term_var_kernel<K, MASK, PCNT, KRX, KRV, 4>);
+        go(term_var_kernel<K, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, 4, false>);
+}
+
+// shared memory of one CTA: two weight rows + the K-path ring must fit 227 KB
+size_t var_smem(int np, int k, int nx, int krx) {
+    return (2 * static_cast<size_t>(np) * nx + static_cast<size_t>(k) * kRing * (nx + 2 * krx)) * 8;
 }
 
 } // namespace
@@ -267,27 +347,33 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
 bool term_var_supported(const s2b_operator* op) {
     const char* e = std::getenv("S2B_TERMVAR");
     if (e && e[0] == '0') return false;
-    if (op->compressed || !op->wfinite || op->nx < 1 || op->nx > 4 * static_cast<size_t>(kVarNT)) return false;
-    const uint64_t pc = pcnt_from(op);
-    return (op->union_mask == kMask19 && (pc == kPc19var || pc == kPc19con)) ||
-           (op->union_mask == kMask11 && pc == kPc11) || (op->union_mask == kMask5 && pc == kPc5);
+    if (op->compressed || !op->wfinite || op->nx < 2 || op->nx % 2 != 0 || op->nx > 4 * static_cast<size_t>(kVarNT))
+        return false;
+    const int f = fam_of(op);
+    if (f < 0) return false;
+    const int nx = static_cast<int>(op->nx);
+    return nx > kVarNT || var_smem(op->npairs, 4, nx, 2) <= 227 * 1024;
 }
 
 void launch_term_var(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, size_t live_max) {
-    const bool wide = op->nx > 2 * static_cast<size_t>(kVarNT);
-    const uint64_t pc = pcnt_from(op);
-    if (op->union_mask == kMask19 && pc == kPc19var) {
-        if (wide) launch_var_k<2, kMask19, kPc19var, 2, 2>(ctx, a, live_max);
-        else launch_var_k<4, kMask19, kPc19var, 2, 2>(ctx, a, live_max);
-    } else if (op->union_mask == kMask19) {
-        if (wide) launch_var_k<2, kMask19, kPc19con, 2, 2>(ctx, a, live_max);
-        else launch_var_k<4, kMask19, kPc19con, 2, 2>(ctx, a, live_max);
-    } else if (op->union_mask == kMask11) {
-        if (wide) launch_var_k<2, kMask11, kPc11, 1, 2>(ctx, a, live_max);
-        else launch_var_k<4, kMask11, kPc11, 1, 2>(ctx, a, live_max);
-    } else {
-        if (wide) launch_var_k<2, kMask5, kPc5, 1, 1>(ctx, a, live_max);
-        else launch_var_k<4, kMask5, kPc5, 1, 1>(ctx, a, live_max);
+    const bool wide = op->nx > 2 * static_cast<size_t>(kVarNT); // 2 paths per item at 1024^2
+    switch (fam_of(op)) {
+    case 0:
+        if (wide) launch_var_k<2, kFam19v, 2, 2>(ctx, a, live_max);
+        else launch_var_k<4, kFam19v, 2, 2>(ctx, a, live_max);
+        break;
+    case 1:
+        if (wide) launch_var_k<2, kFam19c, 2, 2>(ctx, a, live_max);
+        else launch_var_k<4, kFam19c, 2, 2>(ctx, a, live_max);
+        break;
+    case 2:
+        if (wide) launch_var_k<2, kFam11, 1, 2>(ctx, a, live_max);
+        else launch_var_k<4, kFam11, 1, 2>(ctx, a, live_max);
+        break;
+    default:
+        if (wide) launch_var_k<2, kFam5, 1, 1>(ctx, a, live_max);
+        else launch_var_k<4, kFam5, 1, 1>(ctx, a, live_max);
+        break;
     }
 }
 

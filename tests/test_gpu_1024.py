@@ -10,9 +10,12 @@ from test_gpu_parity import gpu_magnus
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("family,order", [("langevin-constant", 3), ("langevin-variable", 2)])
-def test_magnus_bitwise_1024(ref, s2b, ctx, family, order):
-    d, T, dt, dt_leb, M, seed = 1024, 4e-4, 2e-4, 1e-5, 2, 1024 + order
+@pytest.mark.parametrize("family,order,d", [("langevin-constant", 3, 1024), ("langevin-variable", 2, 1024),
+                                            ("langevin-variable", 3, 512), ("langevin-variable", 3, 1024)])
+def test_magnus_bitwise_1024(ref, s2b, ctx, family, order, d):
+    """Streaming engines at 512^2 / 1024^2: term_tma_kernel (constant), term_var_kernel with
+    weights loaded per point (variable coefficients, 4 and 2 paths per item)."""
+    T, dt, dt_leb, M, seed = 4e-4, 2e-4, 1e-5, 3, d + order
     ops = ref.Ops(family, d, order=order)
     values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
     want, wst, _ = ops.solve_magnus(values, dt_leb, T, dt, record_times=[dt], seed=seed)
