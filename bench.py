@@ -198,6 +198,12 @@ def max_over_ranks(x, dist, local):
     return float(t.item())
 
 
+ENGINE_VAR = {"name": "stream", "kernel": "term_var_kernel", "profile": "term_var_ncu.json",
+              "note": "streaming pass engine, x-dependent weights: Y folded per point from the source weights "
+                      "(streamed through shared memory by TMA, shared by 4 paths) every term; term and "
+                      "accumulator round-trip HBM; bound by the fp64 pipe (fold + apply, compute_roofline)"}
+
+
 def cpu_reference_leg(args, n_paths, windows, reps=1):
     """The reference C++ (oracle/_ref, OpenMP on every host core) on a bounded sample:
     `n_paths` paths over `windows` Magnus windows of the same workload."""
@@ -307,6 +313,8 @@ def run_ours(args):
     tk_ms = st1["term_kernel_ms"] - st0["term_kernel_ms"]
     tk_launches = st1["term_launches"] - st0["term_launches"]
     engine = ENGINES.get(st1.get("engine", 0), ENGINES[0])
+    if engine["name"] == "stream" and args.family == "langevin-variable":
+        engine = ENGINE_VAR  # x-dependent weights: the streaming pass runs term_var_kernel
     peak, peak_kind = peaks()
     achieved = alg_bytes / (tk_ms / 1e3) / 1e9 if tk_ms > 0 else 0.0
     traffic = None
@@ -328,11 +336,14 @@ def run_ours(args):
         pass
     # the on-chip engines are bound by the fp64 pipe, not HBM: report that ceiling beside it
     # (DMUL + DADD per stencil point, no FMA for bitwise parity; +1 DMUL, +1 DADD per point)
-    fp64_ops = n * terms * (2.0 * stencil_points(args.order) + 2.0)
+    ops_pt = 2 * stencil_points(args.order) + 2
+    if args.family == "langevin-variable":  # + the per-term fold of Y from the source pairs
+        ops_pt += 2 * {1: 7, 2: 15, 3: 39}[args.order]
+    fp64_ops = n * terms * float(ops_pt)
     fp64_peak = fp64_peak_tops()
     compute = {"bound": "fp64", "achieved": fp64_ops / (tk_ms / 1e3) / 1e12 if tk_ms > 0 else 0.0,
                "peak": fp64_peak, "unit": "TFLOP/s (DMUL/DADD, non-FMA)",
-               "ops_model": f"{2 * stencil_points(args.order) + 2} fp64 ops per path*gridpoint*term",
+               "ops_model": f"{ops_pt} fp64 ops per path*gridpoint*term",
                "ncu_fp64_pipe_pct_of_active": prof.get("fp64_pipe_pct_of_active")}
     compute["frac"] = compute["achieved"] / fp64_peak if fp64_peak else None
 

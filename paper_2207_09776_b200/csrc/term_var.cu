@@ -84,12 +84,16 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     }
     __syncthreads();
     uint32_t ph = 0; // parity of the next wait on each weight buffer (bit b)
-    // one elected thread streams row jw's weights (NP rows of nx doubles) into buffer jw & 1
+    // warp 0 streams row jw's weights (NP rows of nx doubles) into buffer jw & 1: lane 0 arms
+    // the barrier, then every lane issues the bulk copies of its pairs
     auto issue = [&](int jw) {
         double* dst = wbuf + static_cast<size_t>(jw & 1) * NP * nx;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
-        mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * nx * 8));
-        for (int q = 0; q < NP; ++q)
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
+            mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * nx * 8));
+        }
+        __syncwarp();
+        for (int q = lane; q < NP; q += 32)
             tma_row(dst + static_cast<size_t>(q) * nx, a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx,
                     static_cast<uint32_t>(nx * 8), &bar[jw & 1]);
     };
@@ -98,8 +102,11 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     const int groups = (live + K - 1) / K;
     const long long items = static_cast<long long>(groups) * strips;
     for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-        const int strip = static_cast<int>(it / groups);
-        const int g = static_cast<int>(it - static_cast<long long>(strip) * groups);
+        // TW (all weights L2-resident): strips fastest, so the CTAs resident at one time read
+        // different weight rows (no L2-slice hot spot); otherwise path groups fastest, so they
+        // share one strip's weights while the whole set does not fit L2
+        const int strip = TW ? static_cast<int>(it % strips) : static_cast<int>(it / groups);
+        const int g = TW ? static_cast<int>(it / strips) : static_cast<int>(it - static_cast<long long>(strip) * groups);
         const int j0 = strip * kVarRows, j1 = min(nv, j0 + kVarRows);
         int pk[K];
         const double* in[K];
@@ -123,7 +130,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
             for (int q = 0; q < 6; ++q) c[k][q] = pk[k] >= 0 ? cp[q] : 0.0;
         }
         __syncthreads(); // the previous item is done with the ring and both weight buffers
-        if (TW && t == 0) issue(j0);
+        if (TW && warp == 0) issue(j0);
         // ring rows j0-KRV .. j0+KRV (zero outside the grid)
         for (int jr = j0 - KRV; jr <= j0 + KRV; ++jr) {
 #pragma unroll
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 
         for (int j = j0; j < j1; ++j) {
             // the next row's weights (its buffer was last read in row j-1, before the barrier)
-            if (TW && t == 0 && j + 1 < j1) issue(j + 1);
+            if (TW && warp == 0 && j + 1 < j1) issue(j + 1);
             // prefetch: the ring's next row and this row's accumulator
             const int jn = j + KRV + 1;
             double nxt[K][XPT], sacc[K][XPT];
