@@ -35,6 +35,7 @@ constexpr int kEmCl = 8;
 
 struct EmXmArgs {
     const double* rowf; // [9][nv] row values of the x-invariant fields
+    const double* colf; // [9][nx] column values of the v-invariant (x-dependent) fields, 1/2 applied to g
     double st[5];
     double dt;
     const double* values; // [M][vstride] Brownian prefix values
@@ -231,7 +232,9 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_kernel(EmXmArgs a) {
 // columns a warp reads from its neighbour segments (x0-1, x0+LX) are preloaded before a CTA
 // barrier; the halo rows from the neighbour CTAs are double-buffered by step parity (two
 // slot sets per side: row -1 at index 1 / 0, row RPC at RPC+2 / RPC+3).
-template <int NX, int RPC, int NT, int P, int MASK, int CL, int NP, bool NZ>
+// XD: fields that depend on x only (v-invariant; e.g. a(x), sigma(x) of the variable Langevin
+// family): lane = row, so a warp's 32 lanes read the same column value (one L1 broadcast).
+template <int NX, int RPC, int NT, int P, int MASK, int CL, int NP, bool NZ, int XD = 0>
 __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
     static_assert((MASK & 16) == 0, "in-place E-M: no mixed derivative");
     constexpr int TRI = RPC + 4;
@@ -370,7 +373,10 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
                         const double dvu = (uvp - uvm) * st2;
                         double drift = 0.0; // (NZ: the first present term starts the fold, see em_first)
                         if (MASK & 1) drift = EM_ADD(1, drift, fh * uc);
-                        if (MASK & 2) drift = EM_ADD(2, drift, ffx * dxu);
+                        if (MASK & 2) {
+                            const double fx = (XD & 2) ? __ldg(a.colf + 1 * NX + x0 + c) : ffx;
+                            drift = EM_ADD(2, drift, fx * dxu);
+                        }
                         if (MASK & 4) drift = EM_ADD(4, drift, ffv * dvu);
                         if (MASK & 8) {
                             const double dxxu = (uxp - 2.0 * uc + uxm) * st1;
@@ -378,12 +384,16 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
                         }
                         if (MASK & 32) {
                             const double dvvu = (uvp - 2.0 * uc + uvm) * st3;
-                            drift = EM_ADD(32, drift, hgvv * dvvu);
+                            const double g = (XD & 32) ? __ldg(a.colf + 5 * NX + x0 + c) : hgvv;
+                            drift = EM_ADD(32, drift, g * dvvu);
                         }
                         double noise = 0.0;
                         if (MASK & 64) noise = EM_ADD(64, noise, fsig * uc);
                         if (MASK & 128) noise = EM_ADD(128, noise, fsx * dxu);
-                        if (MASK & 256) noise = EM_ADD(256, noise, fsv * dvu);
+                        if (MASK & 256) {
+                            const double sv = (XD & 256) ? __ldg(a.colf + 8 * NX + x0 + c) : fsv;
+                            noise = EM_ADD(256, noise, sv * dvu);
+                        }
                         const double next = uc + drift * dt + noise * dW[pi];
                         own[c * TRI] = next;
                         if (do_rem) rout[c * TRI] = next;
@@ -409,10 +419,10 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
     }
 }
 
-template <int MASK, int NX, int CL, int NP, bool NZ>
+template <int MASK, int NX, int CL, int NP, bool NZ, int XD = 0>
 void launch_em_ip(s2b_context* ctx, const EmXmArgs& a) {
     constexpr int RPC = 32, NT = 256, P = 4;
-    auto kern = em_cluster_ip_kernel<NX, RPC, NT, P, MASK, CL, NP, NZ>;
+    auto kern = em_cluster_ip_kernel<NX, RPC, NT, P, MASK, CL, NP, NZ, XD>;
     const size_t smem = 8 * static_cast<size_t>(NP) * (NX + 2) * (RPC + 4);
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -481,8 +491,12 @@ bool em_multi_path() {
 bool em_cluster_supported(const s2b_fields* f) {
     const char* e = std::getenv("S2B_EMXM");
     if (e && e[0] == '0') return false;
-    return f->xinv && ((f->nx == 256 && f->nv == 256) || (f->nx == 512 && f->nv == 512)) &&
-           f->mask == (2 | 32 | 256);
+    if (!((f->nx == 256 && f->nv == 256) || (f->nx == 512 && f->nv == 512)) || f->mask != (2 | 32 | 256))
+        return false;
+    if (f->xinv) return true;
+    // separable fields (each x- or v-invariant): the in-place kernels take x-dependent gvv / sigv
+    // (and fx) from a column table; the double-buffered one-path kernel only row values
+    return f->sep && f->xdep == (32 | 256) && (f->nx == 512 || em_multi_path());
 }
 
 void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const double* d_phi,
@@ -498,6 +512,7 @@ void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const do
     S2B_CUDA(cudaMemcpyAsync(drec.p, d_rec, rec_k.size() * sizeof(double*), cudaMemcpyHostToDevice, ctx->stream));
     EmXmArgs a{};
     a.rowf = f->d_rowf.p;
+    a.colf = f->d_colf.p;
     std::copy(f->st, f->st + 5, a.st);
     a.dt = dt;
     a.values = paths->d_values.p;
@@ -512,8 +527,18 @@ void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const do
     a.M = M;
     a.nv = static_cast<int>(f->nv);
     a.work = work.p;
-    constexpr int LC = 2 | 32 | 256; // the constant Langevin fields
-    if (no_neg_zero) {
+    constexpr int LC = 2 | 32 | 256; // the Langevin fields
+    const int xd = f->xinv ? 0 : f->xdep;
+    if (xd == (32 | 256)) { // the variable Langevin family: a(x), sigma(x)
+        constexpr int XV = 32 | 256;
+        if (no_neg_zero) {
+            if (f->nx == 512) launch_em_ip<LC, 512, 16, 1, true, XV>(ctx, a);
+            else launch_em_ip<LC, 256, 8, S2B_EM_NP, true, XV>(ctx, a);
+        } else {
+            if (f->nx == 512) launch_em_ip<LC, 512, 16, 1, false, XV>(ctx, a);
+            else launch_em_ip<LC, 256, 8, S2B_EM_NP, false, XV>(ctx, a);
+        }
+    } else if (no_neg_zero) {
         if (f->nx == 512) launch_em_ip<LC, 512, 16, 1, true>(ctx, a);
         else if (em_multi_path()) launch_em_ip<LC, 256, 8, S2B_EM_NP, true>(ctx, a);
         else launch_em<LC, true>(ctx, a);

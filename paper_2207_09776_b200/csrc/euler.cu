@@ -268,6 +268,35 @@ s2b_fields* make_fields(s2b_context* ctx, const s2b_grid* grid, const double* co
         f->d_rowf.alloc(9 * nv);
         S2B_CUDA(cudaMemcpy(f->d_rowf.p, rowf.data(), rowf.size() * sizeof(double), cudaMemcpyHostToDevice));
     }
+    // separable fields: x-dependent ones must be v-invariant; rows of the others feed d_rowf
+    {
+        f->sep = true;
+        f->xdep = 0;
+        std::vector<double> colf(9 * nx, 0.0), rowf2(9 * nv, 0.0);
+        for (int k = 0; k < 9 && f->sep; ++k) {
+            if (!(f->mask >> k & 1)) continue;
+            const double* F = fields9[k];
+            bool xi = true, vi = true;
+            for (size_t j = 0; j < nv && xi; ++j)
+                for (size_t i = 1; i < nx; ++i)
+                    if (std::memcmp(&F[j * nx + i], &F[j * nx], sizeof(double)) != 0) {
+                        xi = false;
+                        break;
+                    }
+            for (size_t j = 1; j < nv && vi; ++j)
+                if (std::memcmp(&F[j * nx], &F[0], nx * sizeof(double)) != 0) vi = false;
+            if (!xi && !vi) f->sep = false;
+            if (!xi) f->xdep |= 1 << k;
+            for (size_t i = 0; i < nx; ++i) colf[k * nx + i] = (k == 3 || k == 5) ? 0.5 * F[i] : F[i];
+            for (size_t j = 0; j < nv; ++j) rowf2[k * nv + j] = F[j * nx];
+        }
+        if (f->sep && !f->xinv) {
+            f->d_colf.alloc(9 * nx);
+            S2B_CUDA(cudaMemcpy(f->d_colf.p, colf.data(), colf.size() * sizeof(double), cudaMemcpyHostToDevice));
+            f->d_rowf.alloc(9 * nv); // x-invariant fields' row values (x-dependent rows unused)
+            S2B_CUDA(cudaMemcpy(f->d_rowf.p, rowf2.data(), rowf2.size() * sizeof(double), cudaMemcpyHostToDevice));
+        }
+    }
     // EulerStencils::from_grid (euler.cpp:18-26)
     const double dx = (grid->bx - grid->ax) / static_cast<double>(nx + 1);
     const double dv = (grid->bv - grid->av) / static_cast<double>(nv + 1);

@@ -111,6 +111,11 @@ struct s2b_fields {
     s2b_grid grid{};
     bool xinv = false;          // every non-zero field constant along x (bitwise)
     s2b::DevBuf<double> d_rowf; // [9][nv] row values when xinv
+    // separable: every non-zero field is x-invariant or v-invariant (bitwise); xdep = the
+    // fields that depend on x, given per column in d_colf [9][nx] (g^xx, g^vv pre-halved)
+    bool sep = false;
+    int xdep = 0;
+    s2b::DevBuf<double> d_colf;
 };
 
 struct s2b_paths {

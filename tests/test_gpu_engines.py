@@ -79,15 +79,17 @@ def em_engine(request, monkeypatch):
 
 @pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
 @pytest.mark.parametrize("d", [256, 512])
-def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine, d):
-    """solve_euler at 256^2 / 512^2 (constant Langevin: the cluster-resident kernels, in place
-    at 512^2) vs the reference, with a mid-run record."""
-    T, dt_leb, dt, M, seed = 0.01, 1e-4, 1e-4, 3, 21
-    ops = ref.Ops("langevin-constant", d, order=1)
+@pytest.mark.parametrize("family", ["langevin-constant", "langevin-variable"])
+def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine, d, family):
+    """solve_euler at 256^2 / 512^2 (Langevin: the cluster-resident kernels, in place; the
+    variable family's a(x), sigma(x) from a column table) vs the reference, with a mid-run
+    record."""
+    T, dt_leb, dt, M, seed = 0.01, 1e-4, 1e-4, 4, 21
+    ops = ref.Ops(family, d, order=1)
     values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
     want, wst, _ = ops.solve_euler(values, dt_leb, T, dt, record_times=[0.005], seed=seed)
     g = s2b.GridSpec.square(d)
-    f = s2b.Fields.from_family(g, "langevin-constant", ctx=ctx)
+    f = s2b.Fields.from_family(g, family, ctx=ctx)
     paths = s2b.BrownianPaths.from_values(values, dt_leb, seed=seed, ctx=ctx)
     ens = s2b.solve_euler(s2b.EulerConfig(dt=dt, record_times=[0.005]), f, g, ops.datum(), paths, T)
     assert len(ens) == len(want)
