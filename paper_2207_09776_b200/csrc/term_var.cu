@@ -257,6 +257,196 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     }
 }
 
+// x-split variant of the TMA-weight kernel: a work item is (K paths, strip, x-part of NT
+// columns), one point per thread, so a CTA's two weight rows and its ring are small enough for
+// two CTAs per SM -- one CTA's per-row barrier and weight wait hide behind the other's math.
+// The ring (RING = 2*KRV+2 rows, slot = row mod RING) holds the part's columns plus KRX halo
+// columns on each side (the neighbour part's values, zero outside the grid).
+template <int K, uint64_t MASK, uint64_t PCNT, uint64_t PS0, uint64_t PS1, int KRX, int KRV, int NT>
+__global__ void __launch_bounds__(NT, 2) term_varx_kernel(TermArgs a, int strips, int gfast) {
+    constexpr int RING = 2 * KRV + 2;
+    constexpr int NB = MaskInfo<MASK>::count();
+    constexpr int NP = Pc<PCNT>::off(NB);
+    constexpr int RWS = NT + 2 * KRX; // ring row stride
+    const int nx = a.op.nx, nv = a.op.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+    const int parts = (nx + NT - 1) / NT;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+    extern __shared__ __align__(128) double vsm[];
+    double* wbuf = vsm;                               // [2][NP][NT] weights of rows j, j+1 (this part)
+    double* ring = wbuf + 2 * static_cast<size_t>(NP) * NT; // [K][RING][RWS]
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ unsigned long long red[K][2][NT / 32];
+
+    for (int q = t; q < K * RING * RWS; q += NT) ring[q] = 0.0;
+    if (t == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t ph = 0;
+    int xlo = 0, wpart = NT; // current part: first column, width in the grid
+    auto issue = [&](int jw) {
+        double* dst = wbuf + static_cast<size_t>(jw & 1) * NP * NT;
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * wpart * 8));
+        }
+        __syncwarp();
+        for (int q = lane; q < NP; q += 32)
+            tma_row(dst + static_cast<size_t>(q) * NT,
+                    a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx + xlo,
+                    static_cast<uint32_t>(wpart * 8), &bar[jw & 1]);
+    };
+    auto slot = [](int jr) { return ((jr % RING) + RING) % RING; };
+
+    const int live = a.cnt[0];
+    const int groups = (live + K - 1) / K;
+    const long long items = static_cast<long long>(groups) * strips * parts;
+    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        // gfast (weights beyond L2): path groups fastest, so resident CTAs share a strip's weights
+        const long long pg = static_cast<long long>(parts) * groups;
+        const int part = gfast ? static_cast<int>((it / groups) % parts) : static_cast<int>(it % parts);
+        const int strip = gfast ? static_cast<int>(it / pg) : static_cast<int>((it / parts) % strips);
+        const int g = gfast ? static_cast<int>(it % groups) : static_cast<int>(it / (static_cast<long long>(parts) * strips));
+        const int j0 = strip * kVarRows, j1 = min(nv, j0 + kVarRows);
+        xlo = part * NT;
+        wpart = min(NT, nx - xlo);
+        const int i = xlo + t;          // this thread's column
+        const bool act = t < wpart;
+        // halo column of this thread (t < 2*KRX): left xlo-KRX+t, right xlo+wpart+(t-KRX)
+        const int hi_col = t < KRX ? xlo - KRX + t : xlo + wpart + (t - KRX);
+        const int hi_loc = t < KRX ? t : KRX + wpart + (t - KRX);
+        const bool has_h = t < 2 * KRX;
+        const bool h_in = has_h && hi_col >= 0 && hi_col < nx;
+        int pk[K];
+        const double* in[K];
+        const double* Sin[K];
+        double* Tout[K];
+        double* Sout[K];
+        double inv[K];
+        double c[K][6];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            pk[k] = g * K + k < live ? a.act[g * K + k] : -1;
+            const int p = pk[k] >= 0 ? pk[k] : a.act[g * K];
+            const int kk = a.k[p], par = a.par[p];
+            inv[k] = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
+            Sin[k] = (par ? a.S1 : a.S0) + static_cast<size_t>(p) * n;
+            in[k] = kk == 1 ? Sin[k] : (par ? a.T1 : a.T0) + static_cast<size_t>(p) * n;
+            Tout[k] = (par ? a.T0 : a.T1) + static_cast<size_t>(p) * n;
+            Sout[k] = (par ? a.S0 : a.S1) + static_cast<size_t>(p) * n;
+            const double* cp = a.ctab + (static_cast<size_t>(p) * a.nwin + a.win[p]) * 6;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) c[k][q] = pk[k] >= 0 ? cp[q] : 0.0;
+        }
+        __syncthreads(); // the previous item is done with the ring and both weight buffers
+        if (warp == 0) issue(j0);
+        auto fill = [&](int k, int jr, double v_own, double v_h) {
+            double* dst = ring + (static_cast<size_t>(k) * RING + slot(jr)) * RWS;
+            if (act) dst[KRX + t] = v_own;
+            if (has_h) dst[hi_loc] = v_h;
+            if (!act && t < NT) dst[KRX + t] = 0.0; // columns past the grid's edge
+        };
+        auto ldv = [&](int k, int jr, int col, bool ok) -> double {
+            return (ok && jr >= 0 && jr < nv && pk[k] >= 0) ? in[k][static_cast<size_t>(jr) * nx + col] : 0.0;
+        };
+        for (int jr = j0 - KRV; jr <= j0 + KRV; ++jr)
+#pragma unroll
+            for (int k = 0; k < K; ++k) fill(k, jr, ldv(k, jr, i, act), ldv(k, jr, hi_col, h_in));
+        __syncthreads();
+
+        unsigned long long tb[K], sb[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) tb[k] = sb[k] = 0;
+
+        for (int j = j0; j < j1; ++j) {
+            if (warp == 0 && j + 1 < j1) issue(j + 1);
+            const int jn = j + KRV + 1;
+            double nxt[K], nxh[K], sacc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                nxt[k] = ldv(k, jn, i, act);
+                nxh[k] = ldv(k, jn, hi_col, h_in);
+                sacc[k] = (act && pk[k] >= 0) ? Sin[k][static_cast<size_t>(j) * nx + i] : 0.0;
+            }
+            int sl[2 * KRV + 1];
+#pragma unroll
+            for (int d = 0; d <= 2 * KRV; ++d) sl[d] = slot(j - KRV + d);
+            mbar_wait(&bar[j & 1], (ph >> (j & 1)) & 1u);
+            ph ^= 1u << (j & 1);
+            const double* wr = wbuf + static_cast<size_t>(j & 1) * NP * NT;
+            if (act) {
+                const size_t r = static_cast<size_t>(j) * nx + i;
+                double acc[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) acc[k] = 0.0;
+                static_for<NB>([&](auto E) {
+                    constexpr int e = decltype(E)::value;
+                    constexpr int b = MaskInfo<MASK>::bit_of(e);
+                    constexpr int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
+                    constexpr int q0 = Pc<PCNT>::off(e);
+                    double y[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) y[k] = 0.0;
+                    static_for<Pc<PCNT>::cnt(e)>([&](auto C) {
+                        constexpr int q = q0 + decltype(C)::value;
+                        constexpr int ps = Ps<PS0, PS1>::slot(q);
+                        const double w = wr[q * NT + t];
+#pragma unroll
+                        for (int k = 0; k < K; ++k) y[k] += c[k][ps] * w;
+                    });
+                    const int rs = sl[dv + KRV];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const double x = ring[(static_cast<size_t>(k) * RING + rs) * RWS + KRX + t + dx];
+                        acc[k] += y[k] * x;
+                    }
+                });
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (pk[k] < 0) continue;
+                    const double tv = acc[k] * inv[k];
+                    const double sv = sacc[k] + tv;
+                    Tout[k][r] = tv;
+                    Sout[k][r] = sv;
+                    tb[k] = umax64(tb[k], abs_bits(tv));
+                    sb[k] = umax64(sb[k], abs_bits(sv));
+                }
+            }
+            // row jn replaces row jn - RING (= j - KRV - 1, out of this row's window): every
+            // thread is past its reads of that slot only after the barrier of row j - 1
+#pragma unroll
+            for (int k = 0; k < K; ++k) fill(k, jn, nxt[k], nxh[k]);
+            __syncthreads();
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const unsigned long long wt = warp_umax(tb[k]), ws = warp_umax(sb[k]);
+            if (lane == 0) {
+                red[k][0][warp] = wt;
+                red[k][1][warp] = ws;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                unsigned long long t2 = lane < NT / 32 ? red[k][0][lane] : 0ULL;
+                unsigned long long s2 = lane < NT / 32 ? red[k][1][lane] : 0ULL;
+                t2 = warp_umax(t2);
+                s2 = warp_umax(s2);
+                if (lane == 0 && pk[k] >= 0) {
+                    if (t2) atomicMax(&a.tn[pk[k]], t2);
+                    if (s2) atomicMax(&a.sn[pk[k]], s2);
+                }
+            }
+        }
+    }
+}
+
 constexpr uint64_t pcnt_of(std::initializer_list<int> c) {
     uint64_t v = 0;
     int e = 0;
@@ -320,11 +510,32 @@ int fam_of(const s2b_operator* op) {
     return -1;
 }
 
+constexpr int kVarxNT = 128; // columns (threads) per CTA of the x-split kernel
+
 template <int K, VarFam F, int KRX, int KRV>
 void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     constexpr int NP = Pc<F.pc>::off(MaskInfo<F.mask>::count());
     const int nx = a.op.nx, nv = a.op.nv;
     const int strips = (nv + kVarRows - 1) / kVarRows;
+    // wide grids: the x-split TMA kernel (measured 2.04e8 vs 1.71e8 windows/s at 1024^2); up to
+    // 256 columns the full-row kernel is ahead (1.65e8 vs 1.56e8 at cfg3).  S2B_VARX=0/1 forces.
+    const char* ev = std::getenv("S2B_VARX");
+    const bool varx = ev ? ev[0] != '0' : nx > kVarNT;
+    if (varx) {
+        // x-split TMA kernel, 4 paths per item, two CTAs per SM
+        constexpr int NT = kVarxNT;
+        auto kern = term_varx_kernel<4, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, NT>;
+        const size_t smem = (2 * static_cast<size_t>(NP) * NT + 4 * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
+        S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+        const size_t parts = (nx + NT - 1) / NT;
+        const size_t items = (live_max + 3) / 4 * static_cast<size_t>(strips) * parts;
+        const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
+        const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
+        kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
+        return;
+    }
     const bool tw = nx <= kVarNT;
     const size_t smem = ((tw ? 2 * static_cast<size_t>(NP) * nx : 0) + static_cast<size_t>(K) * kRing * (nx + 2 * KRX)) * 8;
     auto go = [&](auto kern) {
