@@ -8,7 +8,12 @@ form (exact_reference, the reference's own error measure, analysis.cpp:99-127) a
 time of each solve call (synchronous; per path = total / M like the reference's
 time_per_sim_s), then reads the speed-up off the log-log interpolated curves.
 
-usage: python scripts/time_to_error.py [--d 512] [--paths 128] [--out FILE]
+For the variable-coefficient family (cfg3, no closed form) the reference is the reference's
+own choice (build_reference, experiment.cpp:379-397): a finest-dt E-M run on the same paths
+(--ref-dt, default dt_leb), and Err is measured against it.
+
+usage: python scripts/time_to_error.py [--d 512] [--paths 128] [--family langevin-variable]
+                                       [--ref-dt 1e-5] [--out FILE]
 """
 import argparse
 import json
@@ -46,16 +51,28 @@ def main():
     ap.add_argument("--seed", type=int, default=424242)
     ap.add_argument("--magnus-dt", default="0.05,0.02,0.01,0.005,0.0025")
     ap.add_argument("--euler-dt", default="1e-4,5e-5,2e-5,1e-5")
+    ap.add_argument("--family", default="langevin-constant", choices=["langevin-constant", "langevin-variable"])
+    ap.add_argument("--ref-dt", type=float, default=None, help="E-M reference dt (variable family)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "time_to_error.json"))
     args = ap.parse_args()
+    fam = args.family
 
     a, sigma = 1.1, 1.0 / math.sqrt(10.0)
     g = s2b.GridSpec.square(args.d)
     ctx = s2b.default_context()
     t0 = time.perf_counter()
     paths = s2b.BrownianPaths.philox(args.T, args.dt_leb, args.paths, seed=args.seed, ctx=ctx)
-    ref = s2b.exact_reference(g, args.T, a, sigma, paths, ctx=ctx)
     phi = s2b.gaussian_datum(g)
+    fields = s2b.Fields.from_family(g, fam, a=a, sigma=sigma, ctx=ctx)
+    if fam == "langevin-constant":
+        ref = s2b.exact_reference(g, args.T, a, sigma, paths, ctx=ctx)
+        ref_desc = "exact_reference (closed form)"
+    else:
+        rdt = args.ref_dt or args.dt_leb
+        ref = s2b.solve_euler(s2b.EulerConfig(dt=rdt), fields, g, phi, paths, args.T)[-1]
+        if ref.blowup_count():
+            raise SystemExit("reference E-M run blew up (experiment.cpp:391-397)")
+        ref_desc = f"finest-dt E-M run, dt={rdt} (build_reference, experiment.cpp:379-397)"
     setup_s = time.perf_counter() - t0
     rows = []
 
@@ -72,12 +89,11 @@ def main():
         print(json.dumps(row), flush=True)
 
     for order in (2, 3):
-        op = s2b.Operator.from_family(g, "langevin-constant", a=a, sigma=sigma, order=order, ctx=ctx)
+        op = s2b.Operator.from_family(g, fam, a=a, sigma=sigma, order=order, ctx=ctx)
         for dt in [float(x) for x in args.magnus_dt.split(",")]:
             record("magnus", order, dt, lambda: s2b.solve_iterated_magnus(
                 s2b.MagnusConfig(order=order, dt=dt), op, phi, paths, args.T, g))
         del op
-    fields = s2b.Fields.from_family(g, "langevin-constant", a=a, sigma=sigma, ctx=ctx)
     for dt in [float(x) for x in args.euler_dt.split(",")]:
         record("euler", 0, dt, lambda: s2b.solve_euler(s2b.EulerConfig(dt=dt), fields, g, phi, paths, args.T))
 
@@ -101,8 +117,8 @@ def main():
                     speedups.append({"order": order, "err": e, "euler_s_at_worse_err": best_t,
                                      "euler_err": best_e, "magnus_s": t, "speedup_lower_bound": best_t / t})
     out = {"config": {"d": args.d, "paths": args.paths, "T": args.T, "dt_leb": args.dt_leb,
-                      "seed": args.seed, "family": "langevin-constant", "a": a, "sigma": sigma,
-                      "error": "mean_rel_error vs exact_reference at T (Frobenius, all paths)",
+                      "seed": args.seed, "family": fam, "a": a, "sigma": sigma,
+                      "error": f"mean_rel_error vs {ref_desc} at T (Frobenius, all paths)",
                       "timing": "wall time of each synchronous solve call on one B200"},
            "setup_s": setup_s, "runs": rows, "speedups": speedups,
            "gpu": os.popen("nvidia-smi --query-gpu=name,clocks.sm --format=csv,noheader").read().strip()}
