@@ -127,7 +127,7 @@ __device__ __forceinline__ double em_point(int mask, const double* fv, const dou
 // read the one value across the warp boundary from L1).  The P paths share every field load.
 // Items are ordered strip-fastest so neighbouring CTAs share halo rows in L2.
 template <int P, int D, int MASK, bool XINV>
-__global__ void __launch_bounds__(512) em_rows_kernel(EmArgs a, int R, int strips, int items) {
+__global__ void __launch_bounds__(512, P == 1 ? 2 : 1) em_rows_kernel(EmArgs a, int R, int strips, int items) {
     const int nx = a.nx, nv = a.nv;
     const size_t n = static_cast<size_t>(nx) * nv;
     const int t = threadIdx.x, lane = t & 31;
@@ -360,20 +360,30 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         const unsigned gx = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64));
         // the row-marching kernel: even nx up to 1024 points, no g^xv (S2B_EMROWS=0: the old one)
 #ifndef S2B_EM_D
-#define S2B_EM_D 4
+#define S2B_EM_D 2
 #endif
-        constexpr int kP = 2, kR = 32, kD = S2B_EM_D; // paths per item, rows per strip, rows in flight
+        // paths per item, rows per strip, rows in flight: one path per item and two CTAs per SM
+        // (64 registers) measured 0.745 of HBM at 1024^2 vs 0.56 for 2 paths x 4 rows (ncu)
+        constexpr int kP = 2, kR = 32, kD = S2B_EM_D;
         const char* er = std::getenv("S2B_EMROWS");
         const bool rows = !(f->mask & 16) && f->nx % 2 == 0 && f->nx <= 1024 && !(er && er[0] == '0');
         const int nt = static_cast<int>(((f->nx / 2 + 31) / 32) * 32);
         const int strips = static_cast<int>((f->nv + kR - 1) / kR);
-        const size_t items_sz = ((M + kP - 1) / kP) * static_cast<size_t>(strips);
+        const char* ep0 = std::getenv("S2B_EM_P");
+        const int pit0 = ep0 && std::atoi(ep0) == 2 ? kP : 1;
+        const size_t items_sz = ((M + pit0 - 1) / pit0) * static_cast<size_t>(strips);
         if (items_sz > static_cast<size_t>(INT_MAX)) fail(S2B_ERR_CONFIG, "solve_euler: too many paths");
         const int items = static_cast<int>(items_sz);
         a.rowf = f->d_rowf.p;
         using RowsFn = void (*)(EmArgs, int, int, int);
+        const char* ep = std::getenv("S2B_EM_P"); // paths per item (A/B runs): 1 (default) or 2
+        const int psel = ep ? std::atoi(ep) : 1;
         auto pick = [&](auto dtag) -> RowsFn {
             constexpr int D = decltype(dtag)::value;
+            if (psel == 1)
+                return f->mask == (2 | 32 | 256) ? (f->xinv ? em_rows_kernel<1, D, 2 | 32 | 256, true>
+                                                            : em_rows_kernel<1, D, 2 | 32 | 256, false>)
+                                                 : em_rows_kernel<1, D, -1, false>;
             return f->mask == (2 | 32 | 256) ? (f->xinv ? em_rows_kernel<kP, D, 2 | 32 | 256, true>
                                                         : em_rows_kernel<kP, D, 2 | 32 | 256, false>)
                                              : em_rows_kernel<kP, D, -1, false>;
@@ -383,6 +393,7 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         RowsFn rows_fn = dsel == 2 ? pick(std::integral_constant<int, 2>{})
                          : dsel == 6 ? pick(std::integral_constant<int, 6>{})
                                      : pick(std::integral_constant<int, kD>{});
+        const int pitem = psel == 1 ? 1 : kP;
         int rows_grid = 0;
         if (rows) {
             int per_sm = 0;
