@@ -100,12 +100,17 @@ def parse():
     return args
 
 
-# BASELINE.json configs as bench presets.  cfg5's 128k paths over 8 GPUs are 16384 per GPU, far
+# BASELINE.json configs as bench presets (cfg1: the reference's own CPU-runnable case; cfg4: the
+# north-star 512^2 grid, Magnus side of the time-to-accuracy comparison).  cfg5's 128k paths over 8 GPUs are 16384 per GPU, far
 # beyond one B200 at 1024^2 (4 state vectors x 8 MB per path): they run as independent waves of
 # 4096 resident paths (128 GB of state), and one timed step is one window of one wave — every
 # wave is the same work, so the wave's rate is the job's rate.  A full T = 1 is hours at 1024^2
 # (SURVEY 8(d)): the preset times a fixed handful of windows (dt = 5e-4, dt_leb = 1e-5).
 PRESETS = {
+    "cfg1": {"d": 64, "paths": 1000, "dt": 0.1, "dt_leb": 1e-4, "T": 1.0, "order": 2,
+             "family": "langevin-constant", "steps": 3, "warmup": 3},
+    "cfg4": {"d": 512, "paths": 4096, "dt": 0.005, "dt_leb": 1e-4, "T": 1.0, "order": 3,
+             "family": "langevin-constant"},
     "cfg2": {"d": 256, "paths": 16384, "dt": 0.01, "dt_leb": 1e-4, "T": 1.0, "order": 3,
              "family": "langevin-constant"},
     "cfg3": {"d": 256, "paths": 16384, "dt": 0.01, "dt_leb": 1e-4, "T": 1.0, "order": 3,
@@ -401,7 +406,7 @@ def run_ours(args):
                                f"T={args.T}, dt_leb={args.dt_leb}, tol=1e-10, theta=1",
                    "grid": args.d, "family": args.family, "paths_per_gpu": M, "order": args.order, "dt": args.dt,
                    "windows_per_step": 1, "parallelism": f"path-sharded x{world}",
-                   "l2": "inputs larger than L2 (34 GB resident state per GPU)"},
+                   "l2": f"inputs larger than L2 ({4 * M * n * 8 / 1e9:.3g} GB resident state per GPU vs 126 MB L2)"},
         "path_terms_per_window": terms / max(1, M * args.steps),
         "path_gridpoint_terms_per_s": world * n * terms / (ms_max / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
