@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "s2b_internal.cuh"
 
@@ -491,8 +492,9 @@ bool em_multi_path() {
 bool em_cluster_supported(const s2b_fields* f) {
     const char* e = std::getenv("S2B_EMXM");
     if (e && e[0] == '0') return false;
-    if (!((f->nx == 256 && f->nv == 256) || (f->nx == 512 && f->nv == 512)) || f->mask != (2 | 32 | 256))
-        return false;
+    const bool grid_ok = f->nx == f->nv && (f->nx == 64 || f->nx == 128 || f->nx == 256 || f->nx == 512);
+    if (!grid_ok || f->mask != (2 | 32 | 256)) return false;
+    if (f->nx < 256) return f->xinv || (f->sep && f->xdep == (32 | 256)); // in-place kernels only
     if (f->xinv) return true;
     // separable fields (each x- or v-invariant): the in-place kernels take x-dependent gvv / sigv
     // (and fx) from a column table; the double-buffered one-path kernel only row values
@@ -529,7 +531,21 @@ void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const do
     a.work = work.p;
     constexpr int LC = 2 | 32 | 256; // the Langevin fields
     const int xd = f->xinv ? 0 : f->xdep;
-    if (xd == (32 | 256)) { // the variable Langevin family: a(x), sigma(x)
+    // small grids: 2-CTA (64^2, 6 paths per cluster) / 4-CTA (128^2, 3 paths) in-place clusters
+    auto small = [&](auto nz_tag, auto xd_tag) {
+        constexpr bool NZ = decltype(nz_tag)::value;
+        constexpr int XD = decltype(xd_tag)::value;
+        if (f->nx == 64) launch_em_ip<LC, 64, 2, 6, NZ, XD>(ctx, a);
+        else launch_em_ip<LC, 128, 4, 3, NZ, XD>(ctx, a);
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    using X0 = std::integral_constant<int, 0>;
+    using XV_ = std::integral_constant<int, 32 | 256>;
+    if (f->nx < 256) {
+        if (xd == 0) no_neg_zero ? small(T_{}, X0{}) : small(F_{}, X0{});
+        else no_neg_zero ? small(T_{}, XV_{}) : small(F_{}, XV_{});
+    } else if (xd == (32 | 256)) { // the variable Langevin family: a(x), sigma(x)
         constexpr int XV = 32 | 256;
         if (no_neg_zero) {
             if (f->nx == 512) launch_em_ip<LC, 512, 16, 1, true, XV>(ctx, a);

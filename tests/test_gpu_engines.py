@@ -78,7 +78,7 @@ def em_engine(request, monkeypatch):
 
 
 @pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
-@pytest.mark.parametrize("d", [256, 512])
+@pytest.mark.parametrize("d", [64, 128, 256, 512])
 @pytest.mark.parametrize("family", ["langevin-constant", "langevin-variable"])
 def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine, d, family):
     """solve_euler at 256^2 / 512^2 (Langevin: the cluster-resident kernels, in place; the
@@ -99,7 +99,7 @@ def test_euler_engines_bitwise_256(ref, s2b, ctx, em_engine, d, family):
 
 
 @pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
-@pytest.mark.parametrize("d", [256, 512])
+@pytest.mark.parametrize("d", [64, 256, 512])
 def test_euler_engines_blowup_256(ref, s2b, ctx, em_engine, d):
     """dt far beyond the stability bound: Ok (finite, huge) at t = 20, blown by T = 200."""
     T, M, seed = 200.0, 2, 9
