@@ -17,6 +17,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "magnus_common.cuh"  // mbarrier / TMA helpers
 #include "s2b_internal.cuh"
 
 namespace s2b {
@@ -33,6 +34,7 @@ struct EmArgs {
     const double* values;
     size_t vstride; // steps + 1
     size_t k0, k1;  // Lebesgue indices: dW = values[k1] - values[k0]
+    size_t k2;      // two-step kernel: the second step's dW = values[k2] - values[k1]
     const double* in;
     double* out;
     int* blown;
@@ -220,6 +222,131 @@ __global__ void __launch_bounds__(512, P == 1 ? 2 : 1) em_rows_kernel(EmArgs a, 
     }
 }
 
+// Temporally blocked streaming step: TWO explicit steps per pass, u0 -> u1 -> u2, with u1
+// never leaving the SM.  A work item is (path, strip of kTbRows output rows); rows of u0 stream
+// through a TMA ring (kTbStages deep, zero x-halo), each u1 row is computed into a 4-row
+// shared ring as soon as its three u0 rows are in, each u2 row as soon as its three u1 rows
+// are, one CTA barrier per row.  HBM traffic per path*point*2 steps: read u0 + write u2
+// (+ the 4 halo rows per strip) instead of 2 x (read + write).  The per-point arithmetic is
+// em_point (the reference's); rows outside the grid are zero at every step, as in
+// euler_step_into.  A blow-up (infinite |u|) in either step flags the path; the host only
+// pairs steps whose intermediate state is not a record, so statuses and records are those of
+// two single steps.
+constexpr int kTbStages = 8;
+constexpr int kTbRows = 32;
+
+template <int MASK, bool XINV>
+__global__ void __launch_bounds__(512, 2) em_tb_kernel(EmArgs a, int strips, int items) {
+    const int nx = a.nx, nv = a.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+    const int t = threadIdx.x;
+    const int x0 = 2 * t;
+    const bool act = x0 < nx;
+    const int mask = MASK >= 0 ? MASK : a.mask;
+    const int RW = nx + 4; // row stride: 2 zero doubles on each side (16-byte aligned data)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    double* u0 = reinterpret_cast<double*>(smem_raw + 128); // [kTbStages][RW]
+    double* u1 = u0 + kTbStages * RW;                      // [4][RW]
+    for (int q = t; q < (kTbStages + 4) * RW; q += blockDim.x) u0[q] = 0.0;
+    if (t == 0) {
+        for (int s = 0; s < kTbStages; ++s) mg::mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int LA = kTbStages - 2; // rows issued ahead (slot of row r-2 is free after row r's barrier)
+    const double inf = __longlong_as_double(0x7FF0000000000000LL);
+    uint32_t g = 0; // running row counter (mbarrier phases)
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int m = item / strips;
+        if (a.blown[m]) continue; // the reference stops a blown path (euler.cpp:159-162)
+        const int j0 = (item - m * strips) * kTbRows, j1 = min(nv, j0 + kTbRows);
+        const double* u = a.in + static_cast<size_t>(m) * n;
+        double* o = a.out + static_cast<size_t>(m) * n;
+        const double* pv = a.values + static_cast<size_t>(m) * a.vstride;
+        const double dW1 = pv[a.k1] - pv[a.k0], dW2 = pv[a.k2] - pv[a.k1];
+        const int NR = (j1 - j0) + 4; // u0 rows j0-2 .. j1+1
+        auto issue = [&](int s) {
+            const uint32_t gs = g + s, slot = gs % kTbStages;
+            const int r = j0 - 2 + s;
+            if (r >= 0 && r < nv) {
+                mg::mbar_expect_tx(&full[slot], static_cast<uint32_t>(nx * 8));
+                mg::tma_row(u0 + slot * RW + 2, u + static_cast<size_t>(r) * nx, static_cast<uint32_t>(nx * 8), &full[slot]);
+            } else {
+                mg::mbar_arrive(&full[slot]);
+            }
+        };
+        if (t == 0)
+            for (int s = 0; s < LA && s < NR; ++s) issue(s);
+        bool inf_seen = false;
+        for (int s = 0; s < NR; ++s) {
+            const uint32_t gs = g + s;
+            mg::mbar_wait(&full[gs % kTbStages], (gs / kTbStages) & 1);
+            const int r = j0 - 2 + s;
+            const int q = r - 1; // u1 row of this step
+            if (s >= 2 && q >= 0 && q < nv && act) {
+                const double* A = u0 + ((gs - 1) % kTbStages) * RW + 2;       // row q
+                const double* B = u0 + ((gs - 2) % kTbStages) * RW + 2;       // row q-1
+                const double* C = u0 + (gs % kTbStages) * RW + 2;             // row q+1
+                const double2 c2 = *reinterpret_cast<const double2*>(A + x0);
+                const double2 b2 = q - 1 >= 0 ? *reinterpret_cast<const double2*>(B + x0) : make_double2(0.0, 0.0);
+                const double2 d2 = q + 1 < nv ? *reinterpret_cast<const double2*>(C + x0) : make_double2(0.0, 0.0);
+                const double lft = A[x0 - 1], rgt = A[x0 + 2];
+                double fa[9], fb[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    fa[k] = fb[k] = 0.0;
+                    if (k != 4 && (mask >> k & 1)) {
+                        if (XINV) {
+                            fa[k] = fb[k] = __ldg(a.rowf + k * nv + q);
+                        } else {
+                            const double2 fk = __ldg(reinterpret_cast<const double2*>(a.f + k * n + static_cast<size_t>(q) * nx + x0));
+                            fa[k] = fk.x;
+                            fb[k] = fk.y;
+                        }
+                    }
+                }
+                const double na = em_point(mask, fa, a.st, a.dt, dW1, c2.x, lft, c2.y, b2.x, d2.x);
+                const double nb = em_point(mask, fb, a.st, a.dt, dW1, c2.y, c2.x, rgt, b2.y, d2.y);
+                *reinterpret_cast<double2*>(u1 + (q & 3) * RW + 2 + x0) = make_double2(na, nb);
+                inf_seen |= (fabs(na) == inf) | (fabs(nb) == inf);
+            }
+            __syncthreads(); // u1 row q visible; every thread is done with u0 row r-2
+            if (t == 0 && s + LA < NR) issue(s + LA);
+            const int p = r - 2; // u2 row of this step
+            if (p >= j0 && p < j1 && act) {
+                const double* A = u1 + (p & 3) * RW + 2;
+                const double* B = u1 + ((p - 1) & 3) * RW + 2;
+                const double* C = u1 + ((p + 1) & 3) * RW + 2;
+                const double2 c2 = *reinterpret_cast<const double2*>(A + x0);
+                const double2 b2 = p - 1 >= 0 ? *reinterpret_cast<const double2*>(B + x0) : make_double2(0.0, 0.0);
+                const double2 d2 = p + 1 < nv ? *reinterpret_cast<const double2*>(C + x0) : make_double2(0.0, 0.0);
+                const double lft = A[x0 - 1], rgt = A[x0 + 2];
+                double fa[9], fb[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    fa[k] = fb[k] = 0.0;
+                    if (k != 4 && (mask >> k & 1)) {
+                        if (XINV) {
+                            fa[k] = fb[k] = __ldg(a.rowf + k * nv + p);
+                        } else {
+                            const double2 fk = __ldg(reinterpret_cast<const double2*>(a.f + k * n + static_cast<size_t>(p) * nx + x0));
+                            fa[k] = fk.x;
+                            fb[k] = fk.y;
+                        }
+                    }
+                }
+                const double na = em_point(mask, fa, a.st, a.dt, dW2, c2.x, lft, c2.y, b2.x, d2.x);
+                const double nb = em_point(mask, fb, a.st, a.dt, dW2, c2.y, c2.x, rgt, b2.y, d2.y);
+                *reinterpret_cast<double2*>(o + static_cast<size_t>(p) * nx + x0) = make_double2(na, nb);
+                inf_seen |= (fabs(na) == inf) | (fabs(nb) == inf);
+            }
+        }
+        g += NR;
+        if (inf_seen) a.blown[m] = 1;
+    }
+}
+
 __global__ void em_record_status_kernel(const int* blown, uint8_t* status, size_t M) {
     const size_t m = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (m < M) status[m] = blown[m] ? 1 : 0;
@@ -400,15 +527,40 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
             S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fn, nt, 0));
             rows_grid = std::max(1, std::min(items, std::max(1, per_sm) * ctx->num_sms));
         }
+        // two steps per pass where the intermediate state is not a record (S2B_EMTB=0: never)
+        const char* etb = std::getenv("S2B_EMTB");
+        const bool tb = rows && !(etb && etb[0] == '0');
+        const int tb_strips = static_cast<int>((f->nv + kTbRows - 1) / kTbRows);
+        const size_t tb_items_sz = M * static_cast<size_t>(tb_strips);
+        if (tb && tb_items_sz > static_cast<size_t>(INT_MAX)) fail(S2B_ERR_CONFIG, "solve_euler: too many paths");
+        const int tb_items = static_cast<int>(tb_items_sz);
+        using TbFn = void (*)(EmArgs, int, int);
+        TbFn tb_fn = f->mask == (2 | 32 | 256) ? (f->xinv ? em_tb_kernel<2 | 32 | 256, true> : em_tb_kernel<2 | 32 | 256, false>)
+                                                 : em_tb_kernel<-1, false>;
+        const size_t tb_smem = 128 + static_cast<size_t>(kTbStages + 4) * (f->nx + 4) * 8;
+        int tb_grid = 0;
+        if (tb) {
+            S2B_CUDA(cudaFuncSetAttribute(tb_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tb_smem)));
+            int per_sm = 0;
+            S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb_fn, nt, tb_smem));
+            tb_grid = std::max(1, std::min(tb_items, std::max(1, per_sm) * ctx->num_sms));
+        }
+        auto is_record = [&](size_t done) {
+            return std::binary_search(plan.record_steps.begin(), plan.record_steps.end(), done);
+        };
         size_t rec = 0;
         int cur = 0;
-        for (size_t k = 0; k < nsteps; ++k) {
+        for (size_t k = 0; k < nsteps;) {
+            const bool two = tb && k + 1 < nsteps && !is_record((k + 1) * plan.dt_steps);
             a.k0 = k * plan.dt_steps;
             a.k1 = (k + 1) * plan.dt_steps;
+            a.k2 = (k + 2) * plan.dt_steps;
             a.in = U[cur].p;
             a.out = U[cur ^ 1].p;
             dim3 grid(gx, static_cast<unsigned>(std::min<size_t>(M, 65535)));
-            if (rows)
+            if (two)
+                tb_fn<<<tb_grid, nt, tb_smem, ctx->stream>>>(a, tb_strips, tb_items);
+            else if (rows)
                 rows_fn<<<rows_grid, nt, 0, ctx->stream>>>(a, kR, strips, items);
             else if (f->mask & 16)
                 em_step_kernel<true><<<grid, 256, 0, ctx->stream>>>(a);
@@ -416,7 +568,8 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
                 em_step_kernel<false><<<grid, 256, 0, ctx->stream>>>(a);
             S2B_LAUNCHED(ctx);
             cur ^= 1;
-            const size_t done = (k + 1) * plan.dt_steps;
+            k += two ? 2 : 1;
+            const size_t done = k * plan.dt_steps;
             while (rec < plan.record_steps.size() && plan.record_steps[rec] == done) {
                 if (rec + 1 == plan.record_steps.size()) {
                     e->states.push_back(std::move(U[cur])); // last record: the final state itself

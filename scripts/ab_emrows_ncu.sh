@@ -1,7 +1,7 @@
 #!/bin/bash
 # em_rows_kernel per-launch durations under ncu (accurate kernel time; 1024^2, 4096 paths, 16 B/pt/step)
-for cfg in ${CFGS:-"S2B_EM_D=2" "S2B_EM_D=4" "S2B_EM_D=6" "S2B_EMROWS=0"}; do
-  env $cfg ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:em_ -s 5 -c 10 --csv \
+for cfg in ${CFGS:-"S2B_EMTB=1" "S2B_EMTB=0" "S2B_EMROWS=0"}; do
+  env $cfg ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:em_ -s 4 -c 8 --csv \
     python scripts/em_probe.py --d 1024 --paths 4096 --steps 10 20 --family ${FAM:-langevin-constant} 2>/dev/null > gpurun_out/emncu.csv
   python - "$cfg" <<'PY'
 import csv, sys
