@@ -113,3 +113,21 @@ def test_gaussian_datum_bitwise(ref, s2b):
     for d in (7, 16):
         assert np.array_equal(s2b.gaussian_datum(s2b.GridSpec.square(d)),
                               ref.Ops("langevin-constant", d, order=1).datum())
+
+
+def test_bench_presets_parse(monkeypatch):
+    """bench.py --config presets: every BASELINE workload shape parses; explicit flags win."""
+    import importlib
+    import sys as _sys
+    bench = importlib.import_module("bench")
+    for cfg, d in (("cfg1", 64), ("cfg2", 256), ("cfg3", 256), ("cfg4", 512), ("cfg5", 1024)):
+        monkeypatch.setattr(_sys, "argv", ["bench.py", "--config", cfg])
+        a = bench.parse()
+        assert a.d == d and a.preset == cfg
+        nwin = int(round(a.T / a.dt))
+        assert a.warmup >= 3 and a.warmup + 2 * a.steps <= nwin  # timed + e2e windows fit T
+    monkeypatch.setattr(_sys, "argv", ["bench.py", "--config", "cfg5", "--paths", "128"])
+    assert bench.parse().paths == 128
+    monkeypatch.setattr(_sys, "argv", ["bench.py"])
+    a = bench.parse()
+    assert (a.d, a.paths, a.order, a.preset) == (256, 16384, 3, "cfg2")
