@@ -806,7 +806,11 @@ TermArgs term_args(MagnusSession& s) {
     a.S1 = s.S[1].p;
     a.tn = s.tn.p;
     a.sn = s.sn.p;
-    a.nstrips = static_cast<int>((s.op->nv + kStripRows - 1) / kStripRows);
+    {
+        const char* e = std::getenv("S2B_STRIP");
+        a.strip_rows = e ? std::max(8, std::atoi(e)) : kStripRows;
+    }
+    a.nstrips = static_cast<int>((s.op->nv + a.strip_rows - 1) / a.strip_rows);
     a.wt = s.op->d_wt.p;
     a.eslot = s.op->d_eslot.p;
     const uint64_t mask = kVariants[s.op->variant].mask;

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     constexpr int NBM = MaskInfo<MASK>::count();
     constexpr int NYE = kClasses * NBM;             // Y entries of one row
     constexpr int YST = (NYE + 1) & ~1;             // Y row stride (16-byte aligned rows)
-    constexpr int J = kStripRows;
+    const int J = a.strip_rows;
     constexpr int KP = kPairSlots;
 
     const int nx = a.op.nx, nv = a.op.nv;
