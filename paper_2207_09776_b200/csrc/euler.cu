@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(512, 2) em_tb_kernel(EmArgs a, int strips, int
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int m = item / strips;
         if (a.blown[m]) continue; // the reference stops a blown path (euler.cpp:159-162)
-        const int j0 = (item - m * strips) * kTbRows, j1 = min(nv, j0 + kTbRows);
+        const int trows = (nv + strips - 1) / strips; // rows per item (host: kTbRows, S2B_TB_ROWS)
+        const int j0 = (item - m * strips) * trows, j1 = min(nv, j0 + trows);
         const double* u = a.in + static_cast<size_t>(m) * n;
         double* o = a.out + static_cast<size_t>(m) * n;
         const double* pv = a.values + static_cast<size_t>(m) * a.vstride;
@@ -530,7 +531,9 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         // two steps per pass where the intermediate state is not a record (S2B_EMTB=0: never)
         const char* etb = std::getenv("S2B_EMTB");
         const bool tb = rows && !(etb && etb[0] == '0');
-        const int tb_strips = static_cast<int>((f->nv + kTbRows - 1) / kTbRows);
+        const char* etr = std::getenv("S2B_TB_ROWS");
+        const int tbr = etr ? std::max(4, std::atoi(etr)) : kTbRows;
+        const int tb_strips = static_cast<int>((f->nv + tbr - 1) / tbr);
         const size_t tb_items_sz = M * static_cast<size_t>(tb_strips);
         if (tb && tb_items_sz > static_cast<size_t>(INT_MAX)) fail(S2B_ERR_CONFIG, "solve_euler: too many paths");
         const int tb_items = static_cast<int>(tb_items_sz);

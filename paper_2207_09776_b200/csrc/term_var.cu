@@ -31,7 +31,7 @@ namespace mg {
 namespace {
 
 constexpr int kVarNT = 256;  // threads per CTA
-constexpr int kVarRows = 32; // output rows per work item
+constexpr int kVarRows = 128; // output rows per work item (32: 2-4% slower)
 constexpr int kRing = 8;     // ring rows per path (power of two, >= 2*KRV + 2)
 
 template <int N, class F>
@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
         // share one strip's weights while the whole set does not fit L2
         const int strip = TW ? static_cast<int>(it % strips) : static_cast<int>(it / groups);
         const int g = TW ? static_cast<int>(it / strips) : static_cast<int>(it - static_cast<long long>(strip) * groups);
-        const int j0 = strip * kVarRows, j1 = min(nv, j0 + kVarRows);
+        const int vrows = (nv + strips - 1) / strips; // rows per item (host: kVarRows, S2B_VAR_ROWS)
+        const int j0 = strip * vrows, j1 = min(nv, j0 + vrows);
         int pk[K];
         const double* in[K];
         const double* Sin[K];
@@ -311,7 +312,8 @@ __global__ void __launch_bounds__(NT, 256 / NT) term_varx_kernel(TermArgs a, int
         const int part = gfast ? static_cast<int>((it / groups) % parts) : static_cast<int>(it % parts);
         const int strip = gfast ? static_cast<int>(it / pg) : static_cast<int>((it / parts) % strips);
         const int g = gfast ? static_cast<int>(it % groups) : static_cast<int>(it / (static_cast<long long>(parts) * strips));
-        const int j0 = strip * kVarRows, j1 = min(nv, j0 + kVarRows);
+        const int vrows = (nv + strips - 1) / strips; // rows per item (host: kVarRows, S2B_VAR_ROWS)
+        const int j0 = strip * vrows, j1 = min(nv, j0 + vrows);
         xlo = part * NT;
         wpart = min(NT, nx - xlo);
         const int i = xlo + t;          // this thread's column
@@ -516,7 +518,9 @@ template <int K, VarFam F, int KRX, int KRV>
 void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     constexpr int NP = Pc<F.pc>::off(MaskInfo<F.mask>::count());
     const int nx = a.op.nx, nv = a.op.nv;
-    const int strips = (nv + kVarRows - 1) / kVarRows;
+    const char* er = std::getenv("S2B_VAR_ROWS");
+    const int vr = er ? std::max(4, std::atoi(er)) : kVarRows;
+    const int strips = (nv + vr - 1) / vr;
     // wide grids: the x-split TMA kernel (measured 2.04e8 vs 1.71e8 windows/s at 1024^2); up to
     // 256 columns the full-row kernel is ahead (1.65e8 vs 1.56e8 at cfg3).  S2B_VARX=0/1 forces.
     const char* ev = std::getenv("S2B_VARX");
