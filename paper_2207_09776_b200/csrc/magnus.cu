@@ -809,6 +809,11 @@ TermArgs term_args(MagnusSession& s) {
     {
         const char* e = std::getenv("S2B_STRIP");
         a.strip_rows = e ? std::max(8, std::atoi(e)) : kStripRows;
+        // few paths (adaptive rounds, hybrid slices, small sweeps): shorter strips keep every SM busy
+        if (!e)
+            while (a.strip_rows > 16 &&
+                   s.M * ((s.op->nv + a.strip_rows - 1) / a.strip_rows) < 4 * static_cast<size_t>(s.ctx->num_sms))
+                a.strip_rows /= 2;
     }
     a.nstrips = static_cast<int>((s.op->nv + a.strip_rows - 1) / a.strip_rows);
     a.wt = s.op->d_wt.p;

@@ -519,7 +519,11 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     constexpr int NP = Pc<F.pc>::off(MaskInfo<F.mask>::count());
     const int nx = a.op.nx, nv = a.op.nv;
     const char* er = std::getenv("S2B_VAR_ROWS");
-    const int vr = er ? std::max(4, std::atoi(er)) : kVarRows;
+    int vr = er ? std::max(4, std::atoi(er)) : kVarRows;
+    if (!er) // few paths: shorter items keep every SM busy
+        while (vr > 16 && (live_max + K - 1) / K * static_cast<size_t>((nv + vr - 1) / vr) *
+                                  static_cast<size_t>((nx + 127) / 128) < 4 * static_cast<size_t>(ctx->num_sms))
+            vr /= 2;
     const int strips = (nv + vr - 1) / vr;
     // wide grids: the x-split TMA kernel (measured 2.04e8 vs 1.71e8 windows/s at 1024^2); up to
     // 256 columns the full-row kernel is ahead (1.65e8 vs 1.56e8 at cfg3).  S2B_VARX=0/1 forces.
