@@ -108,7 +108,7 @@ def parse():
 # (SURVEY 8(d)): the preset times a fixed handful of windows (dt = 5e-4, dt_leb = 1e-5).
 PRESETS = {
     "cfg1": {"d": 64, "paths": 1000, "dt": 0.1, "dt_leb": 1e-4, "T": 1.0, "order": 2,
-             "family": "langevin-constant", "steps": 3, "warmup": 3},
+             "family": "langevin-constant", "steps": 3, "warmup": 3, "euler_steps": 2000},
     "cfg4": {"d": 512, "paths": 4096, "dt": 0.005, "dt_leb": 1e-4, "T": 1.0, "order": 3,
              "family": "langevin-constant"},
     "cfg2": {"d": 256, "paths": 16384, "dt": 0.01, "dt_leb": 1e-4, "T": 1.0, "order": 3,
@@ -319,7 +319,9 @@ def run_ours(args):
     tk_launches = st1["term_launches"] - st0["term_launches"]
     engine = ENGINES.get(st1.get("engine", 0), ENGINES[0])
     if engine["name"] == "stream" and args.family == "langevin-variable":
-        engine = ENGINE_VAR  # x-dependent weights: the streaming pass runs term_var_kernel
+        engine = dict(ENGINE_VAR)  # x-dependent weights: the streaming pass runs term_var_kernel
+        if args.d > 256:
+            engine["kernel"] = "term_varx_kernel"  # x-split variant for wide grids
     peak, peak_kind = peaks()
     achieved = alg_bytes / (tk_ms / 1e3) / 1e9 if tk_ms > 0 else 0.0
     traffic = None
