@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 // The ring (RING = 2*KRV+2 rows, slot = row mod RING) holds the part's columns plus KRX halo
 // columns on each side (the neighbour part's values, zero outside the grid).
 template <int K, uint64_t MASK, uint64_t PCNT, uint64_t PS0, uint64_t PS1, int KRX, int KRV, int NT>
-__global__ void __launch_bounds__(NT, 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast) {
+__global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast) {
     constexpr int RING = 2 * KRV + 2;
     constexpr int NB = MaskInfo<MASK>::count();
     constexpr int NP = Pc<PCNT>::off(NB);
@@ -531,24 +531,28 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     const bool varx = ev ? ev[0] != '0' : nx > kVarNT;
     if (varx) {
         // x-split TMA kernel, 4 paths per item, several CTAs per SM (S2B_VARX_NT: columns per CTA)
-        auto run = [&](auto ntag) {
+        auto run = [&](auto ntag, auto ktag) {
             constexpr int NT = decltype(ntag)::value;
-            auto kern = term_varx_kernel<4, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, NT>;
-            const size_t smem = (2 * static_cast<size_t>(NP) * NT + 4 * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
+            constexpr int KX = decltype(ktag)::value; // paths per item
+            auto kern = term_varx_kernel<KX, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, NT>;
+            const size_t smem = (2 * static_cast<size_t>(NP) * NT + KX * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
             S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             int per_sm = 0;
             S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
             const size_t parts = (nx + NT - 1) / NT;
-            const size_t items = (live_max + 3) / 4 * static_cast<size_t>(strips) * parts;
+            const size_t items = (live_max + KX - 1) / KX * static_cast<size_t>(strips) * parts;
             const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
             const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
             kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
         };
         const char* en = std::getenv("S2B_VARX_NT");
-        if (en && std::atoi(en) == 64)
-            run(std::integral_constant<int, 64>{});
+        const char* ek = std::getenv("S2B_VARX_K");
+        if (ek && std::atoi(ek) == 2)
+            run(std::integral_constant<int, kVarxNT>{}, std::integral_constant<int, 2>{});
+        else if (en && std::atoi(en) == 64)
+            run(std::integral_constant<int, 64>{}, std::integral_constant<int, 4>{});
         else
-            run(std::integral_constant<int, kVarxNT>{});
+            run(std::integral_constant<int, kVarxNT>{}, std::integral_constant<int, 4>{});
         return;
     }
     const bool tw = nx <= kVarNT;
