@@ -318,6 +318,8 @@ def run_ours(args):
     tk_ms = st1["term_kernel_ms"] - st0["term_kernel_ms"]
     tk_launches = st1["term_launches"] - st0["term_launches"]
     engine = ENGINES.get(st1.get("engine", 0), ENGINES[0])
+    if engine["name"] == "stream" and args.family != "langevin-variable" and args.d >= 1024:
+        engine = dict(engine, profile="r01_term_tma_1024_ncu.json")  # the capture at this grid
     if engine["name"] == "stream" and args.family == "langevin-variable":
         engine = dict(ENGINE_VAR)  # x-dependent weights: the streaming pass runs term_var_kernel
         if args.d > 256:
