@@ -324,6 +324,7 @@ def run_ours(args):
         engine = dict(ENGINE_VAR)  # x-dependent weights: the streaming pass runs term_var_kernel
         if args.d > 256:
             engine["kernel"] = "term_varx_kernel"  # x-split variant for wide grids
+            engine["profile"] = "none"             # no capture of it at this grid: traffic null
     peak, peak_kind = peaks()
     achieved = alg_bytes / (tk_ms / 1e3) / 1e9 if tk_ms > 0 else 0.0
     traffic = None
