@@ -63,9 +63,30 @@ def fp64_peak_tops():
         return None
 
 
+def kinetic_fields(d):
+    """Synthetic x- and v-dependent coefficients of the general kinetic SPDE
+    du = (a/2 d_vv + v d_x + b d_v + c) u dt + (sigma d_v + beta) u dW (fields gvv, fv, h, sigv,
+    sig; transport fx = -v), sampled at the interior nodes a+(i+1)delta, index j*nx+i."""
+    delta = 8.0 / (d + 1)
+    x = np.array([-4.0 + (i + 1) * delta for i in range(d)])
+    X, V = np.meshgrid(x, x, indexing="xy")
+    f = {"h": 0.2 * np.cos(X + 0.3 * V) - 0.1, "fx": -V, "fv": 0.3 * np.sin(X) * np.cos(V),
+         "gvv": 1.1 * (1.0 + 1.0 / (X * X + V * V + 1.0)), "sig": 0.1 * np.cos(V + X),
+         "sigv": 0.3 * np.sqrt(1.0 + 1.0 / (X * X + 1.0 + 0.1 * V * V))}
+    return {k: np.ascontiguousarray(a.reshape(-1)) for k, a in f.items()}
+
+
+def family_args(args):
+    """(family name for the library / oracle, extra keyword arguments)"""
+    if args.family == "kinetic-variable":
+        return "fields", {"fields": kinetic_fields(args.d)}
+    return args.family, {"a": A_LANGEVIN, "sigma": SIGMA}
+
+
 def workload_name(args):
-    fam = ("constant-coefficient Langevin" if args.family == "langevin-constant"
-           else "variable-coefficient Langevin")
+    fam = {"langevin-constant": "constant-coefficient Langevin",
+           "langevin-variable": "variable-coefficient Langevin",
+           "kinetic-variable": "general kinetic SPDE, x/v-dependent a,b,c,sigma,beta"}[args.family]
     return f"{args.preset}: {fam}"
 
 
@@ -79,8 +100,9 @@ def parse():
     ap.add_argument("--paths", type=int, default=16384, help="paths per GPU")
     ap.add_argument("--order", type=int, default=3)
     ap.add_argument("--family", default="langevin-constant",
-                    choices=["langevin-constant", "langevin-variable"],
-                    help="coefficient family (cfg3 = langevin-variable)")
+                    choices=["langevin-constant", "langevin-variable", "kinetic-variable"],
+                    help="coefficient family (cfg3 = langevin-variable; kinetic-variable = the paper's general "
+                         "kinetic SPDE with x- and v-dependent a, b, c, sigma, beta)")
     ap.add_argument("--dt", type=float, default=0.01)
     ap.add_argument("--dt-leb", type=float, default=1e-4)
     ap.add_argument("--T", type=float, default=1.0)
@@ -115,6 +137,9 @@ PRESETS = {
              "family": "langevin-constant"},
     "cfg3": {"d": 256, "paths": 16384, "dt": 0.01, "dt_leb": 1e-4, "T": 1.0, "order": 3,
              "family": "langevin-variable"},
+    # cfg3 taken literally: the general kinetic SPDE with x/v-dependent a, b, c, sigma, beta
+    "cfg3k": {"d": 256, "paths": 16384, "dt": 0.01, "dt_leb": 1e-4, "T": 1.0, "order": 3,
+              "family": "kinetic-variable"},
     "cfg5": {"d": 1024, "paths": 4096, "dt": 5e-4, "dt_leb": 1e-5, "T": 0.005, "order": 3,
              "family": "langevin-constant", "steps": 3, "warmup": 3, "euler_steps": 100},
 }
@@ -213,7 +238,8 @@ def cpu_reference_leg(args, n_paths, windows, reps=1):
     """The reference C++ (oracle/_ref, OpenMP on every host core) on a bounded sample:
     `n_paths` paths over `windows` Magnus windows of the same workload."""
     from oracle import ref
-    ops = ref.Ops(args.family, args.d, a=A_LANGEVIN, sigma=SIGMA, order=args.order)
+    fam, kw = family_args(args)
+    ops = ref.Ops(fam, args.d, order=args.order, **kw)
     T = windows * args.dt
     vals, _ = ref.simulate_brownian(T, args.dt_leb, n_paths, args.seed)
     threads = ref.max_threads()
@@ -263,7 +289,8 @@ def run_ours(args):
     grid = s2b.GridSpec.square(args.d)
     n = grid.dim()
     M = args.paths
-    op = s2b.Operator.from_family(grid, args.family, a=A_LANGEVIN, sigma=SIGMA,
+    fam, fkw = family_args(args)
+    op = s2b.Operator.from_family(grid, fam, **fkw,
                                   order=args.order, ctx=ctx)
     paths = s2b.BrownianPaths.philox(args.T, args.dt_leb, M, seed=args.seed,
                                      path_offset=rank * M, ctx=ctx)
@@ -318,9 +345,9 @@ def run_ours(args):
     tk_ms = st1["term_kernel_ms"] - st0["term_kernel_ms"]
     tk_launches = st1["term_launches"] - st0["term_launches"]
     engine = ENGINES.get(st1.get("engine", 0), ENGINES[0])
-    if engine["name"] == "stream" and args.family != "langevin-variable" and args.d >= 1024:
+    if engine["name"] == "stream" and args.family == "langevin-constant" and args.d >= 1024:
         engine = dict(engine, profile="r01_term_tma_1024_ncu.json")  # the capture at this grid
-    if engine["name"] == "stream" and args.family == "langevin-variable":
+    if engine["name"] == "stream" and args.family != "langevin-constant":
         engine = dict(ENGINE_VAR)  # x-dependent weights: the streaming pass runs term_var_kernel
         if args.d > 256:
             engine["kernel"] = "term_varx_kernel"  # x-split variant for wide grids
@@ -349,6 +376,8 @@ def run_ours(args):
     ops_pt = 2 * stencil_points(args.order) + 2
     if args.family == "langevin-variable":  # + the per-term fold of Y from the source pairs
         ops_pt += 2 * {1: 7, 2: 15, 3: 39}[args.order]
+    elif args.family == "kinetic-variable":
+        ops_pt = 2 * {2: 11, 3: 23}.get(args.order, 5) + 2 + 2 * {2: 24, 3: 64}.get(args.order, 7)
     fp64_ops = n * terms * float(ops_pt)
     fp64_peak = fp64_peak_tops()
     compute = {"bound": "fp64", "achieved": fp64_ops / (tk_ms / 1e3) / 1e12 if tk_ms > 0 else 0.0,
@@ -452,7 +481,9 @@ def run_ours(args):
 
 def euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, world, M, n):
     """E-M at dt = dt_leb on the same paths: path*gridpoint*steps/s (16 B/pt/step roofline)."""
-    f = s2b.Fields.from_family(grid, args.family, a=A_LANGEVIN, sigma=SIGMA, ctx=ctx)
+    fam, fkw = family_args(args)
+    f = (s2b.Fields.from_arrays(grid, fkw["fields"], ctx=ctx) if "fields" in fkw
+         else s2b.Fields.from_family(grid, fam, ctx=ctx, **fkw))
     steps = args.euler_steps
     T = steps * args.dt_leb
     cfg = s2b.EulerConfig(dt=args.dt_leb)

@@ -41,30 +41,72 @@ __device__ __forceinline__ void static_for(F&& f) {
     }(std::make_integer_sequence<int, N>{});
 }
 
-// PCNT: 3 bits per stencil entry (mask rank) = its number of source pairs
-template <uint64_t PCNT>
-struct Pc {
-    static constexpr int cnt(int e) { return static_cast<int>((PCNT >> (3 * e)) & 7); }
+// The operator's exact structure as a template parameter: the union stencil (mask), the number
+// of source pairs of every stencil entry (3 bits per entry, mask rank order, 21 per word) and
+// the CommutatorSet slot of every pair (3 bits per pair, 21 per word).
+struct VarFam {
+    uint64_t mask;
+    uint64_t pc[2];
+    uint64_t ps[4];
+};
+template <VarFam F>
+struct Fam {
+    static constexpr uint64_t MASK = F.mask;
+    static constexpr int cnt(int e) { return static_cast<int>((F.pc[e / 21] >> (3 * (e % 21))) & 7); }
     static constexpr int off(int e) {
         int o = 0;
         for (int i = 0; i < e; ++i) o += cnt(i);
         return o;
     }
+    static constexpr int slot(int q) { return static_cast<int>((F.ps[q / 21] >> (3 * (q % 21))) & 7); }
 };
 
-// PS0, PS1: 3 bits per source pair (pairs 0-20, 21-41) = its CommutatorSet slot
-template <uint64_t PS0, uint64_t PS1>
-struct Ps {
-    static constexpr int slot(int q) { return static_cast<int>(((q < 21 ? PS0 >> (3 * q) : PS1 >> (3 * (q - 21)))) & 7); }
-};
+// structure encodings from lists (compile time) and from an operator (upload time)
+constexpr VarFam fam_of_lists(uint64_t mask, std::initializer_list<int> counts, std::initializer_list<int> slots) {
+    VarFam f{mask, {0, 0}, {0, 0, 0, 0}};
+    int e = 0;
+    for (int c : counts) {
+        f.pc[e / 21] |= static_cast<uint64_t>(c) << (3 * (e % 21));
+        ++e;
+    }
+    int q = 0;
+    for (int sl : slots) {
+        f.ps[q / 21] |= static_cast<uint64_t>(sl) << (3 * (q % 21));
+        ++q;
+    }
+    return f;
+}
+// Langevin unions and the general kinetic SPDE of the paper
+// (a/2 d_vv + v d_x + b d_v + c, sigma d_v + beta: fields gvv, fx, fv, h, sigv, sig; 23-point
+// order-3 union, radius x 2 / v 3), pair structures as the host builder produces them
+constexpr uint64_t kMask23 = mask_of({{0, -3}, {-1, -2}, {0, -2}, {1, -2}, {-2, -1}, {-1, -1}, {0, -1}, {1, -1},
+                                      {2, -1}, {-2, 0}, {-1, 0}, {0, 0}, {1, 0}, {2, 0}, {-2, 1}, {-1, 1},
+                                      {0, 1}, {1, 1}, {2, 1}, {-1, 2}, {0, 2}, {1, 2}, {0, 3}});
+constexpr VarFam kFam19v = fam_of_lists(kMask19, {2, 1, 2, 1, 2, 4, 2, 1, 3, 3, 3, 1, 2, 4, 2, 1, 2, 1, 2},
+    {4, 5, 2, 4, 5, 5, 3, 5, 0, 1, 4, 5, 3, 5, 5, 0, 4, 5, 0, 2, 3, 0, 4, 5, 5, 3, 5, 0, 1, 4, 5, 3, 5, 5, 4, 5, 2, 4, 5});
+constexpr VarFam kFam19c = fam_of_lists(kMask19, {2, 1, 2, 1, 1, 4, 1, 1, 2, 3, 2, 1, 1, 4, 1, 1, 2, 1, 2},
+    {4, 5, 2, 4, 5, 5, 3, 0, 1, 4, 5, 3, 5, 0, 4, 0, 2, 3, 0, 4, 5, 3, 0, 1, 4, 5, 3, 5, 4, 5, 2, 4, 5});
+constexpr VarFam kFam11 = fam_of_lists(kMask11, {1, 1, 2, 1, 1, 3, 1, 1, 2, 1, 1},
+    {2, 3, 0, 1, 3, 0, 0, 2, 3, 0, 3, 0, 1, 3, 2});
+constexpr VarFam kFam5 = fam_of_lists(kMask5, {2, 1, 1, 1, 2}, {0, 1, 0, 0, 0, 0, 1});
+constexpr VarFam kFamK11 = fam_of_lists(kMask11, {2, 1, 4, 1, 2, 4, 2, 1, 4, 1, 2},
+    {2, 3, 3, 0, 1, 2, 3, 3, 0, 3, 0, 1, 2, 3, 0, 3, 3, 0, 1, 2, 3, 3, 2, 3});
+constexpr VarFam kFamK23 = fam_of_lists(kMask23,
+    {2, 2, 4, 2, 1, 3, 6, 3, 1, 1, 4, 6, 4, 1, 1, 3, 6, 3, 1, 2, 4, 2, 2},
+    {4, 5, 4, 5, 2, 3, 4, 5, 4, 5, 5, 3, 4, 5, 0, 1, 2, 3, 4, 5, 3, 4, 5, 5, 5, 0, 3, 4, 5, 0, 1, 2,
+     3, 4, 5, 0, 3, 4, 5, 5, 5, 3, 4, 5, 0, 1, 2, 3, 4, 5, 3, 4, 5, 5, 4, 5, 2, 3, 4, 5, 4, 5, 4, 5});
+constexpr VarFam kFams[] = {kFam19v, kFam19c, kFam11, kFam5, kFamK11, kFamK23};
+
 
 // TW: the weight rows stream through shared memory (TMA, double-buffered); otherwise (grids
 // whose two weight rows do not fit next to the ring) each point loads its weights from L2.
-template <int K, uint64_t MASK, uint64_t PCNT, uint64_t PS0, uint64_t PS1, int KRX, int KRV, int XPT, bool TW>
+template <int K, int FI, int KRX, int KRV, int XPT, bool TW>
 __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int strips) {
+    constexpr uint64_t MASK = kFams[FI].mask;
+    using PF = Fam<kFams[FI]>;
     static_assert(2 * KRV + 2 <= kRing, "ring too short");
     constexpr int NB = MaskInfo<MASK>::count();
-    constexpr int NP = Pc<PCNT>::off(NB);
+    constexpr int NP = PF::off(NB);
     const int nx = a.op.nx, nv = a.op.nv;
     const size_t n = static_cast<size_t>(nx) * nv;
     const int RWS = nx + 2 * KRX; // ring row stride (zero x-halo on both sides)
@@ -189,13 +231,13 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
                     constexpr int e = decltype(E)::value;
                     constexpr int b = MaskInfo<MASK>::bit_of(e);
                     constexpr int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
-                    constexpr int q0 = Pc<PCNT>::off(e);
+                    constexpr int q0 = PF::off(e);
                     double y[K];
 #pragma unroll
                     for (int k = 0; k < K; ++k) y[k] = 0.0;
-                    static_for<Pc<PCNT>::cnt(e)>([&](auto C) {
+                    static_for<PF::cnt(e)>([&](auto C) {
                         constexpr int q = q0 + decltype(C)::value;
-                        constexpr int sl = Ps<PS0, PS1>::slot(q);
+                        constexpr int sl = PF::slot(q);
                         double w;
                         if constexpr (TW) w = wr[q * nx + i];
                         else w = wg[q];
@@ -263,11 +305,13 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 // two CTAs per SM -- one CTA's per-row barrier and weight wait hide behind the other's math.
 // The ring (RING = 2*KRV+2 rows, slot = row mod RING) holds the part's columns plus KRX halo
 // columns on each side (the neighbour part's values, zero outside the grid).
-template <int K, uint64_t MASK, uint64_t PCNT, uint64_t PS0, uint64_t PS1, int KRX, int KRV, int NT>
+template <int K, int FI, int KRX, int KRV, int NT>
 __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast) {
+    constexpr uint64_t MASK = kFams[FI].mask;
+    using PF = Fam<kFams[FI]>;
     constexpr int RING = 2 * KRV + 2;
     constexpr int NB = MaskInfo<MASK>::count();
-    constexpr int NP = Pc<PCNT>::off(NB);
+    constexpr int NP = PF::off(NB);
     constexpr int RWS = NT + 2 * KRX; // ring row stride
     const int nx = a.op.nx, nv = a.op.nv;
     const size_t n = static_cast<size_t>(nx) * nv;
@@ -389,13 +433,13 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
                     constexpr int e = decltype(E)::value;
                     constexpr int b = MaskInfo<MASK>::bit_of(e);
                     constexpr int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
-                    constexpr int q0 = Pc<PCNT>::off(e);
+                    constexpr int q0 = PF::off(e);
                     double y[K];
 #pragma unroll
                     for (int k = 0; k < K; ++k) y[k] = 0.0;
-                    static_for<Pc<PCNT>::cnt(e)>([&](auto C) {
+                    static_for<PF::cnt(e)>([&](auto C) {
                         constexpr int q = q0 + decltype(C)::value;
-                        constexpr int ps = Ps<PS0, PS1>::slot(q);
+                        constexpr int ps = PF::slot(q);
                         const double w = wr[q * NT + t];
 #pragma unroll
                         for (int k = 0; k < K; ++k) y[k] += c[k][ps] * w;
@@ -449,74 +493,43 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     }
 }
 
-constexpr uint64_t pcnt_of(std::initializer_list<int> c) {
-    uint64_t v = 0;
-    int e = 0;
-    for (int x : c) v |= static_cast<uint64_t>(x) << (3 * e++);
-    return v;
-}
-// Langevin unions (both families share the pair structure up to order 2; order 3 differs)
-constexpr uint64_t kPc19var = pcnt_of({2, 1, 2, 1, 2, 4, 2, 1, 3, 3, 3, 1, 2, 4, 2, 1, 2, 1, 2});
-constexpr uint64_t kPc19con = pcnt_of({2, 1, 2, 1, 1, 4, 1, 1, 2, 3, 2, 1, 1, 4, 1, 1, 2, 1, 2});
-constexpr uint64_t kPc11 = pcnt_of({1, 1, 2, 1, 1, 3, 1, 1, 2, 1, 1});
-constexpr uint64_t kPc5 = pcnt_of({2, 1, 1, 1, 2});
-
-uint64_t pcnt_from(const s2b_operator* op) {
-    uint64_t v = 0;
+bool fam_from_op(const s2b_operator* op, VarFam* f) {
+    *f = VarFam{op->union_mask, {0, 0}, {0, 0, 0, 0}};
     int e = 0;
     for (int b = 0; b < kBoxBits; ++b)
         if ((op->union_mask >> b) & 1) {
             const int c = op->pair_begin[b + 1] - op->pair_begin[b];
-            if (c > 7 || e >= 21) return ~0ULL;
-            v |= static_cast<uint64_t>(c) << (3 * e++);
+            if (c > 7 || e >= 42) return false;
+            f->pc[e / 21] |= static_cast<uint64_t>(c) << (3 * (e % 21));
+            ++e;
         }
-    return v;
-}
-// pair slots, 3 bits each: pairs [0, 21) in ps[0], [21, 42) in ps[1]
-bool pslots_from(const s2b_operator* op, uint64_t ps[2]) {
-    ps[0] = ps[1] = 0;
-    if (op->pair_slot.size() > 42) return false;
+    if (op->pair_slot.size() > 84) return false;
     for (size_t q = 0; q < op->pair_slot.size(); ++q)
-        ps[q / 21] |= static_cast<uint64_t>(op->pair_slot[q]) << (3 * (q % 21));
+        f->ps[q / 21] |= static_cast<uint64_t>(op->pair_slot[q]) << (3 * (q % 21));
     return true;
 }
-constexpr uint64_t pslot_of(std::initializer_list<int> sl, int part) {
-    uint64_t v = 0;
-    int q = 0;
-    for (int x : sl) {
-        if (q / 21 == part) v |= static_cast<uint64_t>(x) << (3 * (q % 21));
-        ++q;
-    }
-    return v;
+bool same(const VarFam& a, const VarFam& b) {
+    return a.mask == b.mask && a.pc[0] == b.pc[0] && a.pc[1] == b.pc[1] && a.ps[0] == b.ps[0] &&
+           a.ps[1] == b.ps[1] && a.ps[2] == b.ps[2] && a.ps[3] == b.ps[3];
 }
-#define S2B_SL19V {4, 5, 2, 4, 5, 5, 3, 5, 0, 1, 4, 5, 3, 5, 5, 0, 4, 5, 0, 2, 3, 0, 4, 5, 5, 3, 5, 0, 1, 4, 5, 3, 5, 5, 4, 5, 2, 4, 5}
-#define S2B_SL19C {4, 5, 2, 4, 5, 5, 3, 0, 1, 4, 5, 3, 5, 0, 4, 0, 2, 3, 0, 4, 5, 3, 0, 1, 4, 5, 3, 5, 4, 5, 2, 4, 5}
-#define S2B_SL11 {2, 3, 0, 1, 3, 0, 0, 2, 3, 0, 3, 0, 1, 3, 2}
-#define S2B_SL5 {0, 1, 0, 0, 0, 0, 1}
-struct VarFam {
-    uint64_t mask, pc, ps0, ps1;
-};
-constexpr VarFam kFam19v{kMask19, kPc19var, pslot_of(S2B_SL19V, 0), pslot_of(S2B_SL19V, 1)};
-constexpr VarFam kFam19c{kMask19, kPc19con, pslot_of(S2B_SL19C, 0), pslot_of(S2B_SL19C, 1)};
-constexpr VarFam kFam11{kMask11, kPc11, pslot_of(S2B_SL11, 0), 0};
-constexpr VarFam kFam5{kMask5, kPc5, pslot_of(S2B_SL5, 0), 0};
-
 int fam_of(const s2b_operator* op) {
-    uint64_t ps[2];
-    if (!pslots_from(op, ps)) return -1;
-    const uint64_t pc = pcnt_from(op);
-    const VarFam fams[4] = {kFam19v, kFam19c, kFam11, kFam5};
-    for (int f = 0; f < 4; ++f)
-        if (op->union_mask == fams[f].mask && pc == fams[f].pc && ps[0] == fams[f].ps0 && ps[1] == fams[f].ps1)
-            return f;
+    VarFam f;
+    if (!fam_from_op(op, &f)) return -1;
+    for (int i = 0; i < static_cast<int>(sizeof(kFams) / sizeof(kFams[0])); ++i)
+        if (same(f, kFams[i])) return i;
     return -1;
+}
+
+// shared memory of one CTA: two weight rows + the K-path ring must fit 227 KB
+size_t var_smem(int np, int k, int nx, int krx) {
+    return (2 * static_cast<size_t>(np) * nx + static_cast<size_t>(k) * kRing * (nx + 2 * krx)) * 8;
 }
 
 constexpr int kVarxNT = 128; // columns (threads) per CTA of the x-split kernel
 
-template <int K, VarFam F, int KRX, int KRV>
+template <int K, int FI, int KRX, int KRV>
 void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
-    constexpr int NP = Pc<F.pc>::off(MaskInfo<F.mask>::count());
+    constexpr int NP = Fam<kFams[FI]>::off(MaskInfo<kFams[FI].mask>::count());
     const int nx = a.op.nx, nv = a.op.nv;
     const char* er = std::getenv("S2B_VAR_ROWS");
     int vr = er ? std::max(4, std::atoi(er)) : kVarRows;
@@ -528,13 +541,15 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     // wide grids: the x-split TMA kernel (measured 2.04e8 vs 1.71e8 windows/s at 1024^2); up to
     // 256 columns the full-row kernel is ahead (1.65e8 vs 1.56e8 at cfg3).  S2B_VARX=0/1 forces.
     const char* ev = std::getenv("S2B_VARX");
-    const bool varx = ev ? ev[0] != '0' : nx > kVarNT;
+    // the full-row kernel needs two weight rows + the ring in one CTA's shared memory
+    const bool row_fits = NP <= 40 && var_smem(NP, K, nx, KRX) <= 227 * 1024;
+    const bool varx = (ev ? ev[0] != '0' : nx > kVarNT) || !row_fits;
     if (varx) {
         // x-split TMA kernel, 4 paths per item, several CTAs per SM (S2B_VARX_NT: columns per CTA)
         auto run = [&](auto ntag, auto ktag) {
             constexpr int NT = decltype(ntag)::value;
             constexpr int KX = decltype(ktag)::value; // paths per item
-            auto kern = term_varx_kernel<KX, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, NT>;
+            auto kern = term_varx_kernel<KX, FI, KRX, KRV, NT>;
             const size_t smem = (2 * static_cast<size_t>(NP) * NT + KX * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
             S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             int per_sm = 0;
@@ -547,6 +562,10 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         };
         const char* en = std::getenv("S2B_VARX_NT");
         const char* ek = std::getenv("S2B_VARX_K");
+        if constexpr (NP > 40) { // many source pairs: 64-column parts keep two CTAs per SM
+            run(std::integral_constant<int, 64>{}, std::integral_constant<int, 4>{});
+            return;
+        }
         if (ek && std::atoi(ek) == 2)
             run(std::integral_constant<int, kVarxNT>{}, std::integral_constant<int, 2>{});
         else if (en && std::atoi(en) == 64)
@@ -566,18 +585,16 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
         kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips);
     };
-    if (tw)
-        go(term_var_kernel<K, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, 1, true>);
-    else if (nx <= 2 * kVarNT)
-        go(term_var_kernel<K, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, 2, false>);
-    else
-        go(term_var_kernel<K, F.mask, F.pc, F.ps0, F.ps1, KRX, KRV, 4, false>);
+    if constexpr (NP <= 40) {
+        if (tw)
+            go(term_var_kernel<K, FI, KRX, KRV, 1, true>);
+        else if (nx <= 2 * kVarNT)
+            go(term_var_kernel<K, FI, KRX, KRV, 2, false>);
+        else
+            go(term_var_kernel<K, FI, KRX, KRV, 4, false>);
+    }
 }
 
-// shared memory of one CTA: two weight rows + the K-path ring must fit 227 KB
-size_t var_smem(int np, int k, int nx, int krx) {
-    return (2 * static_cast<size_t>(np) * nx + static_cast<size_t>(k) * kRing * (nx + 2 * krx)) * 8;
-}
 
 } // namespace
 
@@ -586,30 +603,33 @@ bool term_var_supported(const s2b_operator* op) {
     if (e && e[0] == '0') return false;
     if (op->compressed || !op->wfinite || op->nx < 2 || op->nx % 2 != 0 || op->nx > 4 * static_cast<size_t>(kVarNT))
         return false;
-    const int f = fam_of(op);
-    if (f < 0) return false;
-    const int nx = static_cast<int>(op->nx);
-    return nx > kVarNT || var_smem(op->npairs, 4, nx, 2) <= 227 * 1024;
+    return fam_of(op) >= 0;
 }
 
 void launch_term_var(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, size_t live_max) {
     const bool wide = op->nx > 2 * static_cast<size_t>(kVarNT); // 2 paths per item at 1024^2
     switch (fam_of(op)) {
     case 0:
-        if (wide) launch_var_k<2, kFam19v, 2, 2>(ctx, a, live_max);
-        else launch_var_k<4, kFam19v, 2, 2>(ctx, a, live_max);
+        if (wide) launch_var_k<2, 0, 2, 2>(ctx, a, live_max);
+        else launch_var_k<4, 0, 2, 2>(ctx, a, live_max);
         break;
     case 1:
-        if (wide) launch_var_k<2, kFam19c, 2, 2>(ctx, a, live_max);
-        else launch_var_k<4, kFam19c, 2, 2>(ctx, a, live_max);
+        if (wide) launch_var_k<2, 1, 2, 2>(ctx, a, live_max);
+        else launch_var_k<4, 1, 2, 2>(ctx, a, live_max);
         break;
     case 2:
-        if (wide) launch_var_k<2, kFam11, 1, 2>(ctx, a, live_max);
-        else launch_var_k<4, kFam11, 1, 2>(ctx, a, live_max);
+        if (wide) launch_var_k<2, 2, 1, 2>(ctx, a, live_max);
+        else launch_var_k<4, 2, 1, 2>(ctx, a, live_max);
         break;
-    default:
-        if (wide) launch_var_k<2, kFam5, 1, 1>(ctx, a, live_max);
-        else launch_var_k<4, kFam5, 1, 1>(ctx, a, live_max);
+    case 3:
+        if (wide) launch_var_k<2, 3, 1, 1>(ctx, a, live_max);
+        else launch_var_k<4, 3, 1, 1>(ctx, a, live_max);
+        break;
+    case 4: // general kinetic SPDE, order 2
+        launch_var_k<4, 4, 1, 2>(ctx, a, live_max);
+        break;
+    default: // general kinetic SPDE, order 3 (23 points, 64 source pairs)
+        launch_var_k<4, 5, 2, 3>(ctx, a, live_max);
         break;
     }
 }

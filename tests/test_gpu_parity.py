@@ -126,6 +126,29 @@ def test_magnus_custom_nine_fields(ref, s2b, ctx):
     assert np.array_equal(ens[-1].states(), want[-1], equal_nan=True)
 
 
+@pytest.mark.parametrize("d,order", [(16, 2), (20, 3), (130, 3), (258, 2)])
+def test_magnus_kinetic_variable_fields(ref, s2b, ctx, d, order):
+    """The paper's general kinetic SPDE with x- and v-dependent a, b, c, sigma, beta (23-point
+    order-3 union, 64 source pairs): term_var_kernel / term_varx_kernel (64-column parts,
+    a last part 2 columns wide at 130 / 258), bitwise."""
+    from fieldsets import kinetic_fields
+    T, dt_leb, dt = 0.004, 1e-4, 0.002
+    fields = kinetic_fields(d)
+    ops = ref.Ops("fields", d, order=order, fields=fields)
+    values, _ = ref.simulate_brownian(T, dt_leb, 5, d)
+    want, wst, _ = ops.solve_magnus(values, dt_leb, T, dt, record_times=[dt], seed=d)
+    g = s2b.GridSpec.square(d)
+    op = s2b.Operator.from_family(g, "fields", order=order, fields=fields, ctx=ctx)
+    info = op.info()
+    assert info["stencil_points"] == (23 if order == 3 else 11)
+    paths = s2b.BrownianPaths.from_values(values, dt_leb, seed=d, ctx=ctx)
+    ens = s2b.solve_iterated_magnus(s2b.MagnusConfig(order=order, dt=dt, record_times=[dt]), op,
+                                    ops.datum(), paths, T, g)
+    for r, e in enumerate(ens):
+        assert np.array_equal(e.status, wst[r])
+        assert np.array_equal(e.states(), want[r], equal_nan=True)
+
+
 def test_magnus_blowup_flagged(ref, s2b, ctx):
     """test_magnus.cpp:208-223: a tiny norm cap trips on the first window."""
     d, T, dt_leb = 10, 0.2, 1e-3
