@@ -349,8 +349,8 @@ def run_ours(args):
         engine = dict(engine, profile="r01_term_tma_1024_ncu.json")  # the capture at this grid
     if engine["name"] == "stream" and args.family != "langevin-constant":
         engine = dict(ENGINE_VAR)  # x-dependent weights: the streaming pass runs term_var_kernel
-        if args.d > 256:
-            engine["kernel"] = "term_varx_kernel"  # x-split variant for wide grids
+        if args.d > 256 or (args.family == "kinetic-variable" and args.order == 3):
+            engine["kernel"] = "term_varx_kernel"  # x-split variant: wide grids, 64 source pairs
             engine["profile"] = "none"             # no capture of it at this grid: traffic null
     peak, peak_kind = peaks()
     achieved = alg_bytes / (tk_ms / 1e3) / 1e9 if tk_ms > 0 else 0.0
@@ -506,6 +506,7 @@ def euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, worl
             "roofline": {"bound": "hbm", "achieved": 16.0 * rate / world / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": 16.0 * rate / world / 1e9 / peak,
                          "kernel": ("em_tb_kernel" if os.environ.get("S2B_EMXM", "1") == "0" or args.d not in (64, 128, 256, 512)
+                                    or args.family == "kinetic-variable"
                                     else "em_cluster_kernel" if args.d == 256 and os.environ.get("S2B_EM2", "1") == "0"
                                     else "em_cluster_ip_kernel"),
                          "note": "whole solve_euler call incl. state init; 16 B/pt/step streaming-equivalent "
