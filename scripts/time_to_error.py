@@ -51,7 +51,8 @@ def main():
     ap.add_argument("--seed", type=int, default=424242)
     ap.add_argument("--magnus-dt", default="0.05,0.02,0.01,0.005,0.0025")
     ap.add_argument("--euler-dt", default="1e-4,5e-5,2e-5,1e-5")
-    ap.add_argument("--family", default="langevin-constant", choices=["langevin-constant", "langevin-variable"])
+    ap.add_argument("--family", default="langevin-constant",
+                    choices=["langevin-constant", "langevin-variable", "kinetic-variable"])
     ap.add_argument("--ref-dt", type=float, default=None, help="E-M reference dt (variable family)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "time_to_error.json"))
     args = ap.parse_args()
@@ -63,7 +64,14 @@ def main():
     t0 = time.perf_counter()
     paths = s2b.BrownianPaths.philox(args.T, args.dt_leb, args.paths, seed=args.seed, ctx=ctx)
     phi = s2b.gaussian_datum(g)
-    fields = s2b.Fields.from_family(g, fam, a=a, sigma=sigma, ctx=ctx)
+    if fam == "kinetic-variable":  # the general kinetic SPDE, x/v-dependent a, b, c, sigma, beta
+        from bench import kinetic_fields
+        kf = kinetic_fields(args.d)
+        fields = s2b.Fields.from_arrays(g, kf, ctx=ctx)
+        make_op = lambda order: s2b.Operator.from_family(g, "fields", order=order, fields=kf, ctx=ctx)  # noqa: E731
+    else:
+        fields = s2b.Fields.from_family(g, fam, a=a, sigma=sigma, ctx=ctx)
+        make_op = lambda order: s2b.Operator.from_family(g, fam, a=a, sigma=sigma, order=order, ctx=ctx)  # noqa: E731
     if fam == "langevin-constant":
         ref = s2b.exact_reference(g, args.T, a, sigma, paths, ctx=ctx)
         ref_desc = "exact_reference (closed form)"
@@ -89,7 +97,7 @@ def main():
         print(json.dumps(row), flush=True)
 
     for order in (2, 3):
-        op = s2b.Operator.from_family(g, fam, a=a, sigma=sigma, order=order, ctx=ctx)
+        op = make_op(order)
         for dt in [float(x) for x in args.magnus_dt.split(",")]:
             record("magnus", order, dt, lambda: s2b.solve_iterated_magnus(
                 s2b.MagnusConfig(order=order, dt=dt), op, phi, paths, args.T, g))
