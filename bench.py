@@ -506,7 +506,8 @@ def euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, worl
             "roofline": {"bound": "hbm", "achieved": 16.0 * rate / world / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": 16.0 * rate / world / 1e9 / peak,
                          "kernel": ("em_tb_kernel" if os.environ.get("S2B_EMXM", "1") == "0" or args.d not in (64, 128, 256, 512)
-                                    or args.family == "kinetic-variable"
+                                    or (args.family == "kinetic-variable" and args.d == 256
+                                        and os.environ.get("S2B_EM2", "1") == "0")
                                     else "em_cluster_kernel" if args.d == 256 and os.environ.get("S2B_EM2", "1") == "0"
                                     else "em_cluster_ip_kernel"),
                          "note": "whole solve_euler call incl. state init; 16 B/pt/step streaming-equivalent "

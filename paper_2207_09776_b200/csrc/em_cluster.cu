@@ -37,6 +37,7 @@ constexpr int kEmCl = 8;
 struct EmXmArgs {
     const double* rowf; // [9][nv] row values of the x-invariant fields
     const double* colf; // [9][nx] column values of the v-invariant (x-dependent) fields, 1/2 applied to g
+    const double* fgen; // [9][nx][nv] every field per point, x-major (a warp's rows coalesce), 1/2 applied to g
     double st[5];
     double dt;
     const double* values; // [M][vstride] Brownian prefix values
@@ -281,14 +282,15 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
     const bool do_rem = rem0 != nullptr;
     int* next0 = cluster.map_shared_rank(&next_path, 0);
 
-    const double fh = (MASK & 1) ? a.rowf[0 * a.nv + j] : 0.0;
-    const double ffx = (MASK & 2) ? a.rowf[1 * a.nv + j] : 0.0;
-    const double ffv = (MASK & 4) ? a.rowf[2 * a.nv + j] : 0.0;
-    const double hgxx = (MASK & 8) ? 0.5 * a.rowf[3 * a.nv + j] : 0.0;
-    const double hgvv = (MASK & 32) ? 0.5 * a.rowf[5 * a.nv + j] : 0.0;
-    const double fsig = (MASK & 64) ? a.rowf[6 * a.nv + j] : 0.0;
-    const double fsx = (MASK & 128) ? a.rowf[7 * a.nv + j] : 0.0;
-    const double fsv = (MASK & 256) ? a.rowf[8 * a.nv + j] : 0.0;
+    constexpr bool RV = XD != -1; // row values used at all
+    const double fh = (RV && (MASK & 1)) ? a.rowf[0 * a.nv + j] : 0.0;
+    const double ffx = (RV && (MASK & 2)) ? a.rowf[1 * a.nv + j] : 0.0;
+    const double ffv = (RV && (MASK & 4)) ? a.rowf[2 * a.nv + j] : 0.0;
+    const double hgxx = (RV && (MASK & 8)) ? 0.5 * a.rowf[3 * a.nv + j] : 0.0;
+    const double hgvv = (RV && (MASK & 32)) ? 0.5 * a.rowf[5 * a.nv + j] : 0.0;
+    const double fsig = (RV && (MASK & 64)) ? a.rowf[6 * a.nv + j] : 0.0;
+    const double fsx = (RV && (MASK & 128)) ? a.rowf[7 * a.nv + j] : 0.0;
+    const double fsv = (RV && (MASK & 256)) ? a.rowf[8 * a.nv + j] : 0.0;
     const double st0 = a.st[0], st1 = a.st[1], st2 = a.st[2], st3 = a.st[3];
     const double dt = a.dt;
 
@@ -373,26 +375,29 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
                         const double dxu = (uxp - uxm) * st0;
                         const double dvu = (uvp - uvm) * st2;
                         double drift = 0.0; // (NZ: the first present term starts the fold, see em_first)
-                        if (MASK & 1) drift = EM_ADD(1, drift, fh * uc);
+                        if (MASK & 1) drift = EM_ADD(1, drift, (XD == -1 ? __ldg(a.fgen + 0 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j) : fh) * uc);
                         if (MASK & 2) {
-                            const double fx = (XD & 2) ? __ldg(a.colf + 1 * NX + x0 + c) : ffx;
+                            const double fx = XD == -1 ? __ldg(a.fgen + 1 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j)
+                                            : (XD & 2) ? __ldg(a.colf + 1 * NX + x0 + c) : ffx;
                             drift = EM_ADD(2, drift, fx * dxu);
                         }
-                        if (MASK & 4) drift = EM_ADD(4, drift, ffv * dvu);
+                        if (MASK & 4) drift = EM_ADD(4, drift, (XD == -1 ? __ldg(a.fgen + 2 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j) : ffv) * dvu);
                         if (MASK & 8) {
                             const double dxxu = (uxp - 2.0 * uc + uxm) * st1;
-                            drift = EM_ADD(8, drift, hgxx * dxxu);
+                            drift = EM_ADD(8, drift, (XD == -1 ? __ldg(a.fgen + 3 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j) : hgxx) * dxxu);
                         }
                         if (MASK & 32) {
                             const double dvvu = (uvp - 2.0 * uc + uvm) * st3;
-                            const double g = (XD & 32) ? __ldg(a.colf + 5 * NX + x0 + c) : hgvv;
+                            const double g = XD == -1 ? __ldg(a.fgen + 5 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j)
+                                           : (XD & 32) ? __ldg(a.colf + 5 * NX + x0 + c) : hgvv;
                             drift = EM_ADD(32, drift, g * dvvu);
                         }
                         double noise = 0.0;
-                        if (MASK & 64) noise = EM_ADD(64, noise, fsig * uc);
-                        if (MASK & 128) noise = EM_ADD(128, noise, fsx * dxu);
+                        if (MASK & 64) noise = EM_ADD(64, noise, (XD == -1 ? __ldg(a.fgen + 6 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j) : fsig) * uc);
+                        if (MASK & 128) noise = EM_ADD(128, noise, (XD == -1 ? __ldg(a.fgen + 7 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j) : fsx) * dxu);
                         if (MASK & 256) {
-                            const double sv = (XD & 256) ? __ldg(a.colf + 8 * NX + x0 + c) : fsv;
+                            const double sv = XD == -1 ? __ldg(a.fgen + 8 * static_cast<size_t>(n) + static_cast<size_t>(x0 + c) * NX + j)
+                                            : (XD & 256) ? __ldg(a.colf + 8 * NX + x0 + c) : fsv;
                             noise = EM_ADD(256, noise, sv * dvu);
                         }
                         const double next = uc + drift * dt + noise * dW[pi];
@@ -489,11 +494,16 @@ bool em_multi_path() {
     return !(e && e[0] == '0');
 }
 
+// the paper's general kinetic SPDE: h (c), fx (transport), fv (b), gvv (a), sig (beta), sigv (sigma)
+constexpr int kKineticMask = 1 | 2 | 4 | 32 | 64 | 256;
+
 bool em_cluster_supported(const s2b_fields* f) {
     const char* e = std::getenv("S2B_EMXM");
     if (e && e[0] == '0') return false;
     const bool grid_ok = f->nx == f->nv && (f->nx == 64 || f->nx == 128 || f->nx == 256 || f->nx == 512);
-    if (!grid_ok || f->mask != (2 | 32 | 256)) return false;
+    if (!grid_ok) return false;
+    if (f->mask == kKineticMask) return em_multi_path() || f->nx != 256; // general fields per point (in place)
+    if (f->mask != (2 | 32 | 256)) return false;
     if (f->nx < 256) return f->xinv || (f->sep && f->xdep == (32 | 256)); // in-place kernels only
     if (f->xinv) return true;
     // separable fields (each x- or v-invariant): the in-place kernels take x-dependent gvv / sigv
@@ -515,6 +525,7 @@ void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const do
     EmXmArgs a{};
     a.rowf = f->d_rowf.p;
     a.colf = f->d_colf.p;
+    a.fgen = f->d_fgen.p;
     std::copy(f->st, f->st + 5, a.st);
     a.dt = dt;
     a.values = paths->d_values.p;
@@ -542,7 +553,13 @@ void em_cluster_solve(s2b_context* ctx, const s2b_fields* f, double dt, const do
     using F_ = std::false_type;
     using X0 = std::integral_constant<int, 0>;
     using XV_ = std::integral_constant<int, 32 | 256>;
-    if (f->nx < 256) {
+    if (f->mask == kKineticMask) { // general fields: every value per point from the halved table
+        constexpr int KM = kKineticMask;
+        if (f->nx == 64) launch_em_ip<KM, 64, 2, 6, false, -1>(ctx, a);
+        else if (f->nx == 128) launch_em_ip<KM, 128, 4, 3, false, -1>(ctx, a);
+        else if (f->nx == 256) launch_em_ip<KM, 256, 8, S2B_EM_NP, false, -1>(ctx, a);
+        else launch_em_ip<KM, 512, 16, 1, false, -1>(ctx, a);
+    } else if (f->nx < 256) {
         if (xd == 0) no_neg_zero ? small(T_{}, X0{}) : small(F_{}, X0{});
         else no_neg_zero ? small(T_{}, XV_{}) : small(F_{}, XV_{});
     } else if (xd == (32 | 256)) { // the variable Langevin family: a(x), sigma(x)

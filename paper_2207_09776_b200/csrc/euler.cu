@@ -425,6 +425,21 @@ s2b_fields* make_fields(s2b_context* ctx, const s2b_grid* grid, const double* co
             S2B_CUDA(cudaMemcpy(f->d_rowf.p, rowf2.data(), rowf2.size() * sizeof(double), cudaMemcpyHostToDevice));
         }
     }
+    // general fields for the cluster E-M kernels: every field per point, 0.5 * g pre-applied
+    // (the reference's (0.5 * g) product, the same rounding)
+    if (!f->xinv && !(f->mask & 16)) {
+        std::vector<double> fg(9 * n, 0.0);
+        for (int k = 0; k < 9; ++k) {
+            if (!(f->mask >> k & 1)) continue;
+            for (size_t j = 0; j < nv; ++j) // x-major: [k][i][j]
+                for (size_t i = 0; i < nx; ++i) {
+                    const double v = fields9[k][j * nx + i];
+                    fg[k * n + i * nv + j] = (k == 3 || k == 5) ? 0.5 * v : v;
+                }
+        }
+        f->d_fgen.alloc(9 * n);
+        S2B_CUDA(cudaMemcpy(f->d_fgen.p, fg.data(), fg.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     // EulerStencils::from_grid (euler.cpp:18-26)
     const double dx = (grid->bx - grid->ax) / static_cast<double>(nx + 1);
     const double dv = (grid->bv - grid->av) / static_cast<double>(nv + 1);

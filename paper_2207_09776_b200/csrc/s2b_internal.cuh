@@ -116,6 +116,7 @@ struct s2b_fields {
     bool sep = false;
     int xdep = 0;
     s2b::DevBuf<double> d_colf;
+    s2b::DevBuf<double> d_fgen; // [9][nx][nv] every field x-major, g^xx / g^vv pre-halved (cluster E-M)
 };
 
 struct s2b_paths {

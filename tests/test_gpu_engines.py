@@ -218,3 +218,24 @@ def test_xm_small_grids_bitwise(ref, s2b, ctx, d, order):
     for r, e in enumerate(ens):
         assert np.array_equal(e.status, wst[r])
         assert np.array_equal(e.states(), want[r], equal_nan=True)
+
+
+@pytest.mark.parametrize("em_engine", list(EM_ENGINES), indirect=True)
+@pytest.mark.parametrize("d", [64, 128, 256, 512])
+def test_euler_kinetic_fields_bitwise(ref, s2b, ctx, em_engine, d):
+    """The paper's general kinetic SPDE (x/v-dependent a, b, c, sigma, beta): the in-place
+    cluster E-M kernels read every field per point from a (0.5 g pre-applied) table; the
+    streaming kernels as before; both bitwise against the reference with a mid-run record."""
+    from fieldsets import kinetic_fields
+    T, dt_leb, M, seed = 0.002, 1e-4, 4, 31
+    fields = kinetic_fields(d)
+    ops = ref.Ops("fields", d, order=1, fields=fields)
+    values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
+    want, wst, _ = ops.solve_euler(values, dt_leb, T, dt_leb, record_times=[0.0007], seed=seed)
+    g = s2b.GridSpec.square(d)
+    f = s2b.Fields.from_arrays(g, fields, ctx=ctx)
+    paths = s2b.BrownianPaths.from_values(values, dt_leb, seed=seed, ctx=ctx)
+    ens = s2b.solve_euler(s2b.EulerConfig(dt=dt_leb, record_times=[0.0007]), f, g, ops.datum(), paths, T)
+    for r, e in enumerate(ens):
+        assert np.array_equal(e.status, wst[r])
+        assert np.array_equal(e.states(), want[r])
