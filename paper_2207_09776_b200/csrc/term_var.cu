@@ -563,7 +563,12 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         const char* en = std::getenv("S2B_VARX_NT");
         const char* ek = std::getenv("S2B_VARX_K");
         if constexpr (NP > 40) { // many source pairs: 64-column parts keep two CTAs per SM
-            run(std::integral_constant<int, 64>{}, std::integral_constant<int, 4>{});
+            if (en && std::atoi(en) == 128)
+                run(std::integral_constant<int, 128>{}, std::integral_constant<int, 4>{});
+            else if (ek && std::atoi(ek) == 2)
+                run(std::integral_constant<int, 64>{}, std::integral_constant<int, 2>{});
+            else
+                run(std::integral_constant<int, 64>{}, std::integral_constant<int, 4>{});
             return;
         }
         if (ek && std::atoi(ek) == 2)
