@@ -131,3 +131,34 @@ def test_bench_presets_parse(monkeypatch):
     monkeypatch.setattr(_sys, "argv", ["bench.py"])
     a = bench.parse()
     assert (a.d, a.paths, a.order, a.preset) == (256, 16384, 3, "cfg2")
+
+
+def _ref_built():
+    return os.path.isdir(os.path.join(ROOT, "oracle", "_ref")) and any(
+        f.endswith(".so") for f in os.listdir(os.path.join(ROOT, "oracle", "_ref")))
+
+
+@pytest.mark.skipif(not _ref_built(), reason="oracle/_ref not built")
+def test_bench_reference_arm_contract(tmp_path):
+    """`bench.py --impl reference` (the driver's reference arm): rank 0 prints ONE JSON line
+    with the arm's keys on a bounded cfg1 sample; any other rank exits 0 without output."""
+    import json
+    import subprocess
+    import sys as _sys
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    cmd = [_sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1",
+           "--steps", "1", "--warmup", "0"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=tmp_path, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["metric"] == "magnus path*gridpoint*windows/s"
+    assert d["value"] > 0 and d["steps"] == 1 and d["warmup"] == 0 and d["higher_is_better"]
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    env.update(RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=tmp_path, timeout=120)
+    assert out.returncode == 0 and out.stdout.strip() == ""
