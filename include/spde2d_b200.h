@@ -211,13 +211,17 @@ int s2b_solve_adaptive_magnus(s2b_context *ctx, const s2b_operator *op, const s2
                               const s2b_adaptive_config *adaptive, const double *phi,
                               const s2b_paths *paths, s2b_ensemble **out, s2b_magnus_stats *stats);
 
-/* Resident Magnus session: state stays in HBM, windows are advanced on demand. */
+/* Resident Magnus session: state stays in HBM, windows are advanced on demand.
+ * The session borrows `op` and `paths`: both must outlive it (destroy the session first).
+ * After s2b_magnus_session_finish the session's buffers belong to the returned ensemble:
+ * advance / reset / stats / ensemble / moments / a second finish return S2B_ERR_CONFIG;
+ * only destroy is valid. */
 int s2b_magnus_session_create(s2b_context *ctx, const s2b_operator *op,
                               const s2b_magnus_config *cfg, const double *phi,
                               const s2b_paths *paths, s2b_magnus_session **out);
 /* Advance every live path by up to n_windows windows (stops at T). */
 int s2b_magnus_session_advance(s2b_magnus_session *s, size_t n_windows);
-/* Reset every path to phi at window 0 (reuses all buffers). */
+/* Reset every path to phi at window 0 (reuses all buffers; refused after finish). */
 int s2b_magnus_session_reset(s2b_magnus_session *s);
 int s2b_magnus_session_stats(const s2b_magnus_session *s, s2b_magnus_stats *stats);
 /* Enable CUDA-event timing of every term-kernel launch (accumulated in the stats). */

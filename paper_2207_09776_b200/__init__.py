@@ -146,14 +146,19 @@ FIELD_NAMES = ("h", "fx", "fv", "gxx", "gxv", "gvv", "sig", "sigx", "sigv")
 SLOTS = ("B", "A", "A2", "BA", "BAA", "BAB")
 
 
-def _fields_array(fields):
+def _fields_array(fields, grid):
     arr = (C.POINTER(C.c_double) * 9)()
     keep = []
     if fields:
+        unknown = set(fields) - set(FIELD_NAMES)
+        if unknown:
+            raise ConfigError(f"coefficient fields: unknown names {sorted(unknown)}")
         for k, name in enumerate(FIELD_NAMES):
             f = fields.get(name)
             if f is not None:
                 f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+                if f.size != grid.dim():  # C copies exactly nx*nv doubles per field
+                    raise DimensionError(f"coefficient field {name}: {f.size} values, grid has {grid.dim()}")
                 keep.append(f)
                 arr[k] = _dptr(f)
     return arr, keep
@@ -170,7 +175,7 @@ class Operator:
                     sigma=1.0 / np.sqrt(10.0), order=3, fields=None, ctx: Context = None):
         """Host-kept builder (sample_coefficients -> assemble_* -> precompute_commutators)."""
         ctx = ctx or default_context()
-        arr, keep = _fields_array(fields)
+        arr, keep = _fields_array(fields, grid)
         h = C.c_void_p()
         _check(lib().s2b_operator_build(ctx.h, C.byref(grid.c()), FAMILIES[family], a, sigma, arr,
                                         order, C.byref(h)))
@@ -228,7 +233,7 @@ class Fields:
     @classmethod
     def from_arrays(cls, grid: GridSpec, fields: dict, ctx: Context = None):
         ctx = ctx or default_context()
-        arr, keep = _fields_array(fields)
+        arr, keep = _fields_array(fields, grid)
         h = C.c_void_p()
         _check(lib().s2b_fields_create(ctx.h, C.byref(grid.c()), arr, C.byref(h)))
         return cls(h, ctx, grid)
@@ -247,7 +252,7 @@ class HostOps:
 
     def __init__(self, grid: GridSpec, family="langevin-constant", a=1.1,
                  sigma=1.0 / np.sqrt(10.0), order=3, fields=None):
-        arr, keep = _fields_array(fields)
+        arr, keep = _fields_array(fields, grid)
         h = C.c_void_p()
         _check(lib().s2b_host_ops_build(C.byref(grid.c()), FAMILIES[family], a, sigma, arr, order,
                                         C.byref(h)))
@@ -311,8 +316,10 @@ class BrownianPaths:
     @classmethod
     def from_values(cls, values, dt_leb, seed=1, ctx: Context = None):
         """Parity mode: the reference's own BrownianBatch::values."""
-        ctx = ctx or default_context()
         v = np.ascontiguousarray(values, np.float64)
+        if v.ndim != 2 or v.shape[1] < 2:
+            raise DimensionError(f"BrownianPaths.from_values: need [M][steps+1] values, got {v.shape}")
+        ctx = ctx or default_context()
         M, steps = v.shape[0], v.shape[1] - 1
         h = C.c_void_p()
         _check(lib().s2b_paths_create_host(ctx.h, dt_leb, steps, M, seed, _dptr(v), C.byref(h)))
@@ -331,7 +338,14 @@ class BrownianPaths:
 
     def upload(self, k0, k1, values):
         """Overwrite Lebesgue columns [k0, k1] of every path from a host [M][steps+1] array
-        (asynchronous on the context stream when `values` is pinned)."""
+        (asynchronous on the context stream when `values` is pinned).  The array is handed to
+        C as is (no copy, so a pinned buffer stays pinned): it must be float64, C-contiguous
+        and exactly [M][steps+1]."""
+        if not isinstance(values, np.ndarray) or values.dtype != np.float64 or not values.flags.c_contiguous:
+            raise DimensionError("BrownianPaths.upload: values must be a C-contiguous float64 array")
+        if values.shape != (self.M, self.steps + 1):
+            raise DimensionError(f"BrownianPaths.upload: values shape {values.shape} != "
+                                 f"{(self.M, self.steps + 1)}")
         _check(lib().s2b_paths_upload(self.h, k0, k1, _dptr(values)))
 
     def values(self):
@@ -531,7 +545,8 @@ class MagnusSession:
         h = C.c_void_p()
         _check(lib().s2b_magnus_session_create(comms.ctx.h, comms.h, C.byref(ccfg), _dptr(phi),
                                                batch.h, C.byref(h)))
-        self.h, self.ctx, self.grid, self.batch = h, comms.ctx, comms.grid, batch
+        # the C session borrows the operator and the paths: keep both alive as long as it
+        self.h, self.ctx, self.grid, self.batch, self.op = h, comms.ctx, comms.grid, batch, comms
 
     def advance(self, n_windows=1):
         _check(lib().s2b_magnus_session_advance(self.h, n_windows))

@@ -227,18 +227,24 @@ __global__ void init_kernel(Ctl c, int first_window) {
     if (c.status[p] == 2) return; // blown paths stay blown
     c.tn[p] = 0;
     c.sn[p] = 0;
-    if (first_window == 0) {
+    if (first_window == 0) { // the counters accumulate over the session (reset by session_reset)
         c.par[p] = 0;
         c.rec_next[p] = 0;
-        c.terms[p] = 0;
-        c.windows[p] = 0;
-        c.segments[p] = 0;
     }
     if (enter_window(c, p, first_window, c.par[p])) c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
 }
 
 // After a pass: evaluate the stopping rule of expmv_into (sparse.cpp:463-492) and the
 // window-level blow-up rule of solve_iterated_magnus (magnus.cpp:277-291) per live path.
+// solve_iterated_magnus checks max|u| > cap after every window, including a zero-norm one
+// (magnus.cpp:277-286).  Before the first real window u is phi; after one, max|u| <= cap
+// was already checked.  So with max|phi| > cap a path whose first window has norm 0 is
+// BlownUp at once (no record written), and every other path proceeds unchanged.
+__global__ void phi_cap_kernel(const int* __restrict__ stab, int nwin, int* __restrict__ status, size_t M) {
+    const size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (p < M && status[p] == 0 && stab[p * nwin] == 0) status[p] = 2;
+}
+
 __global__ void control_kernel(Ctl c) {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= c.cnt[0]) return;
@@ -731,6 +737,8 @@ struct MagnusSession {
     bool timing = false;
     bool use_cluster = false; // cluster-resident engine (cluster_magnus.cu) for this operator
     bool external_prepare = false; // ctab/stab written by the caller (adaptive driver)
+    bool phi_over_cap = false;     // max|phi| > blowup_norm_cap (zero-norm first windows blow up)
+    bool finished = false;         // finish() moved the buffers out: every later call is refused
     std::vector<cudaEvent_t> ev;
     s2b_magnus_stats stats{};
 
@@ -919,6 +927,11 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
                 s->sx.alloc(cluster_xmi_scratch(static_cast<int>(op->nx), static_cast<int>(op->nv), &s->sx_slots));
         }
         s->phi.assign(phi, phi + n);
+        {
+            double mx = 0.0;
+            for (size_t i = 0; i < n; ++i) mx = std::max(mx, std::fabs(phi[i]));
+            s->phi_over_cap = mx > cfg->blowup_norm_cap;
+        }
         s->nz = true;
         for (size_t i = 0; i < n && s->nz; ++i) s->nz = !(phi[i] == 0.0 && std::signbit(phi[i]));
         const size_t M = s->M;
@@ -969,6 +982,7 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
 }
 
 void session_reset(MagnusSession* s) {
+    if (s->finished) fail(S2B_ERR_CONFIG, "magnus session: reset after finish (the buffers belong to the ensemble)");
     const size_t M = s->M, n = s->n;
     broadcast_rows(s->ctx, s->S[0].p, s->phi.data(), n, M);
     S2B_CUDA(cudaMemsetAsync(s->iv.p, 0, s->iv.bytes(), s->ctx->stream));
@@ -1002,6 +1016,11 @@ void prepare_windows(MagnusSession* s, size_t w0, size_t w1) {
         norm_kernel<<<static_cast<unsigned>(mc * nw), 256, 0, s->ctx->stream>>>(
             ov, s->bits.p, s->nbits, op->rx, s->ctab.p + m0 * s->nwin * 6, s->nwin, w0, nw,
             s->cfg.expmv_theta, s->stab.p + m0 * s->nwin, nullptr);
+        S2B_LAUNCHED(s->ctx);
+    }
+    if (w0 == 0 && s->phi_over_cap) {
+        phi_cap_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, s->ctx->stream>>>(
+            s->stab.p, static_cast<int>(s->nwin), s->iv.p + 4 * M, M);
         S2B_LAUNCHED(s->ctx);
     }
 }
@@ -1130,6 +1149,7 @@ void sessions_run_batched(MagnusSession* const* ss, int n) {
 }
 
 void session_advance(MagnusSession* s, size_t n_windows) {
+    if (s->finished) fail(S2B_ERR_CONFIG, "magnus session: advance after finish");
     if (n_windows == 0 || static_cast<size_t>(s->cur_window) >= s->nwin) return;
     const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
     if (!s->external_prepare) prepare_windows(s, s->cur_window, stop);
@@ -1230,6 +1250,7 @@ void session_advance(MagnusSession* s, size_t n_windows) {
 }
 
 void session_stats(const MagnusSession* s, s2b_magnus_stats* out) {
+    if (s->finished) fail(S2B_ERR_CONFIG, "magnus session: stats after finish (read them from the ensemble)");
     *out = s->stats;
     std::vector<long long> t(s->M), w(s->M);
     S2B_CUDA(cudaMemcpy(t.data(), s->terms.p, s->M * sizeof(long long), cudaMemcpyDeviceToHost));
@@ -1273,6 +1294,7 @@ __global__ void live_status_kernel(const int* __restrict__ status, uint8_t* __re
 } // namespace
 
 s2b_ensemble* session_snapshot(MagnusSession* s) {
+    if (s->finished) fail(S2B_ERR_CONFIG, "magnus session: snapshot after finish");
     auto* e = new s2b_ensemble();
     e->ctx = s->ctx;
     e->R = 1;
@@ -1298,6 +1320,7 @@ s2b_ensemble* session_snapshot(MagnusSession* s) {
 }
 
 s2b_ensemble* session_finish(MagnusSession* s) {
+    if (s->finished) fail(S2B_ERR_CONFIG, "magnus session: finish called twice");
     if (static_cast<size_t>(s->cur_window) < s->nwin) session_advance(s, s->nwin - s->cur_window);
     auto* e = new s2b_ensemble();
     e->ctx = s->ctx;
@@ -1320,6 +1343,7 @@ s2b_ensemble* session_finish(MagnusSession* s) {
     e->status = std::move(s->rec_status);
     e->terms = std::move(s->terms);
     e->windows = std::move(s->windows);
+    s->finished = true;
     S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
     return e;
 }
@@ -1359,6 +1383,7 @@ __global__ void moments_finish_kernel(const double* __restrict__ part, size_t nc
 } // namespace
 
 void session_moments(MagnusSession* s, double* host_out, double* live_out) {
+    if (s->finished) fail(S2B_ERR_CONFIG, "magnus session: moments after finish");
     const size_t nch = (s->M + kMomChunk - 1) / kMomChunk;
     if (s->mom_part.n < nch * 2 * s->n) s->mom_part.alloc(nch * 2 * s->n);
     if (s->mom.n < 2 * s->n) s->mom.alloc(2 * s->n);

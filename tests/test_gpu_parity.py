@@ -376,3 +376,30 @@ def test_config_errors_mirror_reference(s2b, ctx):
 def test_smoke_entry(s2b):
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# BASELINE cfg3 at its exact grid (256^2, dt = 0.01, dt_leb = 1e-4): the engines bench.py
+# --config cfg3 / cfg3k time (term_var_kernel with TMA weight rows and the largest ring;
+# term_varx_kernel at the kinetic family's 64 source pairs), two windows plus a record.
+@pytest.mark.parametrize("kind,order,pairs", [("langevin-variable", 2, 15), ("langevin-variable", 3, 39),
+                                              ("kinetic", 2, 24), ("kinetic", 3, 64)])
+def test_magnus_cfg3_grid_bitwise(ref, s2b, ctx, kind, order, pairs):
+    from fieldsets import kinetic_fields
+    d, T, dt_leb, dt, M, seed = 256, 0.02, 1e-4, 0.01, 4, 303 + order
+    fields = kinetic_fields(d) if kind == "kinetic" else None
+    family = "fields" if kind == "kinetic" else kind
+    ops = ref.Ops(family, d, order=order, fields=fields)
+    values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
+    want, wst, _ = ops.solve_magnus(values, dt_leb, T, dt, record_times=[dt], seed=seed)
+    g = s2b.GridSpec.square(d)
+    op = s2b.Operator.from_family(g, family, order=order, fields=fields, ctx=ctx)
+    info = op.info()
+    assert not info["compressed"] and info["pairs"] == pairs
+    paths = s2b.BrownianPaths.from_values(values, dt_leb, seed=seed, ctx=ctx)
+    stats = {}
+    ens = s2b.solve_iterated_magnus(s2b.MagnusConfig(order=order, dt=dt, record_times=[dt]), op,
+                                    ops.datum(), paths, T, g, stats=stats)
+    assert stats["engine"] == 0  # the streaming pass engine (term_var / term_varx)
+    for r, e in enumerate(ens):
+        assert np.array_equal(e.status, wst[r])
+        assert np.array_equal(e.states(), want[r], equal_nan=True)

@@ -162,3 +162,23 @@ def test_bench_reference_arm_contract(tmp_path):
     env.update(RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=tmp_path, timeout=120)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_python_mirror_validates_host_buffers(s2b):
+    """Shapes/dtypes are checked before any pointer reaches C (no silent reinterpretation)."""
+    g = s2b.GridSpec.square(8)
+    with pytest.raises(s2b.DimensionError):
+        s2b.HostOps(g, "fields", fields={"h": np.ones(63)})
+    with pytest.raises(s2b.ConfigError):
+        s2b.HostOps(g, "fields", fields={"bogus": np.ones(64)})
+    s2b.HostOps(g, "fields", fields={"h": np.ones(64), "sig": np.ones((8, 8))})
+    p = object.__new__(s2b.BrownianPaths)
+    p.h, p.M, p.steps = None, 2, 4
+    with pytest.raises(s2b.DimensionError):
+        p.upload(0, 4, np.zeros((2, 4)))
+    with pytest.raises(s2b.DimensionError):
+        p.upload(0, 4, np.zeros((2, 5), np.float32))
+    with pytest.raises(s2b.DimensionError):
+        p.upload(0, 4, np.zeros((5, 2)).T)
+    with pytest.raises(s2b.DimensionError):
+        s2b.BrownianPaths.from_values(np.zeros(5), 1e-3)
