@@ -21,6 +21,8 @@
  *                               ensemble is materialised), plus moment sums for the
  *                               cross-GPU allreduce
  *   s2b_expmv                <- expmv_into on a general CSR matrix (sparse.hpp:149-151)
+ *   s2b_expmv_into           <- expmv_into + ExpmvWorkspace + ExpmvReport (sparse.hpp:106-151)
+ *   s2b_euler_step           <- euler_step_into / euler_step (euler.hpp:19-40, euler.cpp:18-86)
  *
  * Error codes mirror the reference's exception classes (errors.hpp:10-19):
  * S2B_ERR_CONFIG <-> ConfigError, S2B_ERR_DIMENSION <-> DimensionError,
@@ -266,6 +268,46 @@ int s2b_exact_errors(s2b_context *ctx, const s2b_ensemble *app, size_t app_recor
 /* ---- general expmv ------------------------------------------------------------ */
 int s2b_expmv(s2b_context *ctx, const s2b_csr *m, const double *x, double tol, double theta,
               double *y, int report[4]);
+
+/* ---- kernel level: expmv_into with a workspace (sparse.hpp:106-151) ------------
+ * s2b_expmv_workspace <- ExpmvWorkspace (sparse.hpp:121-130): caller-owned scratch that
+ * caches the device copy of the last pattern (row_ptr / col_idx compared exactly), so a
+ * MagnusLogBuilder refill only moves the values.  One cooperative launch per call runs the
+ * whole segmented Taylor series (no host round trip per term).
+ * s2b_expmv_into <- expmv_into (sparse.hpp:149-151, sparse.cpp:427-503): y = exp(M) x
+ * (host x and y, n = m->rows doubles), report as ExpmvReport: status 0 Ok / 1 Overflow /
+ * 2 ToleranceNotReached, residual = the achieved last-term/result ratio (max over segments;
+ * the last ratio on ToleranceNotReached; +inf on Overflow), segments, max_terms, plus the
+ * total Taylor terms applied.  On Overflow / ToleranceNotReached y holds the result of the
+ * completed segments, as the reference's y does.
+ * s2b_expmv_into_device: the same with x and y in device memory (no copies of the vectors). */
+typedef struct s2b_expmv_workspace s2b_expmv_workspace;
+typedef struct {
+    int status;
+    double residual;
+    int segments;
+    int max_terms;
+    int64_t terms;
+} s2b_expmv_report;
+int s2b_expmv_workspace_create(s2b_context *ctx, s2b_expmv_workspace **out);
+int s2b_expmv_workspace_destroy(s2b_expmv_workspace *ws);
+int s2b_expmv_into(s2b_expmv_workspace *ws, const s2b_csr *m, const double *x, double tol,
+                   double theta, double *y, s2b_expmv_report *report);
+int s2b_expmv_into_device(s2b_expmv_workspace *ws, const s2b_csr *m, const double *d_x, double tol,
+                          double theta, double *d_y, s2b_expmv_report *report);
+
+/* ---- kernel level: one Euler-Maruyama step (euler.hpp:19-40, euler.cpp:18-86) ------
+ * stencils[5] = EulerStencils {inv2dx, invdx2, inv2dv, invdv2, inv4dxdv} as the caller
+ * passes them (NULL: EulerStencils::from_grid of the fields' grid).
+ * s2b_euler_step <- euler_step_into: out = one explicit step of u (host fields of nx*nv
+ * doubles, column-major) with increment dW; *maxabs (NULL-able) = max|out| with the
+ * reference's std::max semantics (NaN entries ignored).
+ * s2b_euler_step_device: M fields at once in device memory ([M][n] in, [M][n] out), dW[M]
+ * and maxabs[M] (NULL-able) on the host. */
+int s2b_euler_step(const s2b_fields *f, const double *stencils, const double *u, double *out,
+                   double dW, double dt, double *maxabs);
+int s2b_euler_step_device(const s2b_fields *f, const double *stencils, const double *d_u,
+                          double *d_out, size_t M, const double *dW, double dt, double *maxabs);
 
 #ifdef __cplusplus
 }

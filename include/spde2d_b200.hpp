@@ -16,11 +16,14 @@
 #include <cstdint>
 #include <functional>
 #include <iosfwd>
+#include <memory>
 #include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+struct s2b_expmv_workspace; // device scratch of ExpmvWorkspace (spde2d_b200.h)
 
 namespace spde2d {
 
@@ -144,7 +147,22 @@ private:
     ExpmvStatus status_;
     double residual_;
 };
-// exp(M) x on the GPU (the segmented-Taylor rule of the reference sparse.hpp:144-155).
+// ExpmvWorkspace (sparse.hpp:121-130): caller-owned scratch reused across expmv_into calls.
+// On the B200 it owns the device buffers and caches the device copy of the last matrix
+// pattern (row_ptr / col_idx compared exactly), so a refill of the same pattern (the
+// MagnusLogBuilder case) only uploads the values.  Created on first use; copies share the
+// device scratch, so keep one workspace per thread as the reference's solvers do.
+struct ExpmvWorkspace {
+    std::shared_ptr<s2b_expmv_workspace> device;
+    std::int64_t terms = 0; // Taylor terms the last call applied (all segments)
+};
+// expmv_into (sparse.hpp:144-151): y = exp(M) x by the segmented truncated Taylor series,
+// one cooperative GPU launch per call; the report (status, residual = achieved
+// last-term/result ratio, segments, max_terms) is the reference's.
+ExpmvReport expmv_into(const SparseView& m, std::span<const double> x, std::vector<double>& y,
+                       double tol, double theta, ExpmvWorkspace& ws);
+// exp(M) x on the GPU (the segmented-Taylor rule of the reference sparse.hpp:153-155);
+// throws ExpmvError carrying the residual on Overflow / ToleranceNotReached.
 std::vector<double> expmv(const SparseMatrix& m, std::span<const double> v, double tol,
                           double theta = 1.0);
 
@@ -282,6 +300,32 @@ struct SolutionEnsemble {
 SparseMatrix magnus_log(int order, const CommutatorSet& comms, const ItoFunctionals& f);
 std::vector<double> magnus_step(const SparseMatrix& y, std::span<const double> u, double tol);
 
+// MagnusLogBuilder (magnus.hpp:61-86): the union pattern of the logarithm's source matrices,
+// built once, and per window a refill of its values -- host-kept setup (the GPU solvers fold
+// Y inside their kernels and never materialise it); fill's arithmetic is the reference's:
+// values from 0.0, += c_s * w_s over the slots in order B, A, A2, BA, BAA, BAB, slots with
+// c_s == 0 skipped.  The builder borrows `comms`: it must outlive the builder.
+class MagnusLogBuilder {
+public:
+    MagnusLogBuilder(const CommutatorSet& comms, int order);
+    std::size_t dim() const { return rows_; }
+    std::size_t nnz() const { return cols_.size(); }
+    void fill(int order, const ItoFunctionals& f, std::vector<double>& values) const;
+    SparseView view_with(std::span<const double> values) const;
+
+private:
+    std::size_t rows_ = 0;
+    int order_ = 1;
+    std::vector<std::size_t> row_start_;
+    std::vector<std::int32_t> cols_;
+    struct Part {
+        int slot = 0;
+        const SparseMatrix* matrix = nullptr;
+        std::vector<std::size_t> to_union; // source entry -> union position
+    };
+    std::vector<Part> parts_;
+};
+
 std::vector<SolutionEnsemble> solve_iterated_magnus(const MagnusConfig& cfg,
                                                     const CommutatorSet& comms,
                                                     std::span<const double> phi,
@@ -301,6 +345,24 @@ struct EulerConfig {
     int threads = 0;
     std::vector<double> record_times;
 };
+
+// EulerStencils (euler.hpp:19-28): the finite-difference scales of one explicit step.
+struct EulerStencils {
+    double inv2dx = 0.0;
+    double invdx2 = 0.0;
+    double inv2dv = 0.0;
+    double invdv2 = 0.0;
+    double inv4dxdv = 0.0;
+    static EulerStencils from_grid(const GridSpec& grid);
+};
+// euler_step / euler_step_into (euler.hpp:30-40): one explicit E-M step of one field on the
+// GPU (the solver's per-point arithmetic); euler_step_into returns max|out| with the
+// reference's std::max semantics (NaN ignored).  The fields' device copy is cached per
+// thread and re-uploaded whenever their contents change.
+Field euler_step(const CoefficientFields& fields, const Field& u, double dW, double dt,
+                 const EulerStencils& stencils);
+double euler_step_into(const CoefficientFields& fields, const Field& u, Field& out, double dW,
+                       double dt, const EulerStencils& stencils);
 
 std::vector<SolutionEnsemble> solve_euler(const EulerConfig& cfg, const CoefficientFields& fields,
                                           const GridSpec& grid, const Field& phi,

@@ -31,7 +31,7 @@ __all__ = [
     "BrownianPaths", "MagnusConfig", "EulerConfig", "Ensemble", "MagnusSession",
     "solve_iterated_magnus", "solve_euler", "exact_reference", "central_region",
     "mean_rel_error", "mean_abs_error", "avg_mean_abs_error", "exact_errors", "gaussian_datum",
-    "expmv", "default_context",
+    "expmv", "default_context", "ExpmvWorkspace", "expmv_into", "EulerStencils", "euler_step",
 ]
 
 
@@ -682,3 +682,91 @@ def expmv(csr, x, tol, theta=1.0, ctx: Context = None, throw=True):
         raise ExpmvError(rep[0], "expmv: overflow" if rep[0] == 1 else
                          "expmv: tolerance not reached within term budget")
     return y, report
+
+
+# ---------------------------------------------------------------- kernel level
+def _csr_struct(csr):
+    rp = np.ascontiguousarray(csr[0], np.uint64)
+    ci = np.ascontiguousarray(csr[1], np.int32)
+    v = np.ascontiguousarray(csr[2], np.float64)
+    if rp.ndim != 1 or len(rp) < 1 or len(ci) != len(v) or int(rp[-1]) != len(v):
+        raise DimensionError("expmv: malformed CSR (row_ptr, col_idx, values)")
+    m = _capi.Csr(len(rp) - 1, rp.ctypes.data_as(C.POINTER(C.c_size_t)),
+                  ci.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(v))
+    return m, (rp, ci, v)
+
+
+_EXPMV_STATUS = {0: "Ok", 1: "Overflow", 2: "ToleranceNotReached"}
+
+
+class ExpmvWorkspace:
+    """ExpmvWorkspace (sparse.hpp:121-130): device scratch reused across expmv_into calls;
+    caches the device copy of the last CSR pattern (a refill of the same pattern only moves
+    the values)."""
+
+    def __init__(self, ctx: Context = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(lib().s2b_expmv_workspace_create(self.ctx.h, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().s2b_expmv_workspace_destroy(self.h)
+        except Exception:
+            pass
+
+
+def expmv_into(csr, x, tol, theta=1.0, ws: ExpmvWorkspace = None, y=None):
+    """expmv_into (sparse.hpp:149-151): returns (y, report) with the reference's ExpmvReport
+    fields (status, residual, segments, max_terms) plus the Taylor terms applied.  Never
+    raises on numerical failure (the status says it), like the reference."""
+    ws = ws or ExpmvWorkspace()
+    m, keep = _csr_struct(csr)
+    n = m.rows
+    x = np.ascontiguousarray(x, np.float64)
+    if x.shape != (n,):
+        raise DimensionError("expmv: vector length mismatch")
+    y = np.empty(n) if y is None else y
+    if y.dtype != np.float64 or y.shape != (n,) or not y.flags.c_contiguous:
+        raise DimensionError("expmv_into: y must be a contiguous float64 vector of length n")
+    rep = _capi.ExpmvReport()
+    _check(lib().s2b_expmv_into(ws.h, C.byref(m), _dptr(x), float(tol), float(theta), _dptr(y),
+                                C.byref(rep)))
+    return y, {"status": _EXPMV_STATUS[rep.status], "residual": rep.residual, "segments": rep.segments,
+               "max_terms": rep.max_terms, "terms": rep.terms}
+
+
+@dataclass
+class EulerStencils:
+    """EulerStencils (euler.hpp:19-28)."""
+    inv2dx: float = 0.0
+    invdx2: float = 0.0
+    inv2dv: float = 0.0
+    invdv2: float = 0.0
+    inv4dxdv: float = 0.0
+
+    @staticmethod
+    def from_grid(grid: GridSpec):
+        dx = (grid.bx - grid.ax) / float(grid.nx + 1)
+        dv = (grid.bv - grid.av) / float(grid.nv + 1)
+        return EulerStencils(1.0 / (2.0 * dx), 1.0 / (dx * dx), 1.0 / (2.0 * dv), 1.0 / (dv * dv),
+                             1.0 / (4.0 * dx * dv))
+
+    def c(self):
+        return (C.c_double * 5)(self.inv2dx, self.invdx2, self.inv2dv, self.invdv2, self.inv4dxdv)
+
+
+def euler_step(fields: Fields, u, dW, dt, stencils: EulerStencils = None):
+    """euler_step_into (euler.hpp:36-40): (out, max|out|) for one field u (n doubles,
+    column-major), on the GPU."""
+    n = fields.grid.dim()
+    u = np.ascontiguousarray(u, np.float64).reshape(-1)
+    if u.size != n:
+        raise DimensionError("euler_step: field shape mismatch")
+    out = np.empty(n)
+    mx = C.c_double()
+    st = (stencils or EulerStencils.from_grid(fields.grid)).c()
+    _check(lib().s2b_euler_step(fields.h, st, _dptr(u), _dptr(out), float(dW), float(dt), C.byref(mx)))
+    return out, mx.value

@@ -55,6 +55,11 @@ class MagnusStats(C.Structure):
                 ("engine", C.c_int32), ("hybrid_paths", C.c_int64)]
 
 
+class ExpmvReport(C.Structure):
+    _fields_ = [("status", C.c_int), ("residual", C.c_double), ("segments", C.c_int),
+                ("max_terms", C.c_int), ("terms", C.c_int64)]
+
+
 # Exported symbols with their ctypes signatures (restype int unless noted).
 _VP = C.c_void_p
 _P = C.POINTER
@@ -123,6 +128,16 @@ SIGNATURES = {
                                    _P(C.c_double)]),
     "s2b_expmv": (C.c_int, [_VP, _P(Csr), _P(C.c_double), C.c_double, C.c_double,
                             _P(C.c_double), _P(C.c_int)]),
+    "s2b_expmv_workspace_create": (C.c_int, [_VP, _P(_VP)]),
+    "s2b_expmv_workspace_destroy": (C.c_int, [_VP]),
+    "s2b_expmv_into": (C.c_int, [_VP, _P(Csr), _P(C.c_double), C.c_double, C.c_double,
+                                 _P(C.c_double), _P(ExpmvReport)]),
+    "s2b_expmv_into_device": (C.c_int, [_VP, _P(Csr), C.c_void_p, C.c_double, C.c_double,
+                                        C.c_void_p, _P(ExpmvReport)]),
+    "s2b_euler_step": (C.c_int, [_VP, _P(C.c_double), _P(C.c_double), _P(C.c_double), C.c_double,
+                                 C.c_double, _P(C.c_double)]),
+    "s2b_euler_step_device": (C.c_int, [_VP, _P(C.c_double), C.c_void_p, C.c_void_p, C.c_size_t,
+                                        _P(C.c_double), C.c_double, _P(C.c_double)]),
 }
 
 _lib = None

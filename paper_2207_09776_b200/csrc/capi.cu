@@ -638,4 +638,75 @@ int s2b_expmv(s2b_context* ctx, const s2b_csr* m, const double* x, double tol, d
     });
 }
 
+int s2b_expmv_workspace_create(s2b_context* ctx, s2b_expmv_workspace** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        *out = expmv_workspace_create(ctx);
+    });
+}
+
+int s2b_expmv_workspace_destroy(s2b_expmv_workspace* ws) {
+    return guard([&] { expmv_workspace_destroy(ws); });
+}
+
+int s2b_expmv_into(s2b_expmv_workspace* ws, const s2b_csr* m, const double* x, double tol, double theta,
+                   double* y, s2b_expmv_report* report) {
+    return guard([&] {
+        need(ws, "workspace");
+        need(m, "matrix");
+        need(report, "report");
+        if (m->rows) {
+            need(x, "x");
+            need(y, "y");
+        }
+        expmv_into(ws, m, x, tol, theta, y, report, false);
+    });
+}
+
+int s2b_expmv_into_device(s2b_expmv_workspace* ws, const s2b_csr* m, const double* d_x, double tol, double theta,
+                          double* d_y, s2b_expmv_report* report) {
+    return guard([&] {
+        need(ws, "workspace");
+        need(m, "matrix");
+        need(report, "report");
+        if (m->rows) {
+            need(d_x, "x");
+            need(d_y, "y");
+        }
+        expmv_into(ws, m, d_x, tol, theta, d_y, report, true);
+    });
+}
+
+int s2b_euler_step(const s2b_fields* f, const double* stencils, const double* u, double* out, double dW, double dt,
+                   double* maxabs) {
+    return guard([&] {
+        need(f, "fields");
+        need(u, "u");
+        need(out, "out");
+        const size_t n = f->nx * f->nv;
+        DevBuf<double> du(n), dout(n);
+        S2B_CUDA(cudaMemcpyAsync(du.p, u, n * sizeof(double), cudaMemcpyHostToDevice, f->ctx->stream));
+        double mx = 0.0;
+        euler_step_batch(f, stencils, du.p, dout.p, 1, &dW, dt, &mx);
+        S2B_CUDA(cudaMemcpyAsync(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost, f->ctx->stream));
+        S2B_CUDA(cudaStreamSynchronize(f->ctx->stream));
+        if (maxabs) *maxabs = mx;
+    });
+}
+
+int s2b_euler_step_device(const s2b_fields* f, const double* stencils, const double* d_u, double* d_out, size_t M,
+                          const double* dW, double dt, double* maxabs) {
+    return guard([&] {
+        need(f, "fields");
+        if (M) {
+            need(d_u, "u");
+            need(d_out, "out");
+            need(dW, "dW");
+        }
+        euler_step_batch(f, stencils, d_u, d_out, M, dW, dt, maxabs);
+    });
+}
+
 } // extern "C"

@@ -610,4 +610,77 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
     return e;
 }
 
+namespace {
+// max|out| per field with std::max semantics (euler.cpp:82): NaN never replaces the running
+// maximum; on bit patterns, a NaN's |bits| exceed +inf's and are skipped.
+__global__ void em_maxabs_kernel(const double* __restrict__ out, size_t n, unsigned long long* __restrict__ best) {
+    const size_t m = blockIdx.y;
+    unsigned long long b = 0;
+    for (size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(out[m * n + r])) & 0x7FFFFFFFFFFFFFFFULL;
+        if (v <= 0x7FF0000000000000ULL) b = max(b, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if ((threadIdx.x & 31) == 0 && b) atomicMax(&best[m], b);
+}
+} // namespace
+
+// euler_step_into (euler.cpp:28-86) for M device fields: em_step_kernel's per-point
+// arithmetic (the solver's general kernel) with dW = values[1] - values[0] for a
+// two-column prefix table {0, dW[m]} -- exactly dW[m] -- and the caller's stencil scales.
+void euler_step_batch(const s2b_fields* f, const double* st, const double* d_u, double* d_out, size_t M,
+                      const double* dW, double dt, double* maxabs) {
+    if (M == 0) return;
+    s2b_context* ctx = f->ctx;
+    S2B_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = f->nx * f->nv;
+    std::vector<double> vals(2 * M);
+    for (size_t m = 0; m < M; ++m) {
+        vals[2 * m] = 0.0;
+        vals[2 * m + 1] = dW[m];
+    }
+    DevBuf<double> dv(2 * M);
+    DevBuf<int> blown(M);
+    DevBuf<unsigned long long> best(M);
+    S2B_CUDA(cudaMemcpyAsync(dv.p, vals.data(), vals.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(blown.p, 0, blown.bytes(), ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(best.p, 0, best.bytes(), ctx->stream));
+    EmArgs a{};
+    a.f = f->d_f.p;
+    a.mask = f->mask;
+    a.nx = static_cast<int>(f->nx);
+    a.nv = static_cast<int>(f->nv);
+    std::copy(st ? st : f->st, (st ? st : f->st) + 5, a.st);
+    a.dt = dt;
+    a.values = dv.p;
+    a.vstride = 2;
+    a.k0 = 0;
+    a.k1 = 1;
+    a.in = d_u;
+    a.out = d_out;
+    a.blown = blown.p;
+    a.M = M;
+    dim3 grid(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64)), static_cast<unsigned>(std::min<size_t>(M, 65535)));
+    if (f->mask & 16)
+        em_step_kernel<true><<<grid, 256, 0, ctx->stream>>>(a);
+    else
+        em_step_kernel<false><<<grid, 256, 0, ctx->stream>>>(a);
+    S2B_LAUNCHED(ctx);
+    if (maxabs) {
+        for (size_t m0 = 0; m0 < M; m0 += 65535) {
+            const size_t mc = std::min<size_t>(M - m0, 65535);
+            em_maxabs_kernel<<<dim3(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 32)), static_cast<unsigned>(mc)), 256, 0,
+                               ctx->stream>>>(d_out + m0 * n, n, best.p + m0);
+            S2B_LAUNCHED(ctx);
+        }
+        std::vector<unsigned long long> hb(M);
+        S2B_CUDA(cudaMemcpyAsync(hb.data(), best.p, M * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+        S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (size_t m = 0; m < M; ++m) std::memcpy(&maxabs[m], &hb[m], sizeof(double));
+    } else {
+        S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+}
+
 } // namespace s2b

@@ -260,18 +260,109 @@ Field exact_langevin_field(const GridSpec& grid, double t, const LangevinParams&
     return f;
 }
 
+ExpmvReport expmv_into(const SparseView& m, std::span<const double> x, std::vector<double>& y, double tol,
+                       double theta, ExpmvWorkspace& ws) {
+    if (m.rows != m.cols) throw DimensionError("expmv: matrix must be square");
+    if (x.size() != m.cols) throw DimensionError("expmv: vector length mismatch");
+    if (m.row_ptr.size() != m.rows + 1 || m.col_idx.size() != m.values.size() ||
+        (m.rows && m.row_ptr[m.rows] != m.values.size()))
+        throw DimensionError("expmv: malformed CSR view");
+    if (!ws.device) {
+        s2b_expmv_workspace* w = nullptr;
+        check(s2b_expmv_workspace_create(context(), &w));
+        ws.device = std::shared_ptr<s2b_expmv_workspace>(w, [](s2b_expmv_workspace* q) { s2b_expmv_workspace_destroy(q); });
+    }
+    const s2b_csr c{m.rows, m.row_ptr.data(), m.col_idx.data(), m.values.data()};
+    y.resize(x.size());
+    s2b_expmv_report r{};
+    check(s2b_expmv_into(ws.device.get(), &c, x.data(), tol, theta, y.data(), &r));
+    ws.terms = r.terms;
+    ExpmvReport out;
+    out.status = r.status == 0 ? ExpmvStatus::Ok : (r.status == 1 ? ExpmvStatus::Overflow : ExpmvStatus::ToleranceNotReached);
+    out.residual = r.residual;
+    out.segments = r.segments;
+    out.max_terms = r.max_terms;
+    return out;
+}
+
 std::vector<double> expmv(const SparseMatrix& m, std::span<const double> v, double tol, double theta) {
-    if (m.rows() != m.cols()) throw DimensionError("expmv: matrix must be square");
-    if (v.size() != m.cols()) throw DimensionError("expmv: vector length mismatch");
-    const s2b_csr c = c_csr(m);
-    std::vector<double> y(v.size());
-    int rep[4];
-    check(s2b_expmv(context(), &c, v.data(), tol, theta, y.data(), rep));
-    if (rep[0] == 1) throw ExpmvError(ExpmvStatus::Overflow, std::numeric_limits<double>::infinity(),
-                                      "expmv: overflow (non-finite intermediate)");
-    if (rep[0] == 2)
-        throw ExpmvError(ExpmvStatus::ToleranceNotReached, 0.0, "expmv: tolerance not reached within term budget");
+    ExpmvWorkspace ws;
+    std::vector<double> y;
+    const ExpmvReport rep = expmv_into(m.view(), v, y, tol, theta, ws);
+    if (rep.status == ExpmvStatus::Overflow)
+        throw ExpmvError(rep.status, rep.residual, "expmv: overflow (non-finite intermediate)");
+    if (rep.status == ExpmvStatus::ToleranceNotReached)
+        throw ExpmvError(rep.status, rep.residual,
+                         "expmv: tolerance not reached within term budget, residual " + std::to_string(rep.residual));
     return y;
+}
+
+namespace {
+// Device copy of the CoefficientFields the last euler_step_into call on this thread used;
+// reused while the fields' contents (and shape) are unchanged, compared exactly.
+struct StepFields {
+    std::vector<double> data; // the non-zero fields, in field order
+    int mask = -1;
+    std::size_t nx = 0, nv = 0;
+    s2b_fields* dev = nullptr;
+    ~StepFields() {
+        if (dev) s2b_fields_destroy(dev);
+    }
+};
+
+s2b_fields* step_fields(const CoefficientFields& f, std::size_t nx, std::size_t nv) {
+    thread_local StepFields cache;
+    const Field* all[9] = {&f.h, &f.fx, &f.fv, &f.gxx, &f.gxv, &f.gvv, &f.sig, &f.sigx, &f.sigv};
+    const bool zero[9] = {f.zero_h,   f.zero_fx,  f.zero_fv,  f.zero_gxx, f.zero_gxv,
+                          f.zero_gvv, f.zero_sig, f.zero_sigx, f.zero_sigv};
+    const std::size_t n = nx * nv;
+    int mask = 0;
+    for (int k = 0; k < 9; ++k) {
+        if (zero[k]) continue;
+        if (all[k]->nx() != nx || all[k]->nv() != nv) throw DimensionError("euler_step: coefficient field shape mismatch");
+        mask |= 1 << k;
+    }
+    bool same = cache.dev && cache.mask == mask && cache.nx == nx && cache.nv == nv;
+    for (int k = 0, q = 0; k < 9 && same; ++k)
+        if (mask >> k & 1) same = std::memcmp(cache.data.data() + n * q++, all[k]->data().data(), n * sizeof(double)) == 0;
+    if (same) return cache.dev;
+    if (cache.dev) {
+        s2b_fields_destroy(cache.dev);
+        cache.dev = nullptr;
+    }
+    cache.data.clear();
+    const double* f9[9] = {};
+    for (int k = 0; k < 9; ++k)
+        if (mask >> k & 1) {
+            f9[k] = all[k]->data().data();
+            cache.data.insert(cache.data.end(), all[k]->data().begin(), all[k]->data().end());
+        }
+    // the grid only fixes the shape here: the step takes the caller's stencil scales
+    const s2b_grid g{-1.0, 1.0, nx, -1.0, 1.0, nv};
+    check(s2b_fields_create(context(), &g, f9, &cache.dev));
+    cache.mask = mask;
+    cache.nx = nx;
+    cache.nv = nv;
+    return cache.dev;
+}
+} // namespace
+
+double euler_step_into(const CoefficientFields& fields, const Field& u, Field& out, double dW, double dt,
+                       const EulerStencils& st) {
+    const std::size_t nx = u.nx(), nv = u.nv();
+    if (out.nx() != nx || out.nv() != nv) throw DimensionError("euler_step: output shape mismatch");
+    if (nx * nv == 0) return 0.0;
+    s2b_fields* f = step_fields(fields, nx, nv);
+    const double s5[5] = {st.inv2dx, st.invdx2, st.inv2dv, st.invdv2, st.inv4dxdv};
+    double mx = 0.0;
+    check(s2b_euler_step(f, s5, u.data().data(), out.data().data(), dW, dt, &mx));
+    return mx;
+}
+
+Field euler_step(const CoefficientFields& fields, const Field& u, double dW, double dt, const EulerStencils& st) {
+    Field out(u.nx(), u.nv());
+    euler_step_into(fields, u, out, dW, dt, st);
+    return out;
 }
 
 } // namespace spde2d

@@ -654,6 +654,90 @@ SparseMatrix magnus_log(int order, const CommutatorSet& comms, const ItoFunction
     return y;
 }
 
+// ---- MagnusLogBuilder (magnus.hpp:61-86, magnus.cpp:88-164) ------------------------------
+namespace {
+int first_order_of(int slot) { return slot < 2 ? 1 : (slot < 4 ? 2 : 3); }
+
+// log_coefficients (magnus.cpp:26-40): weights of B, A, A2, [B,A], [[B,A],A], [[B,A],B]
+void log_weights(int order, const ItoFunctionals& f, double c[6]) {
+    const double h = f.h;
+    c[0] = h;
+    c[1] = f.W;
+    c[2] = order >= 2 ? -0.5 * h : 0.0;
+    c[3] = order >= 2 ? f.IW - 0.5 * h * f.W : 0.0;
+    c[4] = order >= 3 ? 0.5 * f.IW2 - 0.5 * f.W * f.IW + h * f.W * f.W / 12.0 : 0.0;
+    c[5] = order >= 3 ? f.IsW - 0.5 * h * f.IW - h * h * f.W / 12.0 : 0.0;
+}
+} // namespace
+
+MagnusLogBuilder::MagnusLogBuilder(const CommutatorSet& comms, int order) : order_(order) {
+    if (order < 1 || order > 3 || order > comms.order) throw ConfigError("MagnusLogBuilder: unsupported order");
+    rows_ = comms.B.rows();
+    const SparseMatrix* by_slot[6] = {&comms.B, &comms.A, &comms.A2, &comms.BA, &comms.BAA, &comms.BAB};
+    for (int slot = 0; slot < 6; ++slot) {
+        if (first_order_of(slot) > order) continue;
+        if (by_slot[slot]->rows() != rows_) throw DimensionError("MagnusLogBuilder: source dimension mismatch");
+        Part p;
+        p.slot = slot;
+        p.matrix = by_slot[slot];
+        p.to_union.resize(p.matrix->nnz());
+        parts_.push_back(std::move(p));
+    }
+    // per row: every (column, part, entry) of the participating sources, ordered by column;
+    // each distinct column is one union entry, and every source entry learns its position
+    struct Hit {
+        std::int32_t col;
+        std::uint32_t part;
+        std::size_t entry;
+    };
+    std::vector<Hit> hits;
+    row_start_.assign(rows_ + 1, 0);
+    for (std::size_t r = 0; r < rows_; ++r) {
+        hits.clear();
+        for (std::uint32_t q = 0; q < parts_.size(); ++q) {
+            const auto rp = parts_[q].matrix->row_ptr();
+            const auto ci = parts_[q].matrix->col_idx();
+            for (std::size_t k = rp[r]; k < rp[r + 1]; ++k) hits.push_back(Hit{ci[k], q, k});
+        }
+        std::sort(hits.begin(), hits.end(), [](const Hit& a, const Hit& b) { return a.col < b.col; });
+        for (std::size_t h = 0; h < hits.size(); ++h) {
+            if (h == 0 || hits[h].col != hits[h - 1].col) cols_.push_back(hits[h].col);
+            parts_[hits[h].part].to_union[hits[h].entry] = cols_.size() - 1;
+        }
+        row_start_[r + 1] = cols_.size();
+    }
+}
+
+void MagnusLogBuilder::fill(int order, const ItoFunctionals& f, std::vector<double>& values) const {
+    if (order < 1 || order > order_) throw ConfigError("MagnusLogBuilder::fill: order exceeds builder order");
+    double c[6];
+    log_weights(order, f, c);
+    values.assign(cols_.size(), 0.0);
+    for (const Part& p : parts_) { // slot order: every union entry folds its sources in that order
+        if (first_order_of(p.slot) > order) continue;
+        const double coef = c[p.slot];
+        if (coef == 0.0) continue;
+        const auto w = p.matrix->values();
+        for (std::size_t k = 0; k < w.size(); ++k) values[p.to_union[k]] += coef * w[k];
+    }
+}
+
+SparseView MagnusLogBuilder::view_with(std::span<const double> values) const {
+    return SparseView{rows_, rows_, row_start_, cols_, values};
+}
+
+// ---- EulerStencils::from_grid (euler.cpp:18-26) ----------------------------------------
+EulerStencils EulerStencils::from_grid(const GridSpec& grid) {
+    const double dx = grid.x.delta, dv = grid.v.delta;
+    EulerStencils st;
+    st.inv2dx = 1.0 / (2.0 * dx);
+    st.invdx2 = 1.0 / (dx * dx);
+    st.inv2dv = 1.0 / (2.0 * dv);
+    st.invdv2 = 1.0 / (dv * dv);
+    st.inv4dxdv = 1.0 / (4.0 * dx * dv);
+    return st;
+}
+
 // ---- gamma0 (exact_langevin.cpp:20-27) --------------------------------------------
 double gamma0(double t, double x, double v, const LangevinParams& p) {
     if (!(p.a > 0.0) || p.sigma < 0.0 || !(p.gap() > 0.0))

@@ -192,6 +192,12 @@ void errors(s2b_context* ctx, const s2b_ensemble* ref, size_t ref_record, const 
 void exact_errors(s2b_context* ctx, const s2b_ensemble* app, size_t app_record, double a, double sigma,
                   const s2b_paths* paths, int kappa, s2b_error_stats* out, double* me_out,
                   double* per_path_rel, double* moments);
+s2b_expmv_workspace* expmv_workspace_create(s2b_context* ctx);
+void expmv_workspace_destroy(s2b_expmv_workspace* ws);
+void expmv_into(s2b_expmv_workspace* ws, const s2b_csr* m, const double* x, double tol, double theta, double* y,
+                s2b_expmv_report* rep, bool device);
+void euler_step_batch(const s2b_fields* f, const double* st, const double* d_u, double* d_out, size_t M,
+                      const double* dW, double dt, double* maxabs);
 void expmv_csr(s2b_context* ctx, const s2b_csr* m, const double* x, double tol, double theta, double* y,
                int report[4]);
 

@@ -88,13 +88,13 @@ def test_adaptive_counters_do_not_depend_on_the_engine(s2b, ctx, monkeypatch):
     accumulate the Taylor terms of every order-3 and order-2 attempt."""
     g, _, paths = _setup(s2b, ctx, d=64, M=4, T=0.2, seed=17)
     op = s2b.Operator.from_family(g, "langevin-constant", order=3, ctx=ctx)
-    cfg = s2b.MagnusConfig(order=3, dt=0.1, adaptive=s2b.AdaptiveConfig(enabled=True, tolerance=1e-9))
+    cfg = s2b.MagnusConfig(order=3, dt=0.1, adaptive=s2b.AdaptiveConfig(enabled=True, tolerance=1e-6))
     phi = s2b.gaussian_datum(g)
     st_cl, st_sm = {}, {}
     a = s2b.solve_adaptive_magnus(cfg, op, phi, paths, 0.2, g, stats=st_cl)[-1].states()
     monkeypatch.setenv("S2B_ENGINE", "stream")
     b = s2b.solve_adaptive_magnus(cfg, op, phi, paths, 0.2, g, stats=st_sm)[-1].states()
-    assert np.array_equal(a, b)
+    assert np.array_equal(a, b, equal_nan=True)
     assert st_sm["engine"] == 0 and st_cl["engine"] != 0
     assert st_cl["path_terms"] == st_sm["path_terms"] > 0
     assert st_cl["path_segments"] == st_sm["path_segments"] > 0

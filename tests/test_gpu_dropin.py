@@ -128,3 +128,28 @@ def test_run_stepsize_sweep_byte_identical(tmp_path):
     hdr = a.splitlines()[0].split(",")
     tcols = [c for c in hdr if c.startswith("time")]
     assert tcols and _mask_time(a, tcols) == _mask_time(b, tcols)
+
+
+UNIT_B200 = os.path.join(ROOT, "build", "dropin", "unit_b200")
+BENCH_B200 = os.path.join(ROOT, "build", "dropin", "bench_kernels_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(UNIT_B200), reason="drop-in unit suite not built")
+def test_reference_unit_suite_on_b200():
+    """The reference's own doctest suite (proj/tests/test_*.cpp, 83 test cases), compiled
+    unchanged against include/spde2d_b200.hpp (tests/cpp/compat/doctest.h for the un-shipped
+    vendor header): every case passes on the B200 library, as on the reference library."""
+    r = subprocess.run([UNIT_B200], capture_output=True, text=True, timeout=1500)
+    tail = r.stdout[-600:] + r.stderr[-3000:]
+    assert "test cases: 83 | 83 passed | 0 failed" in r.stdout, tail
+    assert r.returncode == 0, tail
+
+
+@pytest.mark.skipif(not os.path.exists(BENCH_B200), reason="drop-in kernel benchmark not built")
+def test_reference_kernel_benchmark_on_b200():
+    """The reference's benchmarks/bench_kernels.cpp (MagnusLogBuilder + view_with, spmv,
+    ExpmvWorkspace + expmv_into, both solvers) compiled unchanged and run on the B200 library."""
+    r = subprocess.run([BENCH_B200], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    for key in ("spmv (csr reference)", "expmv (dia fast path)", "magnus order 3", "euler dt=1e-4"):
+        assert key in r.stdout, r.stdout
