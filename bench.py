@@ -109,6 +109,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-north-star", action="store_true", help="skip the cfg4 (512^2) sub-measurement")
     ap.add_argument("--euler-steps", type=int, default=200, help="E-M steps timed beside Magnus (0 = skip)")
     ap.add_argument("--config", default=None, choices=sorted(PRESETS),
                     help="BASELINE.json workload preset (cfg2 is the default workload); explicit flags win")
@@ -142,6 +143,20 @@ PRESETS = {
               "family": "kinetic-variable"},
     "cfg5": {"d": 1024, "paths": 4096, "dt": 5e-4, "dt_leb": 1e-5, "T": 0.005, "order": 3,
              "family": "langevin-constant", "steps": 3, "warmup": 3, "euler_steps": 100},
+}
+
+
+# ncu captures in profiles/ per (preset, family, engine): bench.py takes `traffic` from one only
+# when its recorded mangled kernel name equals the kernel this run launched
+PROFILE_OF = {
+    ("cfg2", "langevin-constant", "cluster-xm"): "r02_xm_cfg2_ncu.json",
+    ("cfg4", "langevin-constant", "cluster-xmi"): "r02_xmi_cfg4_ncu.json",
+    ("cfg3", "langevin-variable", "stream"): "r02_term_var_cfg3_ncu.json",
+    ("cfg3k", "kinetic-variable", "stream"): "r02_term_varx_cfg3k_ncu.json",
+    ("cfg5", "langevin-constant", "stream"): "r02_term_tma_cfg5_ncu.json",
+    ("cfg5", "langevin-variable", "stream"): "r02_term_varx_cfg5var_ncu.json",
+    ("hybrid", 256): "r02_term_tma_hybrid256_ncu.json",
+    ("hybrid", 512): "r02_term_tma_hybrid512_ncu.json",
 }
 
 
@@ -207,9 +222,15 @@ class ClockSampler:
 
 
 def dist_setup(gpus):
+    """One process per GPU.  `--gpus N` without a launcher re-executes this script under
+    torch.distributed.run with N local ranks; a world size that differs from --gpus is an error
+    (never a silently mislabelled one-GPU number)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        print(json.dumps({"error": f"--gpus {gpus} but WORLD_SIZE={world}"}), file=sys.stderr, flush=True)
+        raise SystemExit(2)
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -217,6 +238,18 @@ def dist_setup(gpus):
         dist.init_process_group("nccl")
         return rank, local, world, dist
     return 0, 0, 1, None
+
+
+def self_spawn(args):
+    """`python bench.py --gpus N` (N > 1, no WORLD_SIZE): run N ranks on this node."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def max_over_ranks(x, dist, local):
@@ -251,6 +284,18 @@ def cpu_reference_leg(args, n_paths, windows, reps=1):
     return times, threads
 
 
+CPU_WINDOWS = 3  # windows per CPU sample: the per-call setup (MagnusLogBuilder, ensembles) is amortised
+
+
+def cpu_setup_estimate(args, M_cpu):
+    """Per-call setup of the reference's solve (MagnusLogBuilder union build, ensemble allocation,
+    thread start): t(1 window) - (t(3 windows) - t(1 window)) / 2, best of two each."""
+    t1 = min(cpu_reference_leg(args, M_cpu, 1, reps=2)[0])
+    t3 = min(cpu_reference_leg(args, M_cpu, 3, reps=2)[0])
+    per_window = (t3 - t1) / 2.0
+    return max(0.0, t1 - per_window), per_window
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -258,22 +303,26 @@ def run_reference(args):
     nproc = os.cpu_count() or 1
     n = args.d * args.d
     M_cpu = max(2, nproc)
-    times, threads = cpu_reference_leg(args, M_cpu, 1, reps=args.warmup + args.steps)
+    times, threads = cpu_reference_leg(args, M_cpu, CPU_WINDOWS, reps=args.warmup + args.steps)
     timed = times[args.warmup:]
     total = sum(timed)
-    value = M_cpu * n * len(timed) / total
+    value = M_cpu * n * CPU_WINDOWS * len(timed) / total
+    setup_s, per_window_s = cpu_setup_estimate(args, M_cpu)
     line = {
         "metric": "magnus path*gridpoint*windows/s", "value": value,
         "unit": "path*gridpoint*windows/s", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference xoshiro256++ Brownian paths, Gaussian datum)",
-        "config": {"workload": f"{args.preset} bounded sample: {M_cpu} paths x 1 window, {args.d}x{args.d}, "
-                               f"order {args.order}, dt={args.dt}, dt_leb={args.dt_leb}",
-                   "grid": args.d, "paths": M_cpu, "order": args.order, "dt": args.dt},
+        "config": {"workload": f"{args.preset} bounded sample: {M_cpu} paths x {CPU_WINDOWS} windows per step, "
+                               f"{args.d}x{args.d}, order {args.order}, dt={args.dt}, dt_leb={args.dt_leb}",
+                   "grid": args.d, "paths": M_cpu, "order": args.order, "dt": args.dt,
+                   "windows_per_step": CPU_WINDOWS},
         "cpu_baseline": {"value": value, "unit": "path*gridpoint*windows/s", "cores": threads,
                          "kind": "reference",
-                         "sample": f"{M_cpu} paths x 1 window per step (OpenMP {threads} threads)"},
+                         "sample": f"{M_cpu} paths x {CPU_WINDOWS} windows per step (OpenMP {threads} threads)",
+                         "setup_s_per_call": setup_s, "steady_window_s": per_window_s,
+                         "steady_value": M_cpu * n / per_window_s if per_window_s > 0 else None},
         "e2e": {"value": value, "unit": "path*gridpoint*windows/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -281,36 +330,31 @@ def run_reference(args):
     return 0
 
 
-def run_ours(args):
-    rank, local, world, dist = dist_setup(args.gpus)
-    import paper_2207_09776_b200 as s2b
+def load_profile(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
-    ctx = s2b.Context(local)
-    grid = s2b.GridSpec.square(args.d)
+
+def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_session=False):
+    """Time a.steps Magnus windows of every path (after a.warmup) through a resident session.
+    Returns the measurement (value, ms, roofline, compute roofline, clocks, launches) and, with
+    keep_session, the session and paths for the e2e leg."""
+    grid = s2b.GridSpec.square(a.d)
     n = grid.dim()
-    M = args.paths
-    fam, fkw = family_args(args)
-    op = s2b.Operator.from_family(grid, fam, **fkw,
-                                  order=args.order, ctx=ctx)
-    paths = s2b.BrownianPaths.philox(args.T, args.dt_leb, M, seed=args.seed,
-                                     path_offset=rank * M, ctx=ctx)
+    M = a.paths
+    fam, fkw = family_args(a)
+    op = s2b.Operator.from_family(grid, fam, **fkw, order=a.order, ctx=ctx)
+    paths = s2b.BrownianPaths.philox(a.T, a.dt_leb, M, seed=a.seed, path_offset=rank * M, ctx=ctx)
     phi = s2b.gaussian_datum(grid)
-    cfg = s2b.MagnusConfig(order=args.order, dt=args.dt)
-    sess = s2b.MagnusSession(cfg, op, phi, paths, args.T)
-    nwin = int(round(args.T / args.dt))
-    dt_steps = int(round(args.dt / args.dt_leb))
-
-    import torch
-    torch.cuda.set_device(local)
-    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
-
-    # warm-up windows
-    for _ in range(args.warmup):
-        sess.advance(1)
-    win = args.warmup
-    if win + args.steps > nwin:
+    sess = s2b.MagnusSession(s2b.MagnusConfig(order=a.order, dt=a.dt), op, phi, paths, a.T)
+    nwin = int(round(a.T / a.dt))
+    if a.warmup + a.steps > nwin:
         raise SystemExit("warmup + steps exceeds the number of windows; raise T or lower steps")
-
+    for _ in range(a.warmup):
+        sess.advance(1)
     st0 = sess.stats()
     l0 = ctx.launches
     sess.set_timing(True)
@@ -322,7 +366,7 @@ def run_ours(args):
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(a.steps):
         sess.advance(1)
     e1.record(stream)
     e1.synchronize()
@@ -333,9 +377,8 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     st1 = sess.stats()
     launches = ctx.launches - l0
-    win += args.steps
     ms_max = max_over_ranks(ms, dist, local)
-    value = world * M * n * args.steps / (ms_max / 1e3)
+    value = world * M * n * a.steps / (ms_max / 1e3)
 
     # roofline of the dominant kernel: algorithmic bytes per Taylor term (32 B per
     # path*gridpoint*term, 24 B for the k=1 term of a segment), over that kernel's event time
@@ -344,47 +387,82 @@ def run_ours(args):
     alg_bytes = n * (32.0 * (terms - segs) + 24.0 * segs)
     tk_ms = st1["term_kernel_ms"] - st0["term_kernel_ms"]
     tk_launches = st1["term_launches"] - st0["term_launches"]
-    engine = ENGINES.get(st1.get("engine", 0), ENGINES[0])
-    if engine["name"] == "stream" and args.family == "langevin-constant" and args.d >= 1024:
-        engine = dict(engine, profile="r01_term_tma_1024_ncu.json")  # the capture at this grid
-    if engine["name"] == "stream" and args.family != "langevin-constant":
-        engine = dict(ENGINE_VAR)  # x-dependent weights: the streaming pass runs term_var_kernel
-        if args.d > 256 or (args.family == "kinetic-variable" and args.order == 3):
+    engine = dict(ENGINES.get(st1.get("engine", 0), ENGINES[0]))
+    if engine["name"] == "stream" and a.family != "langevin-constant":
+        engine = dict(ENGINE_VAR)
+        if a.d > 256 or (a.family == "kinetic-variable" and a.order == 3):
             engine["kernel"] = "term_varx_kernel"  # x-split variant: wide grids, 64 source pairs
-            engine["profile"] = "none"             # no capture of it at this grid: traffic null
+    names = ctx.kernel_names()
+    launched = names["stream"] if engine["name"] == "stream" else names["cluster"]
+    hyb = st1.get("hybrid_paths", 0) or 0
+    prof_name = PROFILE_OF.get((a.preset, a.family, engine["name"])) or engine["profile"]
+    prof = load_profile(prof_name)
     peak, peak_kind = peaks()
     achieved = alg_bytes / (tk_ms / 1e3) / 1e9 if tk_ms > 0 else 0.0
+    # traffic only from a capture of the binary that ran: the profile's mangled kernel name
+    # must equal the one this session launched (cudaFuncGetName)
+    stale = prof.get("kernel_mangled") != launched
+    stream_stale = False
     traffic = None
-    prof = {}
-    try:
-        with open(os.path.join(ROOT, "profiles", engine["profile"])) as f:
-            prof = json.load(f)
-        hyb = st1.get("hybrid_paths", 0) or 0  # paths on the streaming engine beside the clusters
-        stream_prof = {}
-        if hyb:
-            with open(os.path.join(ROOT, "profiles", ENGINES[0]["profile"])) as f:
-                stream_prof = json.load(f)
+    if not stale:
         if engine["name"] == "stream" and prof.get("dram_bytes_per_path_term") is not None:
             traffic = prof["dram_bytes_per_path_term"] * terms / max(tk_launches, 1)
         elif prof.get("dram_bytes_per_path_window") is not None:
-            traffic = (prof["dram_bytes_per_path_window"] * (M - hyb) * args.steps
-                       + stream_prof.get("dram_bytes_per_path_term", 0.0) * terms * hyb / M) / max(tk_launches, 1)
-    except Exception:
-        pass
+            slice_bytes = 0.0
+            if hyb:
+                sp = load_profile(PROFILE_OF.get(("hybrid", a.d)) or "none")
+                stream_stale = sp.get("kernel_mangled") != names["stream"]
+                slice_bytes = None if stream_stale else sp.get("dram_bytes_per_path_term", 0.0) * terms * hyb / M
+            if slice_bytes is not None:
+                traffic = (prof["dram_bytes_per_path_window"] * (M - hyb) * a.steps + slice_bytes) / max(tk_launches, 1)
     # the on-chip engines are bound by the fp64 pipe, not HBM: report that ceiling beside it
     # (DMUL + DADD per stencil point, no FMA for bitwise parity; +1 DMUL, +1 DADD per point)
-    ops_pt = 2 * stencil_points(args.order) + 2
-    if args.family == "langevin-variable":  # + the per-term fold of Y from the source pairs
-        ops_pt += 2 * {1: 7, 2: 15, 3: 39}[args.order]
-    elif args.family == "kinetic-variable":
-        ops_pt = 2 * {2: 11, 3: 23}.get(args.order, 5) + 2 + 2 * {2: 24, 3: 64}.get(args.order, 7)
+    ops_pt = 2 * stencil_points(a.order) + 2
+    if a.family == "langevin-variable":  # + the per-term fold of Y from the source pairs
+        ops_pt += 2 * {1: 7, 2: 15, 3: 39}[a.order]
+    elif a.family == "kinetic-variable":
+        ops_pt = 2 * {2: 11, 3: 23}.get(a.order, 5) + 2 + 2 * {2: 24, 3: 64}.get(a.order, 7)
     fp64_ops = n * terms * float(ops_pt)
     fp64_peak = fp64_peak_tops()
     compute = {"bound": "fp64", "achieved": fp64_ops / (tk_ms / 1e3) / 1e12 if tk_ms > 0 else 0.0,
                "peak": fp64_peak, "unit": "TFLOP/s (DMUL/DADD, non-FMA)",
                "ops_model": f"{ops_pt} fp64 ops per path*gridpoint*term",
-               "ncu_fp64_pipe_pct_of_active": prof.get("fp64_pipe_pct_of_active")}
+               "ncu_fp64_pipe_pct_of_active": None if stale else prof.get("fp64_pipe_pct_of_active")}
     compute["frac"] = compute["achieved"] / fp64_peak if fp64_peak else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+            "kernel": engine["kernel"], "kernel_mangled": launched, "engine": engine["name"],
+            "launches": tk_launches, "kernel_ms": tk_ms,
+            "bytes_model": "32 B per path*gridpoint*term (24 B for the k=1 term of a segment)",
+            "traffic_source": f"profiles/{prof_name} (ncu dram__bytes, scaled per launch)"
+                              + (" + the streaming-engine capture of the hybrid slice" if hyb else ""),
+            "stale_profile": bool(stale or stream_stale),
+            "hybrid_paths": hyb, "note": engine["note"]}
+    if stale:
+        roof["profile_kernel"] = prof.get("kernel_mangled") or prof.get("kernel")
+    out = {"value": value, "ms_max": ms_max, "terms": terms, "roofline": roof, "compute_roofline": compute,
+           "clocks": clk, "launches": launches, "n": n, "M": M, "nwin": nwin, "win": a.warmup + a.steps}
+    if keep_session:
+        out.update(sess=sess, paths=paths, grid=grid, phi=phi)
+    else:
+        del sess
+    return out
+
+
+def run_ours(args):
+    rank, local, world, dist = dist_setup(args.gpus)
+    import paper_2207_09776_b200 as s2b
+    import torch
+
+    torch.cuda.set_device(local)
+    ctx = s2b.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+    mg = magnus_leg(args, s2b, ctx, torch, stream, dist, local, world, rank, keep_session=True)
+    sess, paths, grid, phi = mg["sess"], mg["paths"], mg["grid"], mg["phi"]
+    n, M, nwin, win = mg["n"], mg["M"], mg["nwin"], mg["win"]
+    dt_steps = int(round(args.dt / args.dt_leb))
+    ms_max, value, terms = mg["ms_max"], mg["value"], mg["terms"]
+    roofline, compute, clk, launches = mg["roofline"], mg["compute_roofline"], mg["clocks"], mg["launches"]
 
     # end-to-end through the C ABI with host buffers: per step the window's Brownian prefix
     # values go H2D from pinned memory, the window runs, the moment statistics come back D2H
@@ -419,13 +497,39 @@ def run_ours(args):
 
     # Euler-Maruyama on the same grid/paths (dt = dt_leb), reported beside Magnus; the Magnus
     # session's state is released first (at 1024^2 both would not fit one GPU)
-    del sess
+    del sess, mg
     em = None
     if args.euler_steps > 0:
         try:
             em = euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, world, M, n)
         except Exception as ex:  # keep the Magnus line even if the E-M leg fails
             em = {"error": str(ex)[:200]}
+    del paths
+
+    # north_star's own target (512^2, >= 60% of the HBM roofline): cfg4 measured in the same
+    # run, beside the unchanged cfg2 headline
+    ns = None
+    if args.preset == "cfg2" and not args.no_north_star:
+        try:
+            a4 = argparse.Namespace(**vars(args))
+            a4.preset = "cfg4"
+            for k, v in PRESETS["cfg4"].items():
+                setattr(a4, k, v)
+            a4.steps, a4.warmup = max(2, min(args.steps, 3)), 3
+            a4.T = (a4.warmup + a4.steps) * a4.dt  # the first windows of T = 1: the same per-window work
+            r4 = magnus_leg(a4, s2b, ctx, torch, stream, dist, local, world, rank)
+            ns = {"metric": "magnus path*gridpoint*windows/s", "value": r4["value"],
+                  "ms_per_step": r4["ms_max"] / a4.steps, "steps": a4.steps, "warmup": a4.warmup,
+                  "config": {"workload": "cfg4: constant-coefficient Langevin 512x512, 4096 paths/GPU, order-3 "
+                                         "iterated Magnus, dt=0.005 (first windows of T=1), dt_leb=1e-4",
+                             "grid": 512, "paths_per_gpu": a4.paths, "order": 3, "dt": a4.dt},
+                  "path_terms_per_window": r4["terms"] / max(1, a4.paths * a4.steps),
+                  "path_gridpoint_terms_per_s": world * r4["n"] * r4["terms"] / (r4["ms_max"] / 1e3),
+                  "roofline": r4["roofline"], "compute_roofline": r4["compute_roofline"],
+                  "target": "north_star: >= 0.60 of the HBM roofline at 512^2 on 1 B200",
+                  "gpu_launches": r4["launches"], "clocks": r4["clocks"]}
+        except Exception as ex:
+            ns = {"error": str(ex)[:300]}
 
     line = {
         "metric": "magnus path*gridpoint*windows/s", "value": value,
@@ -443,15 +547,7 @@ def run_ours(args):
                    "l2": f"inputs larger than L2 ({4 * M * n * 8 / 1e9:.3g} GB resident state per GPU vs 126 MB L2)"},
         "path_terms_per_window": terms / max(1, M * args.steps),
         "path_gridpoint_terms_per_s": world * n * terms / (ms_max / 1e3),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": engine["kernel"], "engine": engine["name"], "launches": tk_launches,
-                     "kernel_ms": tk_ms,
-                     "bytes_model": "32 B per path*gridpoint*term (24 B for the k=1 term of a segment)",
-                     "traffic_source": f"profiles/{engine['profile']} (ncu dram__bytes, scaled per launch)"
-                                       + (" + streaming-engine bytes of the hybrid slice" if st1.get("hybrid_paths") else ""),
-                     "hybrid_paths": st1.get("hybrid_paths", 0),
-                     "note": engine["note"]},
+        "roofline": roofline,
         "compute_roofline": compute,
         "gpu_launches": launches,
         "clocks": clk,
@@ -460,14 +556,16 @@ def run_ours(args):
         line["e2e"] = e2e
     if em is not None:
         line["euler_maruyama"] = em
+    if ns is not None:
+        line["north_star_512"] = ns
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             nproc = os.cpu_count() or 1
             M_cpu = max(2, nproc)
-            times, threads = cpu_reference_leg(args, M_cpu, 1, reps=1)
-            line["cpu_baseline"] = {"value": M_cpu * n / times[0], "unit": "path*gridpoint*windows/s",
+            times, threads = cpu_reference_leg(args, M_cpu, CPU_WINDOWS, reps=1)
+            line["cpu_baseline"] = {"value": M_cpu * n * CPU_WINDOWS / times[0], "unit": "path*gridpoint*windows/s",
                                     "cores": threads, "kind": "reference",
-                                    "sample": f"{M_cpu} paths x 1 window of the same workload, "
+                                    "sample": f"{M_cpu} paths x {CPU_WINDOWS} windows of the same workload, "
                                               f"reference C++ (oracle/_ref) with OpenMP"}
         except Exception as ex:
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
@@ -516,6 +614,8 @@ def euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, worl
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_spawn(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -135,6 +135,10 @@ int s2b_context_synchronize(s2b_context *ctx);
 void *s2b_context_stream(s2b_context *ctx);
 /* Number of kernels launched by this context so far. */
 int64_t s2b_context_launches(s2b_context *ctx);
+/* Mangled names (cudaFuncGetName) of the dominant Magnus kernels this context launched last:
+ * the cluster-resident engine's and the streaming pass engine's ("" if none), each copied
+ * into a caller buffer of `len` bytes.  bench.py matches them against the ncu captures. */
+int s2b_context_kernel_names(s2b_context *ctx, char *cluster, char *stream, size_t len);
 
 /* ---- operators ----------------------------------------------------------------
  * sources: B, A, A2, BA, BAA, BAB (the CommutatorSet slot order of magnus.cpp:42-52).
@@ -308,6 +312,60 @@ int s2b_euler_step(const s2b_fields *f, const double *stencils, const double *u,
                    double dW, double dt, double *maxabs);
 int s2b_euler_step_device(const s2b_fields *f, const double *stencils, const double *d_u,
                           double *d_out, size_t M, const double *dW, double dt, double *maxabs);
+
+/* Moments of one record: sum_m u_m and sum_m u_m^2 over the non-blown paths (2n doubles,
+ * host), ascending m per point; live (NULL-able) = the number of non-blown paths. */
+int s2b_ensemble_moments(const s2b_ensemble *e, size_t record, double *moments, size_t *live);
+
+/* ---- multi-GPU (one node): path sharding + one NCCL reduction -----------
+ * The reference parallelises over paths only (OpenMP, magnus.cpp:258-263,
+ * euler.cpp:142-145).  s2b_multi owns one context per listed device and, when the devices
+ * are distinct, an NCCL clique over them (ncclCommInitAll; NCCL is loaded at run time).
+ * A solve splits the global paths [0, M_total) into contiguous ranges (s2b_shard), runs
+ * each range on its device from its own host thread -- operator build, Philox paths keyed
+ * by the global path id (path_offset = range start, so results do not depend on the device
+ * count), the solver, the per-path norms -- then combines once: ncclAllReduce of the ME sums,
+ * counts, moments and counters, ncclAllGather of the per-path errors, so Err is summed in
+ * ascending global path order (bitwise the one-device value).  A device listed twice
+ * combines on the host instead (same arithmetic; used to test sharding on one GPU). */
+typedef struct s2b_multi s2b_multi;
+/* Operator / coefficient description built on every device (s2b_operator_build arguments;
+ * family 2 = explicit fields9).  a and sigma are also the LangevinParams of the exact norms. */
+typedef struct {
+    int family;
+    double a;
+    double sigma;
+    const double *const *fields9;
+    int order;
+} s2b_operator_spec;
+typedef struct {
+    s2b_error_stats errors; /* combined norms vs the closed form (kappa >= 0) */
+    int64_t path_terms;     /* Magnus Taylor terms over all paths */
+    int64_t path_windows;
+    double max_solve_ms;    /* slowest device's solver time (CUDA events on its stream) */
+    size_t M_total;
+    int devices;
+    int nccl;               /* 1: combined with NCCL, 0: host combine */
+} s2b_multi_stats;
+/* shard(): contiguous range of `rank` among `world`; the first M % world ranks get one more. */
+int s2b_shard(size_t M_total, int rank, int world, size_t *offset, size_t *count);
+int s2b_multi_create(const int *devices, int ndev, s2b_multi **out);
+int s2b_multi_destroy(s2b_multi *m);
+/* info: [0] devices, [1] NCCL clique (1) or host combine (0) */
+int s2b_multi_info(const s2b_multi *m, int info[2]);
+/* kappa >= 0: norms against exact_reference(a, sigma) over the central region I^kappa (the
+ * Langevin families); kappa < 0: moments and counts only.  me_out (w*w), moments_out (2n),
+ * per_path_rel_out (M_total, global path order) are NULL-able host buffers. */
+int s2b_multi_solve_magnus(s2b_multi *m, const s2b_grid *grid, const s2b_operator_spec *op,
+                           const s2b_magnus_config *cfg, const double *phi, double dt_leb,
+                           size_t steps, size_t M_total, uint64_t seed, int kappa,
+                           s2b_multi_stats *out, double *me_out, double *moments_out,
+                           double *per_path_rel_out);
+int s2b_multi_solve_euler(s2b_multi *m, const s2b_grid *grid, const s2b_operator_spec *fields,
+                          const s2b_euler_config *cfg, const double *phi, double dt_leb,
+                          size_t steps, size_t M_total, uint64_t seed, int kappa,
+                          s2b_multi_stats *out, double *me_out, double *moments_out,
+                          double *per_path_rel_out);
 
 #ifdef __cplusplus
 }

@@ -93,6 +93,12 @@ class Context:
     def launches(self) -> int:
         return int(lib().s2b_context_launches(self.h))
 
+    def kernel_names(self):
+        """Mangled names of the dominant Magnus kernels this context launched last."""
+        a, b = C.create_string_buffer(4096), C.create_string_buffer(4096)
+        _check(lib().s2b_context_kernel_names(self.h, a, b, 4096))
+        return {"cluster": a.value.decode(), "stream": b.value.decode()}
+
     def close(self):
         if getattr(self, "h", None):
             lib().s2b_context_destroy(self.h)

@@ -128,6 +128,7 @@ SIGNATURES = {
                                    _P(C.c_double)]),
     "s2b_expmv": (C.c_int, [_VP, _P(Csr), _P(C.c_double), C.c_double, C.c_double,
                             _P(C.c_double), _P(C.c_int)]),
+    "s2b_context_kernel_names": (C.c_int, [_VP, C.c_char_p, C.c_char_p, C.c_size_t]),
     "s2b_expmv_workspace_create": (C.c_int, [_VP, _P(_VP)]),
     "s2b_expmv_workspace_destroy": (C.c_int, [_VP]),
     "s2b_expmv_into": (C.c_int, [_VP, _P(Csr), _P(C.c_double), C.c_double, C.c_double,

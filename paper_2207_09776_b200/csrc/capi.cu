@@ -11,6 +11,11 @@ namespace s2b {
 
 namespace {
 thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& what) { g_last_error = what; }
+
+namespace {
 
 template <class F>
 int guard(F&& f) {
@@ -573,6 +578,15 @@ int s2b_ensemble_counters(const s2b_ensemble* e, int64_t* terms, int64_t* window
     });
 }
 
+int s2b_ensemble_moments(const s2b_ensemble* e, size_t record, double* moments, size_t* live) {
+    return guard([&] {
+        need(e, "ensemble");
+        need(moments, "moments");
+        S2B_CUDA(cudaSetDevice(e->ctx->device));
+        ensemble_moments(e, record, moments, live);
+    });
+}
+
 int s2b_ensemble_destroy(s2b_ensemble* e) {
     return guard([&] { delete e; });
 }
@@ -635,6 +649,21 @@ int s2b_expmv(s2b_context* ctx, const s2b_csr* m, const double* x, double tol, d
         need(report, "report");
         S2B_CUDA(cudaSetDevice(ctx->device));
         expmv_csr(ctx, m, x, tol, theta, y, report);
+    });
+}
+
+int s2b_context_kernel_names(s2b_context* ctx, char* cluster, char* stream, size_t len) {
+    return guard([&] {
+        need(ctx, "ctx");
+        auto put = [&](const void* fn, char* out) {
+            if (!out || len == 0) return;
+            const char* name = "";
+            if (fn) S2B_CUDA(cudaFuncGetName(&name, fn));
+            std::strncpy(out, name, len - 1);
+            out[len - 1] = 0;
+        };
+        put(ctx->k_cluster, cluster);
+        put(ctx->k_stream, stream);
     });
 }
 

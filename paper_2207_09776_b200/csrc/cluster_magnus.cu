@@ -379,6 +379,7 @@ void launch_vr(s2b_context* ctx, const ClusterArgs& a) {
     clusters = std::max(1, std::min(clusters, a.M));
     cfg.gridDim = dim3(CL * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    ctx->k_cluster = reinterpret_cast<const void*>(kern);
 }
 
 // Cluster shapes: 8 CTAs x 4 bands (one CTA per SM) is the default; S2B_CLUSTER=16 selects

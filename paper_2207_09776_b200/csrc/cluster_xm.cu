@@ -473,6 +473,7 @@ void launch_xm(s2b_context* ctx, const ClusterBatch& a) {
     clusters = std::max(1, std::min(clusters, a.total));
     cfg.gridDim = dim3(kXmCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    ctx->k_cluster = reinterpret_cast<const void*>(kern);
 }
 
 bool xm_enabled() {

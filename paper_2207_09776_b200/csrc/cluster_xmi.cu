@@ -470,6 +470,7 @@ void launch_xmi(s2b_context* ctx, const ClusterBatch& a) {
     clusters = std::max(1, std::min({clusters, a.total, a.a[0].sx_slots}));
     cfg.gridDim = dim3(kXiCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    ctx->k_cluster = reinterpret_cast<const void*>(kern);
 }
 
 bool xmi_enabled() {

@@ -851,9 +851,13 @@ void launch_term(MagnusSession& s) {
         if (term_var_supported(s.op))
             launch_term_var(s.ctx, s.op, a, s.M);
         else if (generic_k_enabled())
+        {
             term_generic_k_kernel<kGenK><<<grid_k, bs, 0, s.ctx->stream>>>(a, s.bits.p, s.nbits);
-        else
+            s.ctx->k_stream = reinterpret_cast<const void*>(term_generic_k_kernel<kGenK>);
+        } else {
             term_generic_kernel<<<grid, bs, 0, s.ctx->stream>>>(a, s.bits.p, s.nbits);
+            s.ctx->k_stream = reinterpret_cast<const void*>(term_generic_kernel);
+        }
     } else {
         const int nye = kClasses * tma_popcount(variant);
         const int nt = static_cast<int>((std::max<size_t>((s.op->nx + 1) / 2, nye) + 31) / 32 * 32);
@@ -1205,6 +1209,7 @@ void session_advance(MagnusSession* s, size_t n_windows) {
         s->ctx = c1;
         s->timing = tim;
         c1->launches = c2.launches;
+        c1->k_stream = c2.k_stream;
         S2B_CUDA(cudaEventRecord(done, s->stream2));
         S2B_CUDA(cudaStreamWaitEvent(st1, done, 0));
         if (s->timing) {

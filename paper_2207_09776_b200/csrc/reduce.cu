@@ -167,6 +167,8 @@ __global__ void moments_kernel(const double* app, const uint8_t* st, size_t M, s
     mom[n + r] = s2;
 }
 
+} // namespace
+
 void region_of(size_t d, int kappa, size_t* lo, size_t* hi) {
     if (d < 2) fail(S2B_ERR_CONFIG, "central_region: need d >= 2");
     if (kappa < 0) fail(S2B_ERR_CONFIG, "central_region: kappa must be non-negative");
@@ -179,6 +181,8 @@ void region_of(size_t d, int kappa, size_t* lo, size_t* hi) {
     *hi = static_cast<size_t>(std::min<long long>(hi1 - 1, static_cast<long long>(d) - 1));
     if (*hi < *lo) fail(S2B_ERR_CONFIG, "central_region: empty region");
 }
+
+namespace {
 
 void run_norms(s2b_context* ctx, const double* ref, const uint8_t* ref_status, const double2* wiw,
                const ExactParams& p, const s2b_ensemble* app, size_t app_record, int kappa,
@@ -307,6 +311,26 @@ void exact_errors(s2b_context* ctx, const s2b_ensemble* app, size_t app_record, 
         paths->d_values.p, paths->steps + 1, k1, paths->dt_leb, app->M, wiw.p);
     S2B_LAUNCHED(ctx);
     run_norms(ctx, nullptr, nullptr, wiw.p, p, app, app_record, kappa, out, me_out, per_path_rel, moments);
+}
+
+// sum_m u_m and sum_m u_m^2 over the non-blown paths of one record (ascending m per point)
+void ensemble_moments(const s2b_ensemble* e, size_t record, double* host_moments, size_t* live) {
+    if (record >= e->R) fail(S2B_ERR_DIMENSION, "ensemble moments: record out of range");
+    s2b_context* ctx = e->ctx;
+    const size_t M = e->M, n = e->nx * e->nv;
+    const uint8_t* st = e->status.p + record * M;
+    DevBuf<double> mom(2 * n);
+    moments_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(e->states[record].p, st, M, n, mom.p);
+    S2B_LAUNCHED(ctx);
+    S2B_CUDA(cudaMemcpyAsync(host_moments, mom.p, mom.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<uint8_t> hs(M);
+    S2B_CUDA(cudaMemcpyAsync(hs.data(), st, M, cudaMemcpyDeviceToHost, ctx->stream));
+    S2B_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (live) {
+        size_t k = 0;
+        for (uint8_t v : hs) k += v == 0;
+        *live = k;
+    }
 }
 
 } // namespace s2b

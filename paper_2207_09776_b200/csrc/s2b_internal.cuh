@@ -67,6 +67,10 @@ struct s2b_context {
     int num_sms = 0;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
+    // the dominant kernels the Magnus engines launched last (their mangled names are what
+    // bench.py matches against the ncu captures in profiles/)
+    const void* k_cluster = nullptr;
+    const void* k_stream = nullptr;
 };
 
 namespace s2b {
@@ -198,6 +202,9 @@ void expmv_into(s2b_expmv_workspace* ws, const s2b_csr* m, const double* x, doub
                 s2b_expmv_report* rep, bool device);
 void euler_step_batch(const s2b_fields* f, const double* st, const double* d_u, double* d_out, size_t M,
                       const double* dW, double dt, double* maxabs);
+void region_of(size_t d, int kappa, size_t* lo, size_t* hi); // central_region (analysis.cpp:9-31)
+void set_last_error(const std::string& what); // the calling thread's s2b_last_error()
+void ensemble_moments(const s2b_ensemble* e, size_t record, double* host_moments, size_t* live);
 void expmv_csr(s2b_context* ctx, const s2b_csr* m, const double* x, double tol, double theta, double* y,
                int report[4]);
 

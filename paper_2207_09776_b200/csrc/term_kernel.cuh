@@ -279,6 +279,7 @@ void launch_term_nt(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, si
     const size_t cap = static_cast<size_t>(ctx->num_sms) * blocks_per_sm;
     const int grid = static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
     kern<<<grid, nt, smem, ctx->stream>>>(a);
+    ctx->k_stream = reinterpret_cast<const void*>(kern);
 }
 
 } // namespace mg

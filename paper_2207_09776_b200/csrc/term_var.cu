@@ -559,6 +559,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
             const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
             const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
             kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
+            ctx->k_stream = reinterpret_cast<const void*>(kern);
         };
         const char* en = std::getenv("S2B_VARX_NT");
         const char* ek = std::getenv("S2B_VARX_K");
@@ -589,6 +590,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
         const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
         kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips);
+        ctx->k_stream = reinterpret_cast<const void*>(kern);
     };
     if constexpr (NP <= 40) {
         if (tw)

@@ -229,3 +229,34 @@ def test_magnus_log_builder_bytes_equal_the_reference(tmp_path):
         subprocess.run([exe, str(out)], check=True, timeout=300)
         outs.append(out.read_bytes())
     assert len(outs[0]) > 1_000_000 and outs[0] == outs[1]
+
+
+def test_bench_world_size_must_match_gpus(tmp_path):
+    """A launcher world size that differs from --gpus is refused (exit 2), never reported as a
+    mislabelled one-GPU number."""
+    import subprocess
+    import sys as _sys
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([_sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], capture_output=True,
+                         text=True, env=env, cwd=tmp_path, timeout=300)
+    assert out.returncode == 2 and "WORLD_SIZE=1" in out.stderr
+
+
+@pytest.mark.skipif(not _ref_built(), reason="oracle/_ref not built")
+def test_bench_self_spawns_ranks(tmp_path):
+    """`bench.py --gpus 2` with no launcher re-executes itself under torch.distributed.run:
+    two ranks, one JSON line (rank 0), labelled n_gpus 2."""
+    import json
+    import subprocess
+    import sys as _sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["OMP_NUM_THREADS"] = "2"
+    cmd = [_sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference", "--config",
+           "cfg1", "--steps", "1", "--warmup", "0"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=tmp_path, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert d["cpu_baseline"]["setup_s_per_call"] >= 0.0
