@@ -32,6 +32,7 @@ __all__ = [
     "solve_iterated_magnus", "solve_euler", "exact_reference", "central_region",
     "mean_rel_error", "mean_abs_error", "avg_mean_abs_error", "exact_errors", "gaussian_datum",
     "expmv", "default_context", "ExpmvWorkspace", "expmv_into", "EulerStencils", "euler_step",
+    "MultiGPU", "shard",
 ]
 
 
@@ -459,6 +460,13 @@ class Ensemble:
     def blowup_count(self):
         return int(self.status.sum())
 
+    def moments(self):
+        """(sum_m u_m, sum_m u_m^2) over the non-blown paths of this record, and the live count."""
+        mom = np.empty(2 * self.n)
+        live = C.c_size_t()
+        _check(lib().s2b_ensemble_moments(self._h.h, self.record, _dptr(mom), C.byref(live)))
+        return mom[:self.n], mom[self.n:], int(live.value)
+
     def counters(self):
         t = np.empty(self.M, np.int64)
         w = np.empty(self.M, np.int64)
@@ -776,3 +784,78 @@ def euler_step(fields: Fields, u, dW, dt, stencils: EulerStencils = None):
     st = (stencils or EulerStencils.from_grid(fields.grid)).c()
     _check(lib().s2b_euler_step(fields.h, st, _dptr(u), _dptr(out), float(dW), float(dt), C.byref(mx)))
     return out, mx.value
+
+
+# ---------------------------------------------------------------- multi-GPU (one node)
+def shard(M_total, rank, world):
+    """Contiguous path range (offset, count) of `rank` (s2b_shard)."""
+    off, cnt = C.c_size_t(), C.c_size_t()
+    rc = lib().s2b_shard(int(M_total), int(rank), int(world), C.byref(off), C.byref(cnt))
+    if rc != _capi.OK:
+        raise ConfigError("shard: need 0 <= rank < world")
+    return off.value, cnt.value
+
+
+class MultiGPU:
+    """Path-sharded solves over several devices of one node from ONE process (s2b_multi):
+    a context and a host thread per device, Philox paths keyed by the global path id, one
+    NCCL all-reduce + all-gather of the statistics at the end.  A device listed twice
+    combines on the host (the sharding path on a one-GPU box)."""
+
+    def __init__(self, devices: Sequence[int]):
+        arr = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(lib().s2b_multi_create(arr, len(devices), C.byref(h)))
+        self.h, self.devices = h, list(devices)
+        info = (C.c_int * 2)()
+        _check(lib().s2b_multi_info(self.h, info))
+        self.nccl = bool(info[1])
+
+    def _run(self, fn, grid, family, cfgc, phi, dt_leb, steps, M_total, seed, kappa, a, sigma, order, fields):
+        arr, keep = _fields_array(fields, grid)
+        spec = _capi.OperatorSpec(FAMILIES[family], float(a), float(sigma),
+                                  C.cast(arr, C.POINTER(C.POINTER(C.c_double))) if fields else None, int(order))
+        phi = np.ascontiguousarray(phi, np.float64)
+        if phi.size != grid.dim():
+            raise DimensionError("multi solve: datum shape mismatch")
+        st = _capi.MultiStats()
+        n = grid.dim()
+        w2 = 0
+        if kappa >= 0:
+            lo, hi = central_region(grid.nx, kappa)
+            w2 = (hi - lo + 1) ** 2
+        me = np.empty(max(w2, 1))
+        mom = np.empty(2 * n)
+        rel = np.empty(M_total) if kappa >= 0 else None
+        _check(fn(self.h, C.byref(grid.c()), C.byref(spec), C.byref(cfgc), _dptr(phi), float(dt_leb), int(steps),
+                  int(M_total), int(seed), int(kappa), C.byref(st), _dptr(me), _dptr(mom),
+                  _dptr(rel) if rel is not None else None))
+        out = {k: getattr(st, k) for k, _ in _capi.MultiStats._fields_ if k != "errors"}
+        out.update({k: getattr(st.errors, k) for k, _ in _capi.ErrorStats._fields_})
+        out["sum_u"], out["sum_u2"] = mom[:n], mom[n:]
+        if kappa >= 0:
+            w = int(round(np.sqrt(w2)))
+            out["me"] = me[:w2].reshape(w, w)
+            out["per_path_rel"] = rel
+        return out
+
+    def solve_magnus(self, cfg: MagnusConfig, grid: GridSpec, phi, T, dt_leb, M_total, seed=1, kappa=-1,
+                     family="langevin-constant", a=1.1, sigma=1.0 / np.sqrt(10.0), fields=None):
+        steps = int(round(T / dt_leb))
+        cfgc, keep = cfg.c(T)
+        return self._run(lib().s2b_multi_solve_magnus, grid, family, cfgc, phi, dt_leb, steps, M_total, seed,
+                         kappa, a, sigma, cfg.order, fields)
+
+    def solve_euler(self, cfg: EulerConfig, grid: GridSpec, phi, T, dt_leb, M_total, seed=1, kappa=-1,
+                    family="langevin-constant", a=1.1, sigma=1.0 / np.sqrt(10.0), fields=None):
+        steps = int(round(T / dt_leb))
+        cfgc, keep = cfg.c(T)
+        return self._run(lib().s2b_multi_solve_euler, grid, family, cfgc, phi, dt_leb, steps, M_total, seed,
+                         kappa, a, sigma, 1, fields)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().s2b_multi_destroy(self.h)
+        except Exception:
+            pass

@@ -60,6 +60,17 @@ class ExpmvReport(C.Structure):
                 ("max_terms", C.c_int), ("terms", C.c_int64)]
 
 
+class OperatorSpec(C.Structure):
+    _fields_ = [("family", C.c_int), ("a", C.c_double), ("sigma", C.c_double),
+                ("fields9", C.POINTER(C.POINTER(C.c_double))), ("order", C.c_int)]
+
+
+class MultiStats(C.Structure):
+    _fields_ = [("errors", ErrorStats), ("path_terms", C.c_int64), ("path_windows", C.c_int64),
+                ("max_solve_ms", C.c_double), ("M_total", C.c_size_t), ("devices", C.c_int),
+                ("nccl", C.c_int)]
+
+
 # Exported symbols with their ctypes signatures (restype int unless noted).
 _VP = C.c_void_p
 _P = C.POINTER
@@ -129,6 +140,17 @@ SIGNATURES = {
     "s2b_expmv": (C.c_int, [_VP, _P(Csr), _P(C.c_double), C.c_double, C.c_double,
                             _P(C.c_double), _P(C.c_int)]),
     "s2b_context_kernel_names": (C.c_int, [_VP, C.c_char_p, C.c_char_p, C.c_size_t]),
+    "s2b_ensemble_moments": (C.c_int, [_VP, C.c_size_t, _P(C.c_double), _P(C.c_size_t)]),
+    "s2b_shard": (C.c_int, [C.c_size_t, C.c_int, C.c_int, _P(C.c_size_t), _P(C.c_size_t)]),
+    "s2b_multi_create": (C.c_int, [_P(C.c_int), C.c_int, _P(_VP)]),
+    "s2b_multi_destroy": (C.c_int, [_VP]),
+    "s2b_multi_info": (C.c_int, [_VP, _P(C.c_int)]),
+    "s2b_multi_solve_magnus": (C.c_int, [_VP, _P(Grid), _P(OperatorSpec), _P(MagnusConfig), _P(C.c_double),
+                                         C.c_double, C.c_size_t, C.c_size_t, C.c_uint64, C.c_int,
+                                         _P(MultiStats), _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
+    "s2b_multi_solve_euler": (C.c_int, [_VP, _P(Grid), _P(OperatorSpec), _P(EulerConfig), _P(C.c_double),
+                                        C.c_double, C.c_size_t, C.c_size_t, C.c_uint64, C.c_int,
+                                        _P(MultiStats), _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "s2b_expmv_workspace_create": (C.c_int, [_VP, _P(_VP)]),
     "s2b_expmv_workspace_destroy": (C.c_int, [_VP]),
     "s2b_expmv_into": (C.c_int, [_VP, _P(Csr), _P(C.c_double), C.c_double, C.c_double,
