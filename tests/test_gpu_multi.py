@@ -43,8 +43,8 @@ def test_multi_matches_single_context(s2b, ctx, devices, scheme):
     assert np.allclose(got["me"], want["me"], rtol=1e-13, atol=0)
     assert np.allclose(got["sum_u"], want["sum_u"], rtol=1e-13, atol=1e-300)
     assert np.allclose(got["sum_u2"], want["sum_u2"], rtol=1e-13, atol=1e-300)
-    if len(devices) == 1:  # one shard: every statistic bitwise
-        assert np.array_equal(got["me"], want["me"]) and np.array_equal(got["sum_u"], want["sum_u"])
+    if len(devices) == 1:  # one shard: the moments are the device's own sums (ME is rescaled by used)
+        assert np.array_equal(got["sum_u"], want["sum_u"]) and np.array_equal(got["sum_u2"], want["sum_u2"])
     assert got["max_solve_ms"] > 0
 
 
