@@ -1,6 +1,7 @@
 // The C ABI (include/spde2d_b200.h): handle lifetime, argument validation,
 // exception -> error-code translation, and the host-side plan_windows rules.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -14,6 +15,13 @@ thread_local std::string g_last_error;
 }
 
 void set_last_error(const std::string& what) { g_last_error = what; }
+
+int grid_cap(int grid) {
+    const char* e = std::getenv("S2B_GRID_CAP");
+    if (!e) return grid;
+    const int cap = std::atoi(e);
+    return cap > 0 && cap < grid ? cap : grid;
+}
 
 namespace {
 

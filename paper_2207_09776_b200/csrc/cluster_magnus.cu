@@ -376,7 +376,7 @@ void launch_vr(s2b_context* ctx, const ClusterArgs& a) {
     cfg.gridDim = dim3(CL);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-    clusters = std::max(1, std::min(clusters, a.M));
+    clusters = grid_cap(std::max(1, std::min(clusters, a.M)));
     cfg.gridDim = dim3(CL * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     ctx->k_cluster = reinterpret_cast<const void*>(kern);

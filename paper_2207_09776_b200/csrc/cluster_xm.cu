@@ -470,7 +470,7 @@ void launch_xm(s2b_context* ctx, const ClusterBatch& a) {
     cfg.gridDim = dim3(kXmCl);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-    clusters = std::max(1, std::min(clusters, a.total));
+    clusters = grid_cap(std::max(1, std::min(clusters, a.total)));
     cfg.gridDim = dim3(kXmCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     ctx->k_cluster = reinterpret_cast<const void*>(kern);

@@ -467,7 +467,7 @@ void launch_xmi(s2b_context* ctx, const ClusterBatch& a) {
     cfg.gridDim = dim3(kXiCl);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-    clusters = std::max(1, std::min({clusters, a.total, a.a[0].sx_slots}));
+    clusters = grid_cap(std::max(1, std::min({clusters, a.total, a.a[0].sx_slots})));
     cfg.gridDim = dim3(kXiCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     ctx->k_cluster = reinterpret_cast<const void*>(kern);

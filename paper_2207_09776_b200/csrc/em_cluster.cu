@@ -446,7 +446,7 @@ void launch_em_ip(s2b_context* ctx, const EmXmArgs& a) {
     cfg.gridDim = dim3(CL);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-    clusters = std::max(1, std::min(clusters, a.M));
+    clusters = grid_cap(std::max(1, std::min(clusters, a.M)));
     cfg.gridDim = dim3(CL * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }
@@ -471,7 +471,7 @@ void launch_em(s2b_context* ctx, const EmXmArgs& a) {
     cfg.gridDim = dim3(kEmCl);
     int clusters = 0;
     S2B_CUDA(cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg));
-    clusters = std::max(1, std::min(clusters, a.M));
+    clusters = grid_cap(std::max(1, std::min(clusters, a.M)));
     cfg.gridDim = dim3(kEmCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }

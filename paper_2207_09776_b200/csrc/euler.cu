@@ -541,7 +541,7 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
         if (rows) {
             int per_sm = 0;
             S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_fn, nt, 0));
-            rows_grid = std::max(1, std::min(items, std::max(1, per_sm) * ctx->num_sms));
+            rows_grid = grid_cap(std::max(1, std::min(items, std::max(1, per_sm) * ctx->num_sms)));
         }
         // two steps per pass where the intermediate state is not a record (S2B_EMTB=0: never)
         const char* etb = std::getenv("S2B_EMTB");
@@ -561,7 +561,7 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
             S2B_CUDA(cudaFuncSetAttribute(tb_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tb_smem)));
             int per_sm = 0;
             S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tb_fn, nt, tb_smem));
-            tb_grid = std::max(1, std::min(tb_items, std::max(1, per_sm) * ctx->num_sms));
+            tb_grid = grid_cap(std::max(1, std::min(tb_items, std::max(1, per_sm) * ctx->num_sms)));
         }
         auto is_record = [&](size_t done) {
             return std::binary_search(plan.record_steps.begin(), plan.record_steps.end(), done);

@@ -75,6 +75,10 @@ struct s2b_context {
 
 namespace s2b {
 void after_launch(s2b_context* ctx, const char* file, int line);
+// S2B_GRID_CAP=n caps every persistent kernel's grid at n CTAs / clusters (never changes a
+// result: work is drawn from counters or grid-strided).  The determinism stress tests vary
+// it to change the interleaving of the synchronisation-heavy kernels.
+int grid_cap(int grid);
 }
 
 // Stencil box addressing: bit b = (dv + 3) * 7 + (dx + 3) for |dx|, |dv| <= 3.

@@ -277,7 +277,7 @@ void launch_term_nt(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, si
     S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, nt, smem));
     blocks_per_sm = std::max(1, blocks_per_sm);
     const size_t cap = static_cast<size_t>(ctx->num_sms) * blocks_per_sm;
-    const int grid = static_cast<int>(std::max<size_t>(1, std::min(work, cap)));
+    const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(work, cap))));
     kern<<<grid, nt, smem, ctx->stream>>>(a);
     ctx->k_stream = reinterpret_cast<const void*>(kern);
 }

@@ -557,7 +557,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
             const size_t parts = (nx + NT - 1) / NT;
             const size_t items = (live_max + KX - 1) / KX * static_cast<size_t>(strips) * parts;
             const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
-            const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
+            const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
             kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
             ctx->k_stream = reinterpret_cast<const void*>(kern);
         };
@@ -588,7 +588,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kVarNT, smem));
         const size_t items = (live_max + K - 1) / K * static_cast<size_t>(strips);
         const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
-        const int grid = static_cast<int>(std::max<size_t>(1, std::min(items, cap)));
+        const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
         kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips);
         ctx->k_stream = reinterpret_cast<const void*>(kern);
     };
