@@ -177,6 +177,18 @@ int s2b_host_ops_build(const s2b_grid *grid, int family, double a, double sigma,
 int s2b_host_ops_csr(const s2b_host_ops *h, int slot, s2b_csr *out);
 int s2b_host_ops_field(const s2b_host_ops *h, int which, const double **data, int *is_zero);
 int s2b_host_ops_destroy(s2b_host_ops *h);
+/* Device-side assembly: the same CommutatorSet computed on the GPU --
+ * assemble_drift / assemble_diffusion (operators.cpp:134-189) and precompute_commutators
+ * (operators.cpp:191-208) as per-row stencil kernels in the CSR algebra's accumulation order
+ * (sparse.cpp:126-261), packed back into CSR with exact zeros pruned: bitwise the host
+ * builder's (and the reference's) CSR.  The fields are sampled on the host as above. */
+int s2b_host_ops_assemble_device(s2b_context *ctx, const s2b_grid *grid, int family, double a,
+                                 double sigma, const double *const *fields9, int order,
+                                 s2b_host_ops **out);
+/* s2b_operator_build with the CommutatorSet assembled on the device. */
+int s2b_operator_build_device(s2b_context *ctx, const s2b_grid *grid, int family, double a,
+                              double sigma, const double *const *fields9, int order,
+                              s2b_operator **out);
 /* simulate_brownian (stochastics.cpp:76-101) on the host: values [M][steps+1]. */
 int s2b_host_simulate_brownian(double T, double dt_leb, size_t M, uint64_t seed,
                                double *values_out);

@@ -189,6 +189,17 @@ class Operator:
         return cls(h, ctx, grid, order)
 
     @classmethod
+    def from_family_device(cls, grid: GridSpec, family="langevin-constant", a=1.1,
+                           sigma=1.0 / np.sqrt(10.0), order=3, fields=None, ctx: Context = None):
+        """from_family with the CommutatorSet assembled on the GPU."""
+        ctx = ctx or default_context()
+        arr, keep = _fields_array(fields, grid)
+        h = C.c_void_p()
+        _check(lib().s2b_operator_build_device(ctx.h, C.byref(grid.c()), FAMILIES[family], a, sigma, arr,
+                                               order, C.byref(h)))
+        return cls(h, ctx, grid, order)
+
+    @classmethod
     def from_csr(cls, grid: GridSpec, order, sources: Sequence, ctx: Context = None):
         """sources: six (row_ptr, col_idx, values) CSR triples in slot order B, A, A2, BA,
         BAA, BAB (None for absent), e.g. a reference CommutatorSet."""
@@ -258,11 +269,17 @@ class HostOps:
     the CSR the GPU operator is laid out from (operators.cpp:134-208 arithmetic)."""
 
     def __init__(self, grid: GridSpec, family="langevin-constant", a=1.1,
-                 sigma=1.0 / np.sqrt(10.0), order=3, fields=None):
+                 sigma=1.0 / np.sqrt(10.0), order=3, fields=None, device: Optional[Context] = None):
+        """device: assemble the CommutatorSet on that context's GPU (s2b_host_ops_assemble_device)
+        instead of the host builder; the CSR is the same, bit for bit."""
         arr, keep = _fields_array(fields, grid)
         h = C.c_void_p()
-        _check(lib().s2b_host_ops_build(C.byref(grid.c()), FAMILIES[family], a, sigma, arr, order,
-                                        C.byref(h)))
+        if device is None:
+            _check(lib().s2b_host_ops_build(C.byref(grid.c()), FAMILIES[family], a, sigma, arr, order,
+                                            C.byref(h)))
+        else:
+            _check(lib().s2b_host_ops_assemble_device(device.h, C.byref(grid.c()), FAMILIES[family], a, sigma,
+                                                      arr, order, C.byref(h)))
         self.h, self.grid, self.order = h, grid, order
 
     def csr(self, slot):

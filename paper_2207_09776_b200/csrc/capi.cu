@@ -278,6 +278,41 @@ int s2b_host_ops_build(const s2b_grid* grid, int family, double a, double sigma,
     });
 }
 
+int s2b_host_ops_assemble_device(s2b_context* ctx, const s2b_grid* grid, int family, double a, double sigma,
+                                 const double* const* fields9, int order, s2b_host_ops** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        auto* h = new s2b_host_ops();
+        try {
+            h->grid = grid_spec(grid);
+            h->fields = host_fields(grid, family, a, sigma, fields9);
+            h->comms = device_commutators(ctx, h->grid, h->fields, order);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int s2b_operator_build_device(s2b_context* ctx, const s2b_grid* grid, int family, double a, double sigma,
+                              const double* const* fields9, int order, s2b_operator** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(grid, "grid");
+        need(out, "out");
+        S2B_CUDA(cudaSetDevice(ctx->device));
+        const spde2d::GridSpec g = grid_spec(grid);
+        const spde2d::CoefficientFields f = host_fields(grid, family, a, sigma, fields9);
+        const spde2d::CommutatorSet cs = device_commutators(ctx, g, f, order);
+        const s2b_csr src[6] = {csr_of(cs.B), csr_of(cs.A), csr_of(cs.A2), csr_of(cs.BA), csr_of(cs.BAA), csr_of(cs.BAB)};
+        *out = make_operator(ctx, grid, order, src);
+    });
+}
+
 int s2b_host_ops_csr(const s2b_host_ops* h, int slot, s2b_csr* out) {
     return guard([&] {
         need(h, "host_ops");

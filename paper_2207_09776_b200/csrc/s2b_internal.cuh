@@ -207,6 +207,16 @@ void expmv_into(s2b_expmv_workspace* ws, const s2b_csr* m, const double* x, doub
 void euler_step_batch(const s2b_fields* f, const double* st, const double* d_u, double* d_out, size_t M,
                       const double* dW, double dt, double* maxabs);
 void region_of(size_t d, int kappa, size_t* lo, size_t* hi); // central_region (analysis.cpp:9-31)
+} // namespace s2b
+namespace spde2d {
+struct GridSpec;
+struct CoefficientFields;
+struct CommutatorSet;
+}
+namespace s2b {
+// device-side assembly of the CommutatorSet (assemble.cu), packed into the reference's CSR
+spde2d::CommutatorSet device_commutators(s2b_context* ctx, const spde2d::GridSpec& grid,
+                                         const spde2d::CoefficientFields& f, int order);
 void set_last_error(const std::string& what); // the calling thread's s2b_last_error()
 void ensemble_moments(const s2b_ensemble* e, size_t record, double* host_moments, size_t* live);
 void expmv_csr(s2b_context* ctx, const s2b_csr* m, const double* x, double tol, double theta, double* y,
