@@ -18,5 +18,6 @@ for nm in $NAMES; do
   ${CMD[$nm]} > gpurun_out/plain_$nm.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:${KERN[$nm]} -s ${SKIP[$nm]} -c 1 \
       -o gpurun_out/prof_$nm -f ${CMD[$nm]} > gpurun_out/ncu_$nm.log 2>&1
-  echo "$nm rc=$? $(tail -c 300 gpurun_out/plain_$nm.log | tr '\n' ' ' | cut -c1-120)"
+  echo "$nm rc=$?"
+  python scripts/ncu_r02.py $nm && rm -f gpurun_out/prof_$nm.ncu-rep
 done
