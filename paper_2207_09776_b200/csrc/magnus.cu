@@ -299,14 +299,120 @@ __global__ void control_kernel(Ctl c) {
     c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
 }
 
+// The two-term engine's state machine (term2_kernel.cuh): one pass applied terms k and k+1.
+// Term k is judged first with (tn, sn); only if the segment did not stop there is term k+1
+// judged with (tn2, sn2) -- exactly the reference's sequence of single terms (sparse.cpp:463-492).
+// par holds the accumulator buffer index (0..2) during the loop: s_k went to S[(par+2)%3],
+// s_{k+1} to S[(par+1)%3]; tpar flips when the segment continues.
+__device__ void finish_segment(const Ctl& c, int p, int par, double sn) {
+    const int seg = c.seg[p] + 1;
+    c.segments[p] += 1;
+    if (seg < c.nseg[p]) {
+        c.seg[p] = seg;
+        c.k[p] = 1;
+        c.prev[p] = __longlong_as_double(static_cast<long long>(kInfBits));
+        c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
+        return;
+    }
+    if (sn > c.cap) { // window done: u = accum, max|u| == sn (magnus.cpp:282-286)
+        c.status[p] = 2;
+        return;
+    }
+    const int w = c.win[p];
+    c.windows[p] += 1;
+    const long long step = static_cast<long long>(w + 1) * c.dt_steps;
+    int r = c.rec_next[p];
+    while (r < c.R && c.rec_steps[r] == step) {
+        c.rec_status[static_cast<size_t>(r) * c.M + p] = 0;
+        if (r < c.R - 1) c.recq[atomicAdd(&c.cnt[2], 1)] = make_int4(p, r, par, 0);
+        ++r;
+    }
+    c.rec_next[p] = r;
+    if (enter_window(c, p, w + 1, par)) c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
+}
+
+__global__ void control2_kernel(Ctl c, Term2Args x) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= c.cnt[0]) return;
+    const int p = c.act_in[a];
+    const unsigned long long tb1 = c.tn[p], sb1 = c.sn[p], tb2 = x.tn2[p], sb2 = x.sn2[p];
+    c.tn[p] = 0;
+    c.sn[p] = 0;
+    x.tn2[p] = 0;
+    x.sn2[p] = 0;
+    const int sidx = c.par[p];
+    const int s_next = sidx == 2 ? 0 : sidx + 1; // s_{k+1}
+    const int s_k = sidx == 0 ? 2 : sidx - 1;    // s_k
+    const int k = c.k[p];
+    // term k
+    c.terms[p] += 1;
+    if (tb1 >= kInfBits || sb1 >= kInfBits) {
+        c.status[p] = 2;
+        return;
+    }
+    const double tn1 = __longlong_as_double(static_cast<long long>(tb1));
+    const double sn1 = __longlong_as_double(static_cast<long long>(sb1));
+    const double gate1 = c.tol * sn1;
+    if (tn1 <= gate1 && c.prev[p] <= gate1) {
+        c.par[p] = s_k;
+        finish_segment(c, p, s_k, sn1);
+        return;
+    }
+    if (k >= kMaxTerms) { // ToleranceNotReached
+        c.status[p] = 2;
+        return;
+    }
+    // term k + 1
+    c.terms[p] += 1;
+    if (tb2 >= kInfBits || sb2 >= kInfBits) {
+        c.status[p] = 2;
+        return;
+    }
+    const double tn2 = __longlong_as_double(static_cast<long long>(tb2));
+    const double sn2 = __longlong_as_double(static_cast<long long>(sb2));
+    const double gate2 = c.tol * sn2;
+    c.par[p] = s_next;
+    if (tn2 <= gate2 && tn1 <= gate2) {
+        finish_segment(c, p, s_next, sn2);
+        return;
+    }
+    if (k + 1 >= kMaxTerms) {
+        c.status[p] = 2;
+        return;
+    }
+    c.prev[p] = tn2;
+    c.k[p] = k + 2;
+    x.tpar[p] ^= 1;
+    c.act_out[atomicAdd(&c.cnt[1], 1)] = p;
+}
+
+// After a two-term run: every accumulator back in S0 / S1 (the other engines and the session
+// readers know two buffers), par in {0, 1}.
+__global__ void normalize2_kernel(const int* __restrict__ par, const double* __restrict__ S2, double* __restrict__ S0,
+                                  size_t n, size_t M, int p_lo) {
+    for (size_t m = p_lo + blockIdx.y; m < M; m += gridDim.y) {
+        if (par[m] != 2) continue;
+        const double* src = S2 + m * n;
+        double* dst = S0 + m * n;
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<size_t>(gridDim.x) * blockDim.x)
+            dst[i] = src[i];
+    }
+}
+
+__global__ void normalize2_flag_kernel(int* __restrict__ par, size_t M, int p_lo) {
+    const size_t m = p_lo + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (m < M && par[m] == 2) par[m] = 0;
+}
+
 // Copy queued record snapshots S[par][p] -> rec[r][p].
 __global__ void record_kernel(const int* __restrict__ cnt, const int4* __restrict__ recq,
                               const double* __restrict__ S0, const double* __restrict__ S1,
-                              double* const* __restrict__ rec, size_t n) {
+                              double* const* __restrict__ rec, size_t n, const double* __restrict__ S2 = nullptr) {
     const int nq = cnt[2];
     for (int q = blockIdx.y; q < nq; q += gridDim.y) {
         const int4 e = recq[q];
-        const double* src = (e.z ? S1 : S0) + static_cast<size_t>(e.x) * n;
+        const double* src = (e.z == 2 ? S2 : e.z ? S1 : S0) + static_cast<size_t>(e.x) * n;
         double* dst = rec[e.y] + static_cast<size_t>(e.x) * n;
         for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
              i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -738,6 +844,11 @@ struct MagnusSession {
     bool use_cluster = false; // cluster-resident engine (cluster_magnus.cu) for this operator
     bool external_prepare = false; // ctab/stab written by the caller (adaptive driver)
     bool phi_over_cap = false;     // max|phi| > blowup_norm_cap (zero-norm first windows blow up)
+    // two-term streaming engine (term2_kernel.cuh): third accumulator for paths >= s2_lo
+    DevBuf<double> S2;
+    size_t s2_lo = 0;
+    DevBuf<int> tpar;
+    DevBuf<unsigned long long> tn2, sn2;
     bool finished = false;         // finish() moved the buffers out: every later call is refused
     std::vector<cudaEvent_t> ev;
     s2b_magnus_stats stats{};
@@ -783,10 +894,10 @@ void session_reset(MagnusSession* s);
 
 namespace {
 
-void run_records(MagnusSession& s) {
+void run_records(MagnusSession& s, const double* S2base = nullptr) {
     if (s.R <= 1) return;
     dim3 grid(static_cast<unsigned>(std::min<size_t>((s.n + 255) / 256, 64)), 64);
-    record_kernel<<<grid, 256, 0, s.ctx->stream>>>(s.cnt.p, s.recq.p, s.S[0].p, s.S[1].p, s.rec_ptrs.p, s.n);
+    record_kernel<<<grid, 256, 0, s.ctx->stream>>>(s.cnt.p, s.recq.p, s.S[0].p, s.S[1].p, s.rec_ptrs.p, s.n, S2base);
     S2B_LAUNCHED(s.ctx);
 }
 
@@ -874,6 +985,53 @@ void launch_term(MagnusSession& s) {
         else
             launch_term_nt512(s.ctx, variant, a, nt, smem, work);
     }
+    S2B_LAUNCHED(s.ctx);
+    s.stats.term_launches += 1;
+    if (s.timing) {
+        S2B_CUDA(cudaEventRecord(e1, s.ctx->stream));
+        s.ev.push_back(e0);
+        s.ev.push_back(e1);
+    }
+}
+
+// The two-term engine applies to the compressed Langevin stencils (variants 7-9, even nx up to
+// 1024); S2B_TERM2=0 keeps the one-term passes (A/B measurements).
+bool term2_enabled(const MagnusSession& s) {
+    const char* e = std::getenv("S2B_TERM2");
+    if (e && e[0] == '0') return false;
+    const int v = s.op->variant;
+    return v >= 7 && v <= 9 && s.op->nx % 2 == 0 && s.op->nx >= 6 && s.op->nx <= 1024;
+}
+
+Term2Args term2_args(MagnusSession& s) {
+    // S2 holds paths [s2_lo, M) only: its base pointer is offset so that S2 + p*n addresses path p
+    return Term2Args{s.S2.p - s.s2_lo * s.n, s.tpar.p, s.tn2.p, s.sn2.p};
+}
+
+void launch_term2(MagnusSession& s) {
+    TermArgs a = term_args(s);
+    const Term2Args b = term2_args(s);
+    const int variant = s.op->variant;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (s.timing) {
+        S2B_CUDA(cudaEventCreate(&e0));
+        S2B_CUDA(cudaEventCreate(&e1));
+        S2B_CUDA(cudaEventRecord(e0, s.ctx->stream));
+    }
+    const int nye = kClasses * tma_popcount(variant);
+    const int yst = (nye + 1) & ~1;
+    const int nt = static_cast<int>((std::max<size_t>((s.op->nx + 1) / 2, nye) + 31) / 32 * 32);
+    const int H = kVariants[variant].rx <= 2 ? 2 : 4;
+    const size_t rw = s.op->nx + 2 * H;
+    const size_t smem = 128 + (kStages * rw + kStages * s.op->nx + 2 * rw + 8 * static_cast<size_t>(yst) +
+                               static_cast<size_t>(kPairSlots) * nye) * 8;
+    const size_t work = s.M * static_cast<size_t>(a.nstrips);
+    if (nt <= 128)
+        launch_term2_nt128(s.ctx, variant, a, b, nt, smem, work);
+    else if (nt <= 256)
+        launch_term2_nt256(s.ctx, variant, a, b, nt, smem, work);
+    else
+        launch_term2_nt512(s.ctx, variant, a, b, nt, smem, work);
     S2B_LAUNCHED(s.ctx);
     s.stats.term_launches += 1;
     if (s.timing) {
@@ -1062,6 +1220,61 @@ void stream_loop(MagnusSession* s, int stop, int p_lo) {
     }
 }
 
+// The two-term streaming engine over paths [p_lo, M): two Taylor terms of every live path per
+// pass (term2_kernel.cuh) and control2_kernel; afterwards every accumulator is moved back to
+// S0/S1 (normalize2_kernel), so the session looks exactly as after one-term passes.
+void stream_loop2(MagnusSession* s, int stop, int p_lo) {
+    const size_t M = s->M, n = s->n;
+    if (!s->S2.p || s->s2_lo != static_cast<size_t>(p_lo)) {
+        s->S2.release();
+        s->S2.alloc((M - p_lo) * n);
+        s->s2_lo = p_lo;
+    }
+    if (!s->tpar.p) {
+        s->tpar.alloc(M);
+        s->tn2.alloc(M);
+        s->sn2.alloc(M);
+    }
+    S2B_CUDA(cudaMemsetAsync(s->tpar.p, 0, s->tpar.bytes(), s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->tn2.p, 0, s->tn2.bytes(), s->ctx->stream));
+    S2B_CUDA(cudaMemsetAsync(s->sn2.p, 0, s->sn2.bytes(), s->ctx->stream));
+    const double* S2base = s->S2.p - s->s2_lo * n;
+    {
+        Ctl c = s->ctl(stop);
+        c.p_lo = p_lo;
+        S2B_CUDA(cudaMemsetAsync(s->cnt.p, 0, s->cnt.bytes(), s->ctx->stream));
+        init_kernel<<<static_cast<unsigned>((M + 127) / 128), 128, 0, s->ctx->stream>>>(c, s->cur_window);
+        S2B_LAUNCHED(s->ctx);
+        run_records(*s, S2base);
+        swap_lists(*s);
+    }
+    int chunk = 2;
+    while (true) {
+        S2B_CUDA(cudaMemcpyAsync(s->h_cnt, s->cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s->ctx->stream));
+        S2B_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        if (s->timing) collect_timing(*s);
+        if (s->h_cnt[0] == 0) break;
+        for (int q = 0; q < chunk; ++q) {
+            launch_term2(*s);
+            Ctl c = s->ctl(stop);
+            control2_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, s->ctx->stream>>>(c, term2_args(*s));
+            S2B_LAUNCHED(s->ctx);
+            run_records(*s, S2base);
+            swap_lists(*s);
+            s->stats.passes += 1;
+        }
+        chunk = std::min(chunk * 2, 32);
+    }
+    dim3 g(static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64)), static_cast<unsigned>(std::min<size_t>(M - p_lo, 65535)));
+    if (M > static_cast<size_t>(p_lo)) {
+        normalize2_kernel<<<g, 256, 0, s->ctx->stream>>>(s->iv.p + 5 * M, S2base, s->S[0].p, n, M, p_lo);
+        S2B_LAUNCHED(s->ctx);
+        normalize2_flag_kernel<<<static_cast<unsigned>((M - p_lo + 255) / 256), 256, 0, s->ctx->stream>>>(
+            s->iv.p + 5 * M, M, p_lo);
+        S2B_LAUNCHED(s->ctx);
+    }
+}
+
 // Hybrid split: the clusters of the x-march engines pack 15 x 8 (256^2) or 7 x 16 (512^2) per
 // B200, leaving 28 / 36 of the 148 SMs idle; the streaming engine runs a slice of the paths
 // concurrently on those SMs.  Measured best slices: 0.11-0.14 at 256^2 (+12%), 0.2 at 512^2
@@ -1196,7 +1409,10 @@ void session_advance(MagnusSession* s, size_t n_windows) {
         s->ctx = &c2;
         s->timing = false;
         try {
-            stream_loop(s, stop, M1);
+            if (term2_enabled(*s))
+                stream_loop2(s, stop, M1);
+            else
+                stream_loop(s, stop, M1);
         } catch (...) {
             s->ctx = c1;
             s->timing = tim;
@@ -1250,7 +1466,10 @@ void session_advance(MagnusSession* s, size_t n_windows) {
         s->cur_window = stop;
         return;
     }
-    stream_loop(s, stop, 0);
+    if (term2_enabled(*s))
+        stream_loop2(s, stop, 0);
+    else
+        stream_loop(s, stop, 0);
     s->cur_window = stop;
 }
 

@@ -209,6 +209,20 @@ void launch_term_nt128(s2b_context* ctx, int variant, const TermArgs& a, int nt,
 void launch_term_nt256(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
 void launch_term_nt512(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
 
+// Two Taylor terms per pass (term2_kernel.cuh): the extra state of the two-term engine
+struct Term2Args {
+    double* S2;              // third accumulator buffer
+    int* tpar;               // per path: which T buffer holds t_{k-1}
+    unsigned long long* tn2; // running max |t_{k+1}| (bits)
+    unsigned long long* sn2; // running max |s_{k+1}| (bits)
+};
+void launch_term2_nt128(s2b_context* ctx, int variant, const TermArgs& a, const Term2Args& b, int nt, size_t smem,
+                        size_t work);
+void launch_term2_nt256(s2b_context* ctx, int variant, const TermArgs& a, const Term2Args& b, int nt, size_t smem,
+                        size_t work);
+void launch_term2_nt512(s2b_context* ctx, int variant, const TermArgs& a, const Term2Args& b, int nt, size_t smem,
+                        size_t work);
+
 // Streaming term kernel for uncompressed (x-dependent) weights with a Langevin union mask
 // (term_var.cu); S2B_TERMVAR=0 falls back to term_generic_k_kernel.
 bool term_var_supported(const s2b_operator* op);

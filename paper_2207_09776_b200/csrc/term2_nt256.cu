@@ -1,0 +1,18 @@
+// term2_kernel instantiations (the Langevin stencils, variants 7-9) for blocks of up to 256 threads.
+#include "term2_kernel.cuh"
+
+namespace s2b {
+namespace mg {
+
+void launch_term2_nt256(s2b_context* ctx, int variant, const TermArgs& a, const Term2Args& b, int nt, size_t smem,
+                        size_t work) {
+    switch (variant) {
+    case 7: launch_term2_nt<7, 256>(ctx, a, b, nt, smem, work); return;
+    case 8: launch_term2_nt<8, 256>(ctx, a, b, nt, smem, work); return;
+    case 9: launch_term2_nt<9, 256>(ctx, a, b, nt, smem, work); return;
+    }
+    fail(S2B_ERR_RUNTIME, "term2 kernel: unknown variant");
+}
+
+} // namespace mg
+} // namespace s2b

@@ -126,18 +126,20 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     }
     __syncthreads();
     uint32_t ph = 0; // parity of the next wait on each weight buffer (bit b)
-    // warp 0 streams row jw's weights (NP rows of nx doubles) into buffer jw & 1: lane 0 arms
-    // the barrier, then every lane issues the bulk copies of its pairs
-    auto issue = [&](int jw) {
-        double* dst = wbuf + static_cast<size_t>(jw & 1) * NP * nx;
-        if (lane == 0) {
+    // Row jw's weights (NP rows of nx doubles) stream into buffer jw & 1.  Thread 0 arms the
+    // buffer's barrier (expect_tx) while the buffer's previous phase is complete and before the
+    // CTA barrier that precedes the copies; the NP bulk copies are then issued by threads spread
+    // over every warp (one copy each), so no compute warp is delayed by the issue.
+    constexpr int SPREAD = kVarNT / NP > 0 ? kVarNT / NP : 1;
+    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * nx * 8)); };
+    auto copies = [&](int jw) {
+        const int q = t / SPREAD;
+        if (t % SPREAD == 0 && q < NP) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
-            mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * nx * 8));
+            tma_row(wbuf + static_cast<size_t>(jw & 1) * NP * nx + static_cast<size_t>(q) * nx,
+                    a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx, static_cast<uint32_t>(nx * 8),
+                    &bar[jw & 1]);
         }
-        __syncwarp();
-        for (int q = lane; q < NP; q += 32)
-            tma_row(dst + static_cast<size_t>(q) * nx, a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx,
-                    static_cast<uint32_t>(nx * 8), &bar[jw & 1]);
     };
 
     const int live = a.cnt[0];
@@ -173,7 +175,12 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
             for (int q = 0; q < 6; ++q) c[k][q] = pk[k] >= 0 ? cp[q] : 0.0;
         }
         __syncthreads(); // the previous item is done with the ring and both weight buffers
-        if (TW && warp == 0) issue(j0);
+        if (TW && t == 0) {
+            arm(j0);
+            if (j0 + 1 < j1) arm(j0 + 1);
+        }
+        __syncthreads(); // armed before any copy lands
+        if (TW) copies(j0);
         // ring rows j0-KRV .. j0+KRV (zero outside the grid)
         for (int jr = j0 - KRV; jr <= j0 + KRV; ++jr) {
 #pragma unroll
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 
         for (int j = j0; j < j1; ++j) {
             // the next row's weights (its buffer was last read in row j-1, before the barrier)
-            if (TW && warp == 0 && j + 1 < j1) issue(j + 1);
+            if (TW && j + 1 < j1) copies(j + 1);
             // prefetch: the ring's next row and this row's accumulator
             const int jn = j + KRV + 1;
             double nxt[K][XPT], sacc[K][XPT];
@@ -272,6 +279,8 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
                     if (i < nx) dst[i] = nxt[k][u];
                 }
             }
+            // buffer j & 1 is read in this row only: its next phase (row j + 2) may be armed
+            if (TW && t == 0 && j + 2 < j1) arm(j + 2);
             __syncthreads();
         }
         // path-wide maxima: warp -> CTA -> one atomic per path
@@ -333,17 +342,17 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     __syncthreads();
     uint32_t ph = 0;
     int xlo = 0, wpart = NT; // current part: first column, width in the grid
-    auto issue = [&](int jw) {
-        double* dst = wbuf + static_cast<size_t>(jw & 1) * NP * NT;
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * wpart * 8));
-        }
-        __syncwarp();
-        for (int q = lane; q < NP; q += 32)
-            tma_row(dst + static_cast<size_t>(q) * NT,
-                    a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx + xlo,
-                    static_cast<uint32_t>(wpart * 8), &bar[jw & 1]);
+    // as term_var_kernel: thread 0 arms, the copies are spread over all warps
+    constexpr int SPREAD = NT / NP > 0 ? NT / NP : 1;
+    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * wpart * 8)); };
+    auto copies = [&](int jw) {
+        for (int q = t / SPREAD; q < NP; q += NT / SPREAD)
+            if (t % SPREAD == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma_row(wbuf + static_cast<size_t>(jw & 1) * NP * NT + static_cast<size_t>(q) * NT,
+                        a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx + xlo,
+                        static_cast<uint32_t>(wpart * 8), &bar[jw & 1]);
+            }
     };
     auto slot = [](int jr) { return ((jr % RING) + RING) % RING; };
 
@@ -389,7 +398,12 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
             for (int q = 0; q < 6; ++q) c[k][q] = pk[k] >= 0 ? cp[q] : 0.0;
         }
         __syncthreads(); // the previous item is done with the ring and both weight buffers
-        if (warp == 0) issue(j0);
+        if (t == 0) {
+            arm(j0);
+            if (j0 + 1 < j1) arm(j0 + 1);
+        }
+        __syncthreads(); // armed before any copy lands
+        copies(j0);
         auto fill = [&](int k, int jr, double v_own, double v_h) {
             double* dst = ring + (static_cast<size_t>(k) * RING + slot(jr)) * RWS;
             if (act) dst[KRX + t] = v_own;
@@ -409,7 +423,7 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
         for (int k = 0; k < K; ++k) tb[k] = sb[k] = 0;
 
         for (int j = j0; j < j1; ++j) {
-            if (warp == 0 && j + 1 < j1) issue(j + 1);
+            if (j + 1 < j1) copies(j + 1);
             const int jn = j + KRV + 1;
             double nxt[K], nxh[K], sacc[K];
 #pragma unroll
@@ -466,6 +480,7 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
             // thread is past its reads of that slot only after the barrier of row j - 1
 #pragma unroll
             for (int k = 0; k < K; ++k) fill(k, jn, nxt[k], nxh[k]);
+            if (t == 0 && j + 2 < j1) arm(j + 2); // buffer j & 1's next phase (see term_var_kernel)
             __syncthreads();
         }
 #pragma unroll
