@@ -143,8 +143,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
     // push into T[0] then; re-zeroed after use)
     double* yscr = CL == 1 ? T : scr;
     static_assert(RPC * L::NYE <= (CL == 1 ? 2 : 1) * TBUF, "Y fold scratch must fit the term buffers");
-    __shared__ unsigned long long slots[2][kXmCl][2]; // CTA maxima of every rank, per parity
-    __shared__ unsigned long long red[NW][2];
+    __shared__ unsigned long long slots[2][kXmCl * NW][2]; // warp maxima of every rank, per parity
     __shared__ double c[6];
     __shared__ int next_path;
 
@@ -160,6 +159,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
         rem = cluster.map_shared_rank(T, rank + 1) + (x0 + KRX) * TR + (r - RPC + KRV);
     const bool do_rem = rem != nullptr;
     unsigned long long* slot_dst = cluster.map_shared_rank(&slots[0][0][0], lane < kXmCl ? lane : 0);
+    static_assert(kXmCl * NW <= 64, "slot reduction covers two entries per lane");
     int* next0 = cluster.map_shared_rank(&next_path, 0);
 
     // own (row, x) element offsets
@@ -379,26 +379,25 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
                     for (int cbase = 0; cbase < LX - XB; cbase += XB) block(cbase, std::false_type{});
                     block(LX - XB, std::true_type{});
                     if (ex == 0x7ff00000u) sm = __longlong_as_double(0x7FF8000000000000LL); // non-finite
-                    // path-wide max|t|, max|accum| (NaN-ranked): warps -> CTA -> every rank
+                    // path-wide max|t|, max|accum| (NaN-ranked): every warp pushes its maxima into
+                    // a slot of every rank (lane l -> rank l, DSMEM), so no CTA barrier sits in the
+                    // term loop; after the cluster barrier each warp reduces all CL x NW slots
                     const unsigned long long wtb = warp_max_bits(dbits(tm));
                     const unsigned long long wsb = warp_max_bits(dbits(sm));
-                    if (lane == 0) {
-                        red[warp][0] = wtb;
-                        red[warp][1] = wsb;
-                    }
-                    __syncthreads();
                     const int kp = gterm & 1;
-                    if (warp == 0) {
-                        const unsigned long long ct = warp_max_bits(lane < NW ? red[lane][0] : 0ull);
-                        const unsigned long long cs = warp_max_bits(lane < NW ? red[lane][1] : 0ull);
-                        if (lane < kXmCl) {
-                            slot_dst[(kp * kXmCl + rank) * 2 + 0] = ct;
-                            slot_dst[(kp * kXmCl + rank) * 2 + 1] = cs;
-                        }
+                    if (lane < kXmCl) {
+                        slot_dst[((kp * kXmCl + rank) * NW + warp) * 2 + 0] = wtb;
+                        slot_dst[((kp * kXmCl + rank) * NW + warp) * 2 + 1] = wsb;
                     }
                     cluster_barrier();
-                    const unsigned long long tball = warp_max_bits(lane < kXmCl ? slots[kp][lane][0] : 0ull);
-                    const unsigned long long sball = warp_max_bits(lane < kXmCl ? slots[kp][lane][1] : 0ull);
+                    unsigned long long tball = 0ull, sball = 0ull;
+#pragma unroll
+                    for (int q = lane; q < kXmCl * NW; q += 32) {
+                        tball = umax64(tball, slots[kp][q][0]);
+                        sball = umax64(sball, slots[kp][q][1]);
+                    }
+                    tball = warp_max_bits(tball);
+                    sball = warp_max_bits(sball);
                     int dec = 0;
                     if (tball >= kInfBits || sball >= kInfBits) {
                         dec = 2; // Overflow
