@@ -995,10 +995,13 @@ void launch_term(MagnusSession& s) {
 }
 
 // The two-term engine applies to the compressed Langevin stencils (variants 7-9, even nx up to
-// 1024); S2B_TERM2=0 keeps the one-term passes (A/B measurements).
+// 1024).  It is opt-in (S2B_TERM2=1): bitwise equal to the one-term passes, but measured slower
+// on B200 -- 0.30 vs 0.66 of HBM at 1024^2 (512 threads spill at 128 registers), 6.30e8 vs
+// 6.69e8 windows/s at cfg4 and 1.38e9 vs 1.41e9 at cfg2 as the hybrid slice (one 241-register
+// CTA per SM: the per-row barrier and the fold are exposed) -- see DESIGN.md.
 bool term2_enabled(const MagnusSession& s) {
     const char* e = std::getenv("S2B_TERM2");
-    if (e && e[0] == '0') return false;
+    if (!(e && e[0] == '1')) return false;
     const int v = s.op->variant;
     return v >= 7 && v <= 9 && s.op->nx % 2 == 0 && s.op->nx >= 6 && s.op->nx <= 1024;
 }

@@ -40,6 +40,7 @@ CASES = {
     "cluster_band-256": (lambda s, c: _magnus(s, c, 256, M=3, order=2), {"S2B_XM": "0"}),
     "term_tma-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream"}),
     "term_tma-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {}),
+    "term2-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream", "S2B_TERM2": "1"}),
     "term_var-256": (lambda s, c: _magnus(s, c, 256, "langevin-variable", M=5, dt=0.001), {}),
     "em_cluster_ip-64": (lambda s, c: _euler(s, c, 64, M=7), {}),
     "em_cluster_ip-256": (lambda s, c: _euler(s, c, 256, M=4), {}),
