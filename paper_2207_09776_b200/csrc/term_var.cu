@@ -23,6 +23,8 @@
 #include <type_traits>
 #include <utility>
 
+#include <cuda.h> // CUtensorMap (the encoder comes from cudaGetDriverEntryPoint: no libcuda link)
+
 #include "magnus_common.cuh"
 
 namespace s2b {
@@ -39,6 +41,17 @@ __device__ __forceinline__ void static_for(F&& f) {
     [&]<int... I>(std::integer_sequence<int, I...>) {
         (f(std::integral_constant<int, I>{}), ...);
     }(std::make_integer_sequence<int, N>{});
+}
+
+// One weight row for all NP source pairs in ONE tensor copy: the weights W[pair][row][x] as a
+// 3-D tensor map (x, row, pair), box (columns, 1, NP) -> shared [NP][columns].  (Per-pair bulk
+// copies need uniform operands; issued from many lanes they serialise in a waterfall loop.)
+__device__ __forceinline__ void tma_w3d(void* dst, const CUtensorMap* map, int x, int row, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(row), "r"(0), "r"(smem_u32(bar))
+        : "memory");
 }
 
 // The operator's exact structure as a template parameter: the union stencil (mask), the number
@@ -101,7 +114,8 @@ constexpr VarFam kFams[] = {kFam19v, kFam19c, kFam11, kFam5, kFamK11, kFamK23};
 // TW: the weight rows stream through shared memory (TMA, double-buffered); otherwise (grids
 // whose two weight rows do not fit next to the ring) each point loads its weights from L2.
 template <int K, int FI, int KRX, int KRV, int XPT, bool TW>
-__global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int strips) {
+__global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int strips,
+                                                             const __grid_constant__ CUtensorMap wmap) {
     constexpr uint64_t MASK = kFams[FI].mask;
     using PF = Fam<kFams[FI]>;
     static_assert(2 * KRV + 2 <= kRing, "ring too short");
@@ -130,15 +144,11 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     // buffer's barrier (expect_tx) while the buffer's previous phase is complete and before the
     // CTA barrier that precedes the copies; the NP bulk copies are then issued by threads spread
     // over every warp (one copy each), so no compute warp is delayed by the issue.
-    constexpr int SPREAD = kVarNT / NP > 0 ? kVarNT / NP : 1;
     auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * nx * 8)); };
-    auto copies = [&](int jw) {
-        const int q = t / SPREAD;
-        if (t % SPREAD == 0 && q < NP) {
+    auto copies = [&](int jw) { // one tensor copy of the row's NP weight rows, from the last warp
+        if (TW && t == kVarNT - 32) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
-            tma_row(wbuf + static_cast<size_t>(jw & 1) * NP * nx + static_cast<size_t>(q) * nx,
-                    a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx, static_cast<uint32_t>(nx * 8),
-                    &bar[jw & 1]);
+            tma_w3d(wbuf + static_cast<size_t>(jw & 1) * NP * nx, &wmap, 0, jw, &bar[jw & 1]);
         }
     };
 
@@ -315,7 +325,8 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 // The ring (RING = 2*KRV+2 rows, slot = row mod RING) holds the part's columns plus KRX halo
 // columns on each side (the neighbour part's values, zero outside the grid).
 template <int K, int FI, int KRX, int KRV, int NT>
-__global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast) {
+__global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast,
+                                                                                  const __grid_constant__ CUtensorMap wmap) {
     constexpr uint64_t MASK = kFams[FI].mask;
     using PF = Fam<kFams[FI]>;
     constexpr int RING = 2 * KRV + 2;
@@ -342,17 +353,14 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     __syncthreads();
     uint32_t ph = 0;
     int xlo = 0, wpart = NT; // current part: first column, width in the grid
-    // as term_var_kernel: thread 0 arms, the copies are spread over all warps
-    constexpr int SPREAD = NT / NP > 0 ? NT / NP : 1;
-    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * wpart * 8)); };
+    // as term_var_kernel: thread 0 arms (the full box: columns past the grid arrive as zeros),
+    // the last warp issues one tensor copy per row
+    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * NT * 8)); };
     auto copies = [&](int jw) {
-        for (int q = t / SPREAD; q < NP; q += NT / SPREAD)
-            if (t % SPREAD == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                tma_row(wbuf + static_cast<size_t>(jw & 1) * NP * NT + static_cast<size_t>(q) * NT,
-                        a.op.w + static_cast<size_t>(q) * n + static_cast<size_t>(jw) * nx + xlo,
-                        static_cast<uint32_t>(wpart * 8), &bar[jw & 1]);
-            }
+        if (t == NT - 32) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_w3d(wbuf + static_cast<size_t>(jw & 1) * NP * NT, &wmap, xlo, jw, &bar[jw & 1]);
+        }
     };
     auto slot = [](int jr) { return ((jr % RING) + RING) % RING; };
 
@@ -542,6 +550,32 @@ size_t var_smem(int np, int k, int nx, int krx) {
 
 constexpr int kVarxNT = 128; // columns (threads) per CTA of the x-split kernel
 
+// W[pair][row][x] (x contiguous) as a 3-D tensor map with box (cols, 1, np)
+CUtensorMap weight_map(const TermArgs& a, int np, int cols) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        S2B_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) fail(S2B_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    const cuuint64_t nx = static_cast<cuuint64_t>(a.op.nx), nv = static_cast<cuuint64_t>(a.op.nv);
+    const cuuint64_t dims[3] = {nx, nv, static_cast<cuuint64_t>(np)};
+    const cuuint64_t strides[2] = {nx * 8, nx * nv * 8};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(cols), 1, static_cast<cuuint32_t>(np)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap m;
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.op.w), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(S2B_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weight rows");
+    return m;
+}
+
 template <int K, int FI, int KRX, int KRV>
 void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     constexpr int NP = Fam<kFams[FI]>::off(MaskInfo<kFams[FI].mask>::count());
@@ -573,7 +607,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
             const size_t items = (live_max + KX - 1) / KX * static_cast<size_t>(strips) * parts;
             const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
             const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
-            kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
+            kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0, weight_map(a, NP, NT));
             ctx->k_stream = reinterpret_cast<const void*>(kern);
         };
         const char* en = std::getenv("S2B_VARX_NT");
@@ -604,7 +638,9 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         const size_t items = (live_max + K - 1) / K * static_cast<size_t>(strips);
         const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
         const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
-        kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips);
+        CUtensorMap wm{};
+        if (tw) wm = weight_map(a, NP, nx);
+        kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips, wm);
         ctx->k_stream = reinterpret_cast<const void*>(kern);
     };
     if constexpr (NP <= 40) {
