@@ -128,7 +128,9 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 
     extern __shared__ __align__(128) double vsm[];
     double* wbuf = vsm;                                          // [2][NP][nx] weights of rows j, j+1
-    double* ring = wbuf + (TW ? 2 * static_cast<size_t>(NP) * nx : 0); // [K][kRing][RWS]
+    // weight buffers padded to 128 bytes: a tensor copy needs a 128-byte aligned destination
+    const size_t WSTR = (static_cast<size_t>(NP) * nx + 15) / 16 * 16;
+    double* ring = wbuf + (TW ? 2 * WSTR : 0); // [K][kRing][RWS]
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ unsigned long long red[K][2][kVarNT / 32];
 
@@ -148,7 +150,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     auto copies = [&](int jw) { // one tensor copy of the row's NP weight rows, from the last warp
         if (TW && t == kVarNT - 32) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
-            tma_w3d(wbuf + static_cast<size_t>(jw & 1) * NP * nx, &wmap, 0, jw, &bar[jw & 1]);
+            tma_w3d(wbuf + (jw & 1) * WSTR, &wmap, 0, jw, &bar[jw & 1]);
         }
     };
 
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
                 mbar_wait(&bar[j & 1], (ph >> (j & 1)) & 1u);
                 ph ^= 1u << (j & 1);
             }
-            const double* wr = wbuf + static_cast<size_t>(j & 1) * NP * nx;
+            const double* wr = wbuf + (j & 1) * WSTR;
 #pragma unroll
             for (int u = 0; u < XPT; ++u) {
                 const int i = t + u * kVarNT;
@@ -545,7 +547,7 @@ int fam_of(const s2b_operator* op) {
 
 // shared memory of one CTA: two weight rows + the K-path ring must fit 227 KB
 size_t var_smem(int np, int k, int nx, int krx) {
-    return (2 * static_cast<size_t>(np) * nx + static_cast<size_t>(k) * kRing * (nx + 2 * krx)) * 8;
+    return (2 * ((static_cast<size_t>(np) * nx + 15) / 16 * 16) + static_cast<size_t>(k) * kRing * (nx + 2 * krx)) * 8;
 }
 
 constexpr int kVarxNT = 128; // columns (threads) per CTA of the x-split kernel
@@ -630,7 +632,8 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         return;
     }
     const bool tw = nx <= kVarNT;
-    const size_t smem = ((tw ? 2 * static_cast<size_t>(NP) * nx : 0) + static_cast<size_t>(K) * kRing * (nx + 2 * KRX)) * 8;
+    const size_t smem = ((tw ? 2 * ((static_cast<size_t>(NP) * nx + 15) / 16 * 16) : 0) +
+                         static_cast<size_t>(K) * kRing * (nx + 2 * KRX)) * 8;
     auto go = [&](auto kern) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
