@@ -330,6 +330,15 @@ def run_reference(args):
     return 0
 
 
+def lib_sha256():
+    import hashlib
+    try:
+        with open(os.path.join(ROOT, "paper_2207_09776_b200", "lib", "libspde2d_b200.so"), "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()
+    except Exception:
+        return None
+
+
 def load_profile(name):
     try:
         with open(os.path.join(ROOT, "profiles", name)) as f:
@@ -437,6 +446,7 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
             "traffic_source": f"profiles/{prof_name} (ncu dram__bytes, scaled per launch)"
                               + (" + the streaming-engine capture of the hybrid slice" if hyb else ""),
             "stale_profile": bool(stale or stream_stale),
+            "profile_same_binary": (not stale) and prof.get("lib_sha256") == lib_sha256(),
             "hybrid_paths": hyb, "note": engine["note"]}
     if stale:
         roof["profile_kernel"] = prof.get("kernel_mangled") or prof.get("kernel")

@@ -7,6 +7,7 @@ usage: python scripts/ncu_r02.py name ...   (then rm gpurun_out/prof_*.ncu-rep)
 """
 import csv
 import gzip
+import hashlib
 import io
 import json
 import os
@@ -69,8 +70,10 @@ def main():
         except Exception:
             pass
         tot = sum(mix.values()) or 1.0
+        lib = os.path.join("paper_2207_09776_b200", "lib", "libspde2d_b200.so")
         s = {
             "kernel": d["Kernel Name"][0],
+            "lib_sha256": hashlib.sha256(open(lib, "rb").read()).hexdigest(),
             "kernel_mangled": dm["Kernel Name"][0],
             "capture": f"ncu --set full --clock-control none --import-source on, one launch; scripts/prof_r02.sh {name}",
             "duration_ms": dur * 1e3,
