@@ -403,6 +403,10 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
             engine["kernel"] = "term_varx_kernel"  # x-split variant: wide grids, 64 source pairs
     names = ctx.kernel_names()
     launched = names["stream"] if engine["name"] == "stream" else names["cluster"]
+    for kname in ("term_varx_kernel", "term_var_kernel", "term_generic_k_kernel", "term2_kernel", "term_tma_kernel"):
+        if engine["name"] == "stream" and kname in launched:
+            engine["kernel"] = kname  # the name of the kernel that actually ran
+            break
     hyb = st1.get("hybrid_paths", 0) or 0
     prof_name = PROFILE_OF.get((a.preset, a.family, engine["name"])) or engine["profile"]
     prof = load_profile(prof_name)

@@ -17,7 +17,7 @@ from collections import Counter
 
 OUT = "gpurun_out"
 UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9,
-        "second": 1.0}
+        "second": 1.0, "ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0, "GB": 1e9, "MB": 1e6, "KB": 1e3, "B": 1.0}
 
 
 def raw(rep, mangled=False):
