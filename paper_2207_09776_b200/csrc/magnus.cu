@@ -717,6 +717,13 @@ s2b_operator* make_operator(s2b_context* ctx, const s2b_grid* grid, int order,
     } else {
         hw.assign(static_cast<size_t>(op->npairs) * n, 0.0);
         for (size_t q = 0; q < pw.size(); ++q) std::copy(pw[q]->begin(), pw[q]->end(), hw.begin() + q * n);
+        // point-major copy for the term_var kernels: one row's weights are one contiguous block
+        const size_t npp = static_cast<size_t>(op->npairs | 1);
+        std::vector<double> hp(npp * n, 0.0);
+        for (size_t q = 0; q < pw.size(); ++q)
+            for (size_t r = 0; r < n; ++r) hp[r * npp + q] = (*pw[q])[r];
+        op->d_wpm.alloc(hp.size());
+        S2B_CUDA(cudaMemcpy(op->d_wpm.p, hp.data(), hp.size() * sizeof(double), cudaMemcpyHostToDevice));
     }
     op->d_w.alloc(hw.size());
     op->d_pair_begin.alloc(op->pair_begin.size());
@@ -910,7 +917,7 @@ void swap_lists(MagnusSession& s) {
 TermArgs term_args(MagnusSession& s) {
     TermArgs a{};
     a.op = OpView{s.op->d_pair_begin.p, s.op->d_pair_slot.p, s.op->d_w.p, static_cast<int>(s.op->nx),
-                  static_cast<int>(s.op->nv), s.op->compressed};
+                  static_cast<int>(s.op->nv), s.op->compressed, s.op->d_wpm.p};
     a.ctab = s.ctab.p;
     a.nwin = static_cast<int>(s.nwin);
     a.act = s.act[s.cur].p;

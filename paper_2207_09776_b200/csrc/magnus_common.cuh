@@ -42,6 +42,7 @@ struct OpView {
     const double* w;
     int nx, nv;
     int compressed;
+    const double* wpm = nullptr; // uncompressed weights point-major [row][x][npairs | 1] (term_var)
 };
 
 struct TermArgs {

@@ -106,6 +106,7 @@ struct s2b_operator {
     uint32_t bmask = 0;       // Y entries that differ on x-boundary classes (in-grid offsets)
     // compressed: W[pair][j][cls]; full: W[pair][row]
     s2b::DevBuf<double> d_w;
+    s2b::DevBuf<double> d_wpm; // uncompressed: point-major copy [row][x][npairs | 1] (term_var kernels)
     double dx_delta = 0.0, dv_delta = 0.0;
     s2b_grid grid{};
 };

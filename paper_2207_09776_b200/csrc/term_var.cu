@@ -23,8 +23,6 @@
 #include <type_traits>
 #include <utility>
 
-#include <cuda.h> // CUtensorMap (the encoder comes from cudaGetDriverEntryPoint: no libcuda link)
-
 #include "magnus_common.cuh"
 
 namespace s2b {
@@ -41,17 +39,6 @@ __device__ __forceinline__ void static_for(F&& f) {
     [&]<int... I>(std::integer_sequence<int, I...>) {
         (f(std::integral_constant<int, I>{}), ...);
     }(std::make_integer_sequence<int, N>{});
-}
-
-// One weight row for all NP source pairs in ONE tensor copy: the weights W[pair][row][x] as a
-// 3-D tensor map (x, row, pair), box (columns, 1, NP) -> shared [NP][columns].  (Per-pair bulk
-// copies need uniform operands; issued from many lanes they serialise in a waterfall loop.)
-__device__ __forceinline__ void tma_w3d(void* dst, const CUtensorMap* map, int x, int row, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(row), "r"(0), "r"(smem_u32(bar))
-        : "memory");
 }
 
 // The operator's exact structure as a template parameter: the union stencil (mask), the number
@@ -114,8 +101,7 @@ constexpr VarFam kFams[] = {kFam19v, kFam19c, kFam11, kFam5, kFamK11, kFamK23};
 // TW: the weight rows stream through shared memory (TMA, double-buffered); otherwise (grids
 // whose two weight rows do not fit next to the ring) each point loads its weights from L2.
 template <int K, int FI, int KRX, int KRV, int XPT, bool TW>
-__global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int strips,
-                                                             const __grid_constant__ CUtensorMap wmap) {
+__global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int strips) {
     constexpr uint64_t MASK = kFams[FI].mask;
     using PF = Fam<kFams[FI]>;
     static_assert(2 * KRV + 2 <= kRing, "ring too short");
@@ -127,9 +113,9 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
     extern __shared__ __align__(128) double vsm[];
-    double* wbuf = vsm;                                          // [2][NP][nx] weights of rows j, j+1
-    // weight buffers padded to 128 bytes: a tensor copy needs a 128-byte aligned destination
-    const size_t WSTR = (static_cast<size_t>(NP) * nx + 15) / 16 * 16;
+    double* wbuf = vsm;                                          // [2][nx][NPP] weights of rows j, j+1
+    constexpr int NPP = NP | 1; // point-major weight stride (odd: conflict-free 8-byte lanes)
+    const size_t WSTR = static_cast<size_t>(nx) * NPP; // one row's weights (nx even: 16-byte multiple)
     double* ring = wbuf + (TW ? 2 * WSTR : 0); // [K][kRing][RWS]
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ unsigned long long red[K][2][kVarNT / 32];
@@ -146,11 +132,12 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     // buffer's barrier (expect_tx) while the buffer's previous phase is complete and before the
     // CTA barrier that precedes the copies; the NP bulk copies are then issued by threads spread
     // over every warp (one copy each), so no compute warp is delayed by the issue.
-    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * nx * 8)); };
-    auto copies = [&](int jw) { // one tensor copy of the row's NP weight rows, from the last warp
+    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(WSTR * 8)); };
+    auto copies = [&](int jw) { // the row's weights are contiguous point-major: one bulk copy, last warp
         if (TW && t == kVarNT - 32) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
-            tma_w3d(wbuf + (jw & 1) * WSTR, &wmap, 0, jw, &bar[jw & 1]);
+            tma_row(wbuf + (jw & 1) * WSTR, a.op.wpm + static_cast<size_t>(jw) * WSTR, static_cast<uint32_t>(WSTR * 8),
+                    &bar[jw & 1]);
         }
     };
 
@@ -240,7 +227,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
                 double wg[TW ? 1 : NP]; // the point's weights, all loads in flight at once
                 if constexpr (!TW) {
 #pragma unroll
-                    for (int q = 0; q < NP; ++q) wg[q] = __ldg(a.op.w + static_cast<size_t>(q) * n + r);
+                    for (int q = 0; q < NP; ++q) wg[q] = __ldg(a.op.wpm + r * NPP + q);
                 }
                 double acc[K];
 #pragma unroll
@@ -258,7 +245,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
                         constexpr int q = q0 + decltype(C)::value;
                         constexpr int sl = PF::slot(q);
                         double w;
-                        if constexpr (TW) w = wr[q * nx + i];
+                        if constexpr (TW) w = wr[i * NPP + q];
                         else w = wg[q];
 #pragma unroll
                         for (int k = 0; k < K; ++k) y[k] += c[k][sl] * w;
@@ -327,8 +314,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 // The ring (RING = 2*KRV+2 rows, slot = row mod RING) holds the part's columns plus KRX halo
 // columns on each side (the neighbour part's values, zero outside the grid).
 template <int K, int FI, int KRX, int KRV, int NT>
-__global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast,
-                                                                                  const __grid_constant__ CUtensorMap wmap) {
+__global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast) {
     constexpr uint64_t MASK = kFams[FI].mask;
     using PF = Fam<kFams[FI]>;
     constexpr int RING = 2 * KRV + 2;
@@ -341,8 +327,9 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
     extern __shared__ __align__(128) double vsm[];
-    double* wbuf = vsm;                               // [2][NP][NT] weights of rows j, j+1 (this part)
-    double* ring = wbuf + 2 * static_cast<size_t>(NP) * NT; // [K][RING][RWS]
+    constexpr int NPP = NP | 1;                       // point-major weight stride (odd: conflict-free)
+    double* wbuf = vsm;                               // [2][NT][NPP] weights of rows j, j+1 (this part)
+    double* ring = wbuf + 2 * static_cast<size_t>(NT) * NPP; // [K][RING][RWS]
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ unsigned long long red[K][2][NT / 32];
 
@@ -355,13 +342,15 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     __syncthreads();
     uint32_t ph = 0;
     int xlo = 0, wpart = NT; // current part: first column, width in the grid
-    // as term_var_kernel: thread 0 arms (the full box: columns past the grid arrive as zeros),
-    // the last warp issues one tensor copy per row
-    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(NP * NT * 8)); };
+    // as term_var_kernel: thread 0 arms, the last warp issues one bulk copy of the part's
+    // point-major weights per row (columns past the grid are never read)
+    auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(wpart * NPP * 8)); };
     auto copies = [&](int jw) {
         if (t == NT - 32) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tma_w3d(wbuf + static_cast<size_t>(jw & 1) * NP * NT, &wmap, xlo, jw, &bar[jw & 1]);
+            tma_row(wbuf + static_cast<size_t>(jw & 1) * NT * NPP,
+                    a.op.wpm + (static_cast<size_t>(jw) * nx + xlo) * NPP, static_cast<uint32_t>(wpart * NPP * 8),
+                    &bar[jw & 1]);
         }
     };
     auto slot = [](int jr) { return ((jr % RING) + RING) % RING; };
@@ -447,7 +436,7 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
             for (int d = 0; d <= 2 * KRV; ++d) sl[d] = slot(j - KRV + d);
             mbar_wait(&bar[j & 1], (ph >> (j & 1)) & 1u);
             ph ^= 1u << (j & 1);
-            const double* wr = wbuf + static_cast<size_t>(j & 1) * NP * NT;
+            const double* wr = wbuf + static_cast<size_t>(j & 1) * NT * NPP;
             if (act) {
                 const size_t r = static_cast<size_t>(j) * nx + i;
                 double acc[K];
@@ -464,7 +453,7 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
                     static_for<PF::cnt(e)>([&](auto C) {
                         constexpr int q = q0 + decltype(C)::value;
                         constexpr int ps = PF::slot(q);
-                        const double w = wr[q * NT + t];
+                        const double w = wr[t * NPP + q];
 #pragma unroll
                         for (int k = 0; k < K; ++k) y[k] += c[k][ps] * w;
                     });
@@ -547,36 +536,10 @@ int fam_of(const s2b_operator* op) {
 
 // shared memory of one CTA: two weight rows + the K-path ring must fit 227 KB
 size_t var_smem(int np, int k, int nx, int krx) {
-    return (2 * ((static_cast<size_t>(np) * nx + 15) / 16 * 16) + static_cast<size_t>(k) * kRing * (nx + 2 * krx)) * 8;
+    return (2 * static_cast<size_t>(np | 1) * nx + static_cast<size_t>(k) * kRing * (nx + 2 * krx)) * 8;
 }
 
 constexpr int kVarxNT = 128; // columns (threads) per CTA of the x-split kernel
-
-// W[pair][row][x] (x contiguous) as a 3-D tensor map with box (cols, 1, np)
-CUtensorMap weight_map(const TermArgs& a, int np, int cols) {
-    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static EncodeFn encode = nullptr;
-    if (!encode) {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        S2B_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) fail(S2B_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        encode = reinterpret_cast<EncodeFn>(fn);
-    }
-    const cuuint64_t nx = static_cast<cuuint64_t>(a.op.nx), nv = static_cast<cuuint64_t>(a.op.nv);
-    const cuuint64_t dims[3] = {nx, nv, static_cast<cuuint64_t>(np)};
-    const cuuint64_t strides[2] = {nx * 8, nx * nv * 8};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(cols), 1, static_cast<cuuint32_t>(np)};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    CUtensorMap m;
-    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.op.w), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(S2B_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weight rows");
-    return m;
-}
 
 template <int K, int FI, int KRX, int KRV>
 void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
@@ -601,7 +564,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
             constexpr int NT = decltype(ntag)::value;
             constexpr int KX = decltype(ktag)::value; // paths per item
             auto kern = term_varx_kernel<KX, FI, KRX, KRV, NT>;
-            const size_t smem = (2 * static_cast<size_t>(NP) * NT + KX * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
+            const size_t smem = (2 * static_cast<size_t>(NP | 1) * NT + KX * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
             S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             int per_sm = 0;
             S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
@@ -609,7 +572,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
             const size_t items = (live_max + KX - 1) / KX * static_cast<size_t>(strips) * parts;
             const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
             const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
-            kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0, weight_map(a, NP, NT));
+            kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
             ctx->k_stream = reinterpret_cast<const void*>(kern);
         };
         const char* en = std::getenv("S2B_VARX_NT");
@@ -632,7 +595,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         return;
     }
     const bool tw = nx <= kVarNT;
-    const size_t smem = ((tw ? 2 * ((static_cast<size_t>(NP) * nx + 15) / 16 * 16) : 0) +
+    const size_t smem = ((tw ? 2 * static_cast<size_t>(NP | 1) * nx : 0) +
                          static_cast<size_t>(K) * kRing * (nx + 2 * KRX)) * 8;
     auto go = [&](auto kern) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -641,9 +604,7 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         const size_t items = (live_max + K - 1) / K * static_cast<size_t>(strips);
         const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
         const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
-        CUtensorMap wm{};
-        if (tw) wm = weight_map(a, NP, nx);
-        kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips, wm);
+        kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips);
         ctx->k_stream = reinterpret_cast<const void*>(kern);
     };
     if constexpr (NP <= 40) {
