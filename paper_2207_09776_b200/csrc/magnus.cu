@@ -44,6 +44,25 @@ using namespace mg;
 
 int mg::tma_popcount(int variant) { return __builtin_popcountll(kVariants[variant].mask); }
 
+// term_tma_kernel's shared memory: the TMA rings and the coefficient table, plus YST doubles per
+// strip row (term_kernel.cuh); the strip height is capped so that the total fits kTermSmem
+size_t mg::tma_smem_fixed(int variant, size_t nx) {
+    const size_t nye = static_cast<size_t>(kClasses) * tma_popcount(variant);
+    const size_t H = kVariants[variant].rx <= 2 ? 2 : 4;
+    return 128 + kStages * (nx + 2 * H) * 8 + kStages * nx * 8 + kPairSlots * nye * 8;
+}
+size_t mg::tma_strip_cap(int variant, size_t nx) {
+    const size_t nye = static_cast<size_t>(kClasses) * tma_popcount(variant);
+    const size_t yst = (nye + 1) & ~static_cast<size_t>(1);
+    // resident CTAs per SM of the launch's block-size class (NtClass: 128 -> 4, 256 -> 2, 512 -> 1),
+    // each with ~1 KB of static / reserved shared memory
+    const size_t nt = (std::max<size_t>((nx + 1) / 2, nye) + 31) / 32 * 32;
+    const size_t ctas = nt <= 128 ? 4 : (nt <= 256 ? 2 : 1);
+    const size_t budget = std::min(kTermSmem, (228 * 1024) / ctas - 2048);
+    const size_t fixed = tma_smem_fixed(variant, nx);
+    return budget > fixed + 8 * yst * 8 ? (budget - fixed) / (yst * 8) : 8;
+}
+
 namespace {
 
 // lebesgue_functionals (stochastics.cpp:121-141) + log_coefficients (magnus.cpp:26-40),
@@ -940,6 +959,15 @@ TermArgs term_args(MagnusSession& s) {
             while (a.strip_rows > 16 &&
                    s.M * ((s.op->nv + a.strip_rows - 1) / a.strip_rows) < 4 * static_cast<size_t>(s.ctx->num_sms))
                 a.strip_rows /= 2;
+        // term_tma_kernel keeps the strip's Y rows in shared memory: cap J by the budget, with
+        // balanced strips
+        if (s.op->variant != 0) {
+            const size_t jmax = tma_strip_cap(s.op->variant, s.op->nx);
+            if (static_cast<size_t>(a.strip_rows) > jmax) {
+                const size_t nstr = (s.op->nv + jmax - 1) / jmax;
+                a.strip_rows = static_cast<int>((s.op->nv + nstr - 1) / nstr);
+            }
+        }
     }
     a.nstrips = static_cast<int>((s.op->nv + a.strip_rows - 1) / a.strip_rows);
     a.wt = s.op->d_wt.p;
@@ -981,8 +1009,7 @@ void launch_term(MagnusSession& s) {
         const int nt = static_cast<int>((std::max<size_t>((s.op->nx + 1) / 2, nye) + 31) / 32 * 32);
         const int H = kVariants[variant].rx <= 2 ? 2 : 4;
         const size_t rw = 2 * static_cast<size_t>(nt) + 2 * H;
-        const size_t smem = 128 + kStages * (s.op->nx + 2 * H) * 8 + kStages * s.op->nx * 8 +
-                            ((2 + kPairSlots) * static_cast<size_t>(nye) + 2) * 8;
+        const size_t smem = tma_smem_fixed(variant, s.op->nx) + static_cast<size_t>(a.strip_rows) * ((nye + 1) & ~1) * 8;
         (void)rw;
         const size_t work = s.M * static_cast<size_t>(a.nstrips);
         if (nt <= 128)

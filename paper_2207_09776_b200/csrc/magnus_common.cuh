@@ -205,6 +205,9 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 // Block-size classes: (max threads, min resident blocks) -> register budget.
 int tma_popcount(int variant);
+constexpr size_t kTermSmem = 227 * 1024; // dynamic shared memory of term_tma_kernel (opt-in maximum)
+size_t tma_smem_fixed(int variant, size_t nx);
+size_t tma_strip_cap(int variant, size_t nx);
 // term_tma_kernel launchers, one translation unit per block-size class
 void launch_term_nt128(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);
 void launch_term_nt256(s2b_context* ctx, int variant, const TermArgs& a, int nt, size_t smem, size_t work);

@@ -6,15 +6,16 @@
 namespace s2b {
 namespace mg {
 
-// One work item = (live path, strip of kStripRows output rows).
+// One work item = (live path, strip of J = a.strip_rows output rows).
 //
 // Thread -> points: thread t < (nx-4)/2 owns the interior x-points 2t+2, 2t+3; the next two
 // threads own the x-boundary pairs {0, 1} and {nx-2, nx-1}, so every warp but the last reads
 // ONE interior Y set for both of its points.  Rows stream through a kStages-deep TMA ring
 // (stage s carries input row j0-KRV+s and accum row j0-2KRV+s); each thread keeps a
-// (2KRV+1)-row register window of its x-neighbourhood.  The Y values of the next output row
-// (5 x-classes x the mask's stencil points) are folded one step ahead by their owner threads
-// (thread q < NYE) from entry-major weights loaded one step earlier into registers.
+// (2KRV+1)-row register window of its x-neighbourhood.  The Y rows of the whole strip (5
+// x-classes x the mask's stencil points each) are folded into shared memory once per item, by
+// all threads, before the row loop: no warp does extra work inside the loop, so the per-row
+// barrier only waits for the ring (the host sizes J so that the strip's Y fits).
 template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NTMAX, int MINB>
 __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     constexpr int H = KRX <= 2 ? 2 : 4;             // zero halo (doubles) on each side
@@ -39,8 +40,8 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     double* rows = reinterpret_cast<double*>(smem_raw + 128); // kStages x RW
     double* srow = rows + kStages * RW;                       // kStages x nx
-    double* Ys = srow + kStages * nx;                         // 2 x YST
-    double* cq = Ys + 2 * YST;                                // KP x NYE
+    double* cq = srow + kStages * nx;                         // KP x NYE
+    double* Ys = cq + KP * NYE;                               // J x YST: the strip's Y rows
     const uint32_t full_u = smem_u32(full), rows_u = smem_u32(rows), srow_u = smem_u32(srow);
     __shared__ double c[6];
     __shared__ unsigned long long red[2][32];
@@ -59,31 +60,27 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
     const int clsB = t < nint ? 2 : (t == nint ? 1 : 4);
     const bool wfast = BM == 0 || __all_sync(0xffffffffu, t < nint || !active);
 
-    // Y entry owned by this thread (q = t < NYE; the launch makes NT >= NYE)
-    const bool owner = t < NYE;
-    double own_w[KP];
-    const double* wrow = a.wt + (owner ? t * KP : 0);
-    auto load_w = [&](int j) {
-        if (owner) {
-            const double2* src = reinterpret_cast<const double2*>(wrow + static_cast<size_t>(j) * NYE * KP);
+    // MagnusLogBuilder::fill fold (slots ascending from 0.0, zero coefficients skipped) of every
+    // Y entry of rows [j0, jend), spread over all threads
+    auto fold_strip = [&](int j0, int jend) {
+        const int total = (jend - j0) * NYE;
+        for (int u = t; u < total; u += NT) {
+            const int jr = u / NYE, e = u - jr * NYE;
+            const double2* src = reinterpret_cast<const double2*>(a.wt + (static_cast<size_t>(j0 + jr) * NYE + e) * KP);
+            double w[KP];
 #pragma unroll
             for (int k = 0; k < KP / 2; ++k) {
                 const double2 v = __ldg(src + k);
-                own_w[2 * k] = v.x;
-                own_w[2 * k + 1] = v.y;
+                w[2 * k] = v.x;
+                w[2 * k + 1] = v.y;
             }
-        }
-    };
-    // MagnusLogBuilder::fill fold: slots ascending from 0.0, zero coefficients skipped
-    auto fold_y = [&](int b) {
-        if (owner) {
             double y = 0.0;
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
-                const double cs = cq[k * NYE + t];
-                if (cs != 0.0) y += cs * own_w[k];
+                const double cs = cq[k * NYE + e];
+                if (cs != 0.0) y += cs * w[k];
             }
-            Ys[b * YST + t] = y;
+            Ys[jr * YST + e] = y;
         }
     };
 
@@ -129,14 +126,13 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
         }
         if (t < 6) c[t] = a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + t];
         __syncthreads();
-        if (owner) {
-#pragma unroll
-            for (int k = 0; k < KP; ++k) {
-                const int sl = __ldg(a.eslot + t * KP + k);
-                cq[k * NYE + t] = sl >= 0 ? c[sl] : 0.0;
-            }
+        for (int q = t; q < NYE * KP; q += NT) { // the coefficient of every (entry, pair slot)
+            const int e = q / KP, k = q - e * KP;
+            const int sl = __ldg(a.eslot + e * KP + k);
+            cq[k * NYE + e] = sl >= 0 ? c[sl] : 0.0;
         }
-        load_w(j0);
+        __syncthreads();
+        fold_strip(j0, jend);
         __syncthreads();
 
         double win[WROWS][2 * NP];
@@ -152,11 +148,6 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                 const int s = base + ph;
                 if (s < nsteps) {
                     if (t == 0 && s + kStages - 1 < nsteps) issue(s + kStages - 1);
-                    const int jn = j0 - 2 * KRV + s + 1; // output row of the next step
-                    if (jn >= j0 && jn < jend) {
-                        fold_y(jn & 1);
-                        if (jn + 1 < jend) load_w(jn + 1);
-                    }
                     const uint32_t g = gstep + s;
                     const uint32_t slot = g & (kStages - 1);
                     mbar_wait_u(full_u + 8 * slot, (g / kStages) & 1);
@@ -176,7 +167,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                     const int jo = r - KRV; // output row of this step
                     if (s >= 2 * KRV && jo < jend && active) {
                         const double2 sv = *reinterpret_cast<const double2*>(srow + slot * nx + p0);
-                        const double* yrow = Ys + (jo & 1) * YST;
+                        const double* yrow = Ys + (jo - j0) * YST;
                         double accA = 0.0, accB = 0.0;
                         // ascending stencil offset == ascending DIA diagonal (sparse.cpp:412-423)
                         if (wfast) {
@@ -231,7 +222,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                         tb = umax64(tb, umax64(abs_bits(tA), abs_bits(tB)));
                         sb = umax64(sb, umax64(abs_bits(sA), abs_bits(sB)));
                     }
-                    __syncthreads(); // ring slot and Y row consumed by every thread
+                    __syncthreads(); // ring slot consumed by every thread
                 }
             }
         }
@@ -270,7 +261,7 @@ void launch_term_nt(s2b_context* ctx, const TermArgs& a, int nt, size_t smem, si
     auto kern = term_tma_kernel<v.rx, v.rv, v.mask, v.bm, NTMAX, NtClass<NTMAX>::minb>;
     static int configured_device = -1;
     if (configured_device != ctx->device) {
-        S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTermSmem)));
         configured_device = ctx->device;
     }
     int blocks_per_sm = 1;
