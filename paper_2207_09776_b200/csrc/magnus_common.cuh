@@ -205,7 +205,7 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 // Block-size classes: (max threads, min resident blocks) -> register budget.
 int tma_popcount(int variant);
-constexpr size_t kTermSmem = 227 * 1024; // dynamic shared memory of term_tma_kernel (opt-in maximum)
+constexpr size_t kTermSmem = 226 * 1024; // dynamic shared memory of term_tma_kernel (opt-in maximum less its static part)
 size_t tma_smem_fixed(int variant, size_t nx);
 size_t tma_strip_cap(int variant, size_t nx);
 // term_tma_kernel launchers, one translation unit per block-size class
