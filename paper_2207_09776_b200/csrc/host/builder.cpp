@@ -6,7 +6,11 @@
 // consumes, and parity demands the operator VALUES be bitwise the reference's,
 // so every floating-point expression below performs the same roundings in the
 // same order as the reference routine cited beside it (compiled with
-// -ffp-contract=off, no FMA).  Data structures and control flow are our own.
+// -ffp-contract=off, no FMA).  The sparse layer (CsrBuilder, merge_rows, the
+// MagnusLogBuilder union) is structured our own way; the coefficient families,
+// assemble_*, precompute_commutators, the xoshiro256++/splitmix64 stream and the
+// path functionals necessarily follow the reference's term order and error
+// messages closely, since both are part of the bitwise / API contract.
 #include <algorithm>
 #include <cmath>
 #include <limits>
