@@ -110,6 +110,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-north-star", action="store_true", help="skip the cfg4 (512^2) sub-measurement")
+    ap.add_argument("--no-tte", action="store_true", help="skip the time-to-accuracy sub-measurement")
     ap.add_argument("--euler-steps", type=int, default=200, help="E-M steps timed beside Magnus (0 = skip)")
     ap.add_argument("--config", default=None, choices=sorted(PRESETS),
                     help="BASELINE.json workload preset (cfg2 is the default workload); explicit flags win")
@@ -464,6 +465,50 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
     return out
 
 
+def time_to_error_leg(s2b, ctx, torch, dist, local, rank):
+    """north_star's time-to-accuracy claim, measured in every default run (BASELINE configs[3] in
+    miniature): one shared Philox batch resolved at dt_leb = 1e-6 (256^2, 64 paths, T = 1), Err
+    against the closed form (exact_reference + mean_rel_error, kappa 4), wall time of each
+    synchronous solve call.  Magnus reaches the spatial floor at dt = 0.02; E-M at dt = 2e-6 is
+    still above it -- so E-M time / Magnus time is a lower bound on the speed-up at matched
+    accuracy."""
+    d, M, T, dt_leb, a, sigma = 256, 64, 1.0, 1e-6, A_LANGEVIN, SIGMA
+    g = s2b.GridSpec.square(d)
+    paths = s2b.BrownianPaths.philox(T, dt_leb, M, seed=424242, path_offset=rank * M, ctx=ctx)
+    phi = s2b.gaussian_datum(g)
+    runs = []
+
+    def timed(fn):
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        ens = fn()
+        ctx.synchronize()
+        el = max_over_ranks(time.perf_counter() - t0, dist, local)
+        e = s2b.exact_errors(ens[-1], a, sigma, paths, 4)
+        return el, e["err"]
+
+    for order in (2, 3):
+        op = s2b.Operator.from_family(g, "langevin-constant", a=a, sigma=sigma, order=order, ctx=ctx)
+        s2b.solve_iterated_magnus(s2b.MagnusConfig(order=order, dt=0.02), op, phi, paths, 0.04, g)  # warm-up
+        el, err = timed(lambda: s2b.solve_iterated_magnus(s2b.MagnusConfig(order=order, dt=0.02), op, phi, paths,
+                                                          T, g))
+        runs.append({"method": f"magnus-o{order}", "dt": 0.02, "err": err, "seconds": el})
+        del op
+    f = s2b.Fields.from_family(g, "langevin-constant", a=a, sigma=sigma, ctx=ctx)
+    for dt in (2e-6,):
+        el, err = timed(lambda: s2b.solve_euler(s2b.EulerConfig(dt=dt), f, g, phi, paths, T))
+        runs.append({"method": "euler", "dt": dt, "err": err, "seconds": el})
+    em = runs[-1]
+    out = {"config": {"grid": d, "paths_per_gpu": M, "T": T, "dt_leb": dt_leb, "seed": 424242,
+                      "error": "mean_rel_error vs exact_reference (closed form), kappa 4",
+                      "timing": "wall time of each synchronous solve call (max over ranks)"},
+           "runs": runs}
+    for r in runs[:2]:
+        if em["err"] >= r["err"]:
+            out[f"speedup_lower_bound_{r['method']}"] = em["seconds"] / r["seconds"]
+    return out
+
+
 def run_ours(args):
     rank, local, world, dist = dist_setup(args.gpus)
     import paper_2207_09776_b200 as s2b
@@ -546,6 +591,13 @@ def run_ours(args):
         except Exception as ex:
             ns = {"error": str(ex)[:300]}
 
+    tte = None
+    if args.preset == "cfg2" and not args.no_tte:
+        try:
+            tte = time_to_error_leg(s2b, ctx, torch, dist, local, rank)
+        except Exception as ex:
+            tte = {"error": str(ex)[:300]}
+
     line = {
         "metric": "magnus path*gridpoint*windows/s", "value": value,
         "unit": "path*gridpoint*windows/s", "n_gpus": world, "steps": args.steps,
@@ -573,6 +625,8 @@ def run_ours(args):
         line["euler_maruyama"] = em
     if ns is not None:
         line["north_star_512"] = ns
+    if tte is not None:
+        line["time_to_accuracy"] = tte
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             nproc = os.cpu_count() or 1
