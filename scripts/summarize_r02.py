@@ -11,7 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 for f in sorted(os.listdir(G)):
-    if f.startswith("bench_") and f.endswith(".log"):
+    if f.startswith("bench_") and f.endswith(".log") and f[6:-4] in (
+            "default", "cfg1", "cfg3", "cfg3k", "cfg4", "cfg5", "cfg5var", "cfg3o2", "cfg3ko2", "reference"):
         lines = [l for l in open(os.path.join(G, f)) if l.startswith("{")]
         if lines:
             d = json.loads(lines[-1])
@@ -26,8 +27,10 @@ if os.path.exists(src):
     for x in csv.DictReader(io.StringIO("".join(rows))):
         if x.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(x.get("Metric Unit", ""), 1.0)
-        name = x["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
+        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(
+            x.get("Metric Unit", ""), 1.0)
+        name = x["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        name = name.split("(")[0].split("<")[0].replace("void ", "").split("::")[-1].strip()
         tot[name] += float(x["Metric Value"]) * scale
         cnt[name] += 1
     all_us = sum(tot.values())
