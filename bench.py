@@ -151,6 +151,7 @@ PRESETS = {
 # when its recorded mangled kernel name equals the kernel this run launched
 PROFILE_OF = {
     ("cfg2", "langevin-constant", "cluster-xm"): "r02_xm_cfg2_ncu.json",
+    ("cfg1", "langevin-constant", "cluster-xm"): "r02_xm_cfg1_ncu.json",
     ("cfg4", "langevin-constant", "cluster-xmi"): "r02_xmi_cfg4_ncu.json",
     ("cfg3", "langevin-variable", "stream"): "r02_term_var_cfg3_ncu.json",
     ("cfg3k", "kinetic-variable", "stream"): "r02_term_varx_cfg3k_ncu.json",
