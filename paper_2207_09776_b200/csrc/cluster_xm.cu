@@ -38,9 +38,6 @@ namespace {
 #define S2B_XM_P 4
 #endif
 constexpr int kXmP = S2B_XM_P; // points in flight per thread (ILP of the stencil sums)
-#ifndef S2B_XM_INTNORM
-#define S2B_XM_INTNORM 1 // term maxima on integer bit patterns (0: fp64 compares + exponent flag)
-#endif
 #ifndef S2B_XM_NT
 #define S2B_XM_NT 256
 #endif
@@ -292,15 +289,8 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
                     double* tout = T + (cur ^ 1) * TBUF + tb;
                     double* rout = rem + (cur ^ 1) * TBUF;
                     double* sp = S + sb;
-#if S2B_XM_INTNORM
-                    // maxima of |t|, |accum| as integer maxima of the sign-cleared bit patterns:
-                    // order independent, NaN ranks above +inf (so any non-finite value is caught),
-                    // and no fp64-pipe compare in the march
-                    unsigned long long tmb = 0ull, smb = 0ull;
-#else
                     double tm = 0.0, sm = 0.0; // NaN-ignoring maxima of |t|, |accum|
                     unsigned ex = 0;           // max exponent field of accum: all-ones = non-finite
-#endif
                     // per-row register rings of RW (power of two) slots over absolute columns c:
                     // slot (c - lo) & (RW-1) is periodic in c, so the march is a loop over
                     // blocks of XB columns (the last block, which may touch the zero x-halo of
@@ -379,31 +369,21 @@ __global__ void __launch_bounds__(NT, 1) cluster_xm_kernel(ClusterBatch B) {
                                 toutb[i * TR] = tv;
                                 if (do_rem) routb[i * TR] = tv;
                                 spb[i * RPC] = sv;
-#if S2B_XM_INTNORM
-                                tmb = umax64(tmb, abs_bits(tv));
-                                smb = umax64(smb, abs_bits(sv));
-#else
                                 if (fabs(tv) > tm) tm = abs_of(tv);
                                 if (fabs(sv) > sm) sm = abs_of(sv);
                                 ex = max(ex, static_cast<unsigned>(__double2hiint(sv)) & 0x7ff00000u);
-#endif
                             }
                         }
                     };
 #pragma unroll 1
                     for (int cbase = 0; cbase < LX - XB; cbase += XB) block(cbase, std::false_type{});
                     block(LX - XB, std::true_type{});
-#if S2B_XM_INTNORM
-                    const unsigned long long wtb = warp_max_bits(tmb);
-                    const unsigned long long wsb = warp_max_bits(smb);
-#else
                     if (ex == 0x7ff00000u) sm = __longlong_as_double(0x7FF8000000000000LL); // non-finite
                     // path-wide max|t|, max|accum| (NaN-ranked): every warp pushes its maxima into
                     // a slot of every rank (lane l -> rank l, DSMEM), so no CTA barrier sits in the
                     // term loop; after the cluster barrier each warp reduces all CL x NW slots
                     const unsigned long long wtb = warp_max_bits(dbits(tm));
                     const unsigned long long wsb = warp_max_bits(dbits(sm));
-#endif
                     const int kp = gterm & 1;
                     if (lane < kXmCl) {
                         slot_dst[((kp * kXmCl + rank) * NW + warp) * 2 + 0] = wtb;

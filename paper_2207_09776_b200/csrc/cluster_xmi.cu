@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterBatch B) {
 #pragma unroll
                     for (int dv = -KRV; dv <= KRV; ++dv) rp[dv + KRV] = T + cb + ridx(r + dv, ip);
                     double* rout = op ? rem1 : rem0;
-                    // maxima of |t|, |accum| on the sign-cleared bit patterns (NaN above +inf)
-                    unsigned long long tmb = 0ull, smb = 0ull;
+                    double tm = 0.0, sm = 0.0;
+                    unsigned ex = 0;
                     // per-row register rings of RW (power of two) slots over absolute columns:
                     // slot (c - lo) & (RW-1), periodic in c, so the march can be a rolled loop
                     // over blocks of XB columns (a fully unrolled 64-point march exceeds the
@@ -366,16 +366,18 @@ __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterBatch B) {
                                 ownb[i * TRI] = tv;
                                 if (do_rem) routb[i * TRI] = tv;
                                 __stcg(sxb + i * RPC, sv);
-                                tmb = umax64(tmb, abs_bits(tv));
-                                smb = umax64(smb, abs_bits(sv));
+                                if (fabs(tv) > tm) tm = abs_of_i(tv);
+                                if (fabs(sv) > sm) sm = abs_of_i(sv);
+                                ex = max(ex, static_cast<unsigned>(__double2hiint(sv)) & 0x7ff00000u);
                             }
                         }
                     };
 #pragma unroll 1
                     for (int cbase = 0; cbase < LX - XB; cbase += XB) block(cbase, std::false_type{});
                     block(LX - XB, std::true_type{});
-                    const unsigned long long wtb = warp_max_bits_i(tmb);
-                    const unsigned long long wsb = warp_max_bits_i(smb);
+                    if (ex == 0x7ff00000u) sm = __longlong_as_double(0x7FF8000000000000LL);
+                    const unsigned long long wtb = warp_max_bits_i(static_cast<unsigned long long>(__double_as_longlong(tm)));
+                    const unsigned long long wsb = warp_max_bits_i(static_cast<unsigned long long>(__double_as_longlong(sm)));
                     if (lane == 0) {
                         red[warp][0] = wtb;
                         red[warp][1] = wsb;
