@@ -343,6 +343,81 @@ __global__ void __launch_bounds__(NT, 1) em_cluster_ip_kernel(EmXmArgs a) {
                 right[pi] = r0[LX * TRI];
             }
             __syncthreads();
+            if constexpr (XD == -1) {
+                // general fields (one value per point and field, x-major table): each point's
+                // fields are loaded ONCE per step for all NP paths of the cluster -- the
+                // per-path point loop below would re-read them from L2 for every path
+                const size_t colbase = static_cast<size_t>(x0) * NX + j;
+                double w0[NP][R0];
+                bool infs[NP];
+#pragma unroll
+                for (int pi = 0; pi < NP; ++pi) {
+                    w0[pi][0] = lft[pi];
+                    w0[pi][1] = cur0[pi];
+                    infs[pi] = false;
+                }
+#pragma unroll
+                for (int i0 = 0; i0 < LX; i0 += P) {
+                    double fl[9][P];
+#pragma unroll
+                    for (int f = 0; f < 9; ++f)
+                        if ((MASK >> f) & 1)
+#pragma unroll
+                            for (int q = 0; q < P; ++q)
+                                fl[f][q] = __ldg(a.fgen + static_cast<size_t>(f) * n + colbase + static_cast<size_t>(i0 + q) * NX);
+#pragma unroll
+                    for (int pi = 0; pi < NP; ++pi) {
+                        if (pi >= np) break;
+                        const double* rm = U + pi * TBUF + cb + ridx(r - 1, ip);
+                        const double* r0 = U + pi * TBUF + cb + 2 + r;
+                        const double* rp = U + pi * TBUF + cb + ridx(r + 1, ip);
+                        double* own = U + pi * TBUF + cb + 2 + r;
+                        double* rout = (ip ? rem0 : rem1) + pi * TBUF;
+                        double wm[P], wp[P];
+#pragma unroll
+                        for (int q = 0; q < P; ++q) {
+                            const int c = i0 + q;
+                            w0[pi][(c + 2) % R0] = c + 1 < LX ? r0[(c + 1) * TRI] : right[pi];
+                            wm[q] = rm[c * TRI];
+                            wp[q] = rp[c * TRI];
+                        }
+#pragma unroll
+                        for (int q = 0; q < P; ++q) {
+                            const int c = i0 + q;
+                            const double uc = w0[pi][(c + 1) % R0];
+                            const double uxm = w0[pi][c % R0];
+                            const double uxp = w0[pi][(c + 2) % R0];
+                            const double uvm = wm[q];
+                            const double uvp = wp[q];
+                            const double dxu = (uxp - uxm) * st0;
+                            const double dvu = (uvp - uvm) * st2;
+                            double drift = 0.0; // euler_step_into's fold (euler.cpp:51-80), see em_first
+                            if (MASK & 1) drift = EM_ADD(1, drift, fl[0][q] * uc);
+                            if (MASK & 2) drift = EM_ADD(2, drift, fl[1][q] * dxu);
+                            if (MASK & 4) drift = EM_ADD(4, drift, fl[2][q] * dvu);
+                            if (MASK & 8) {
+                                const double dxxu = (uxp - 2.0 * uc + uxm) * st1;
+                                drift = EM_ADD(8, drift, fl[3][q] * dxxu);
+                            }
+                            if (MASK & 32) {
+                                const double dvvu = (uvp - 2.0 * uc + uvm) * st3;
+                                drift = EM_ADD(32, drift, fl[5][q] * dvvu);
+                            }
+                            double noise = 0.0;
+                            if (MASK & 64) noise = EM_ADD(64, noise, fl[6][q] * uc);
+                            if (MASK & 128) noise = EM_ADD(128, noise, fl[7][q] * dxu);
+                            if (MASK & 256) noise = EM_ADD(256, noise, fl[8][q] * dvu);
+                            const double next = uc + drift * dt + noise * dW[pi];
+                            own[c * TRI] = next;
+                            if (do_rem) rout[c * TRI] = next;
+                            infs[pi] |= fabs(next) == __longlong_as_double(0x7FF0000000000000LL);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int pi = 0; pi < NP; ++pi)
+                    if (pi < np && infs[pi] && first[pi] == INT_MAX) first[pi] = k;
+            } else
 #pragma unroll
             for (int pi = 0; pi < NP; ++pi) {
                 if (pi >= np) break;
