@@ -1408,9 +1408,13 @@ void session_advance(MagnusSession* s, size_t n_windows) {
     const int stop = static_cast<int>(std::min(s->nwin, s->cur_window + n_windows));
     if (!s->external_prepare) prepare_windows(s, s->cur_window, stop);
     const double hf = s->use_cluster ? hybrid_fraction(s) : 0.0;
-    const int Ms = (hf > 0.0 && hf < 1.0 && s->M >= 64 &&
-                    cluster_batch_supported(s->op->variant, static_cast<int>(s->op->nx), static_cast<int>(s->op->nv)))
-                       ? static_cast<int>(static_cast<double>(s->M) * hf) : 0;
+    int Ms = (hf > 0.0 && hf < 1.0 && s->M >= 64 &&
+              cluster_batch_supported(s->op->variant, static_cast<int>(s->op->nx), static_cast<int>(s->op->nv)))
+                 ? static_cast<int>(static_cast<double>(s->M) * hf) : 0;
+    // a slice of fewer than 64 paths is launch-bound (one pass per Taylor term, ~300 per window,
+    // each a few microseconds of work): it would outlast the cluster kernel, so small runs stay
+    // on the cluster engine alone (an explicit S2B_HYBRID keeps any slice, for A/B runs)
+    if (Ms < 64 && !std::getenv("S2B_HYBRID")) Ms = 0;
     if (s->use_cluster && Ms > 0) {
         // hybrid: paths [0, M1) on the cluster engine (stream 1), [M1, M) on the streaming
         // engine concurrently (stream 2, on the SMs the clusters leave idle)
