@@ -100,8 +100,14 @@ constexpr VarFam kFams[] = {kFam19v, kFam19c, kFam11, kFam5, kFamK11, kFamK23};
 
 // TW: the weight rows stream through shared memory (TMA, double-buffered); otherwise (grids
 // whose two weight rows do not fit next to the ring) each point loads its weights from L2.
-template <int K, int FI, int KRX, int KRV, int XPT, bool TW>
-__global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int strips) {
+// G path groups: the CTA has G x kVarNT threads; group g handles the KT = K / G paths
+// [g*KT, (g+1)*KT) of the item at every point, so the K paths still share one copy of each
+// weight row while a thread carries only KT paths' state (G = 2: 16 warps per SM).
+template <int K, int FI, int KRX, int KRV, int XPT, bool TW, int G = 1>
+__global__ void __launch_bounds__(kVarNT * G, 1) term_var_kernel(TermArgs a, int strips) {
+    constexpr int NT = kVarNT * G;
+    constexpr int KT = K / G;
+    static_assert(K % G == 0, "paths per group");
     constexpr uint64_t MASK = kFams[FI].mask;
     using PF = Fam<kFams[FI]>;
     static_assert(2 * KRV + 2 <= kRing, "ring too short");
@@ -111,6 +117,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     const size_t n = static_cast<size_t>(nx) * nv;
     const int RWS = nx + 2 * KRX; // ring row stride (zero x-halo on both sides)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int xt = t % kVarNT, grp = t / kVarNT; // x position, path group
 
     extern __shared__ __align__(128) double vsm[];
     double* wbuf = vsm;                                          // [2][nx][NPP] weights of rows j, j+1
@@ -120,7 +127,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ unsigned long long red[K][2][kVarNT / 32];
 
-    for (int q = t; q < K * kRing * RWS; q += kVarNT) ring[q] = 0.0; // x-halos stay zero
+    for (int q = t; q < K * kRing * RWS; q += NT) ring[q] = 0.0; // x-halos stay zero
     if (TW && t == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
     // over every warp (one copy each), so no compute warp is delayed by the issue.
     auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(WSTR * 8)); };
     auto copies = [&](int jw) { // the row's weights are contiguous point-major: one bulk copy, last warp
-        if (TW && t == kVarNT - 32) {
+        if (TW && t == NT - 32) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // prior generic reads of the buffer
             tma_row(wbuf + (jw & 1) * WSTR, a.op.wpm + static_cast<size_t>(jw) * WSTR, static_cast<uint32_t>(WSTR * 8),
                     &bar[jw & 1]);
@@ -152,16 +159,17 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
         const int g = TW ? static_cast<int>(it / strips) : static_cast<int>(it - static_cast<long long>(strip) * groups);
         const int vrows = (nv + strips - 1) / strips; // rows per item (host: kVarRows, S2B_VAR_ROWS)
         const int j0 = strip * vrows, j1 = min(nv, j0 + vrows);
-        int pk[K];
-        const double* in[K];
-        const double* Sin[K];
-        double* Tout[K];
-        double* Sout[K];
-        double inv[K];
-        double c[K][6];
+        int pk[KT];
+        const double* in[KT];
+        const double* Sin[KT];
+        double* Tout[KT];
+        double* Sout[KT];
+        double inv[KT];
+        double c[KT][6];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            pk[k] = g * K + k < live ? a.act[g * K + k] : -1;
+        for (int k = 0; k < KT; ++k) {
+            const int kg = grp * KT + k; // the path's index in the item
+            pk[k] = g * K + kg < live ? a.act[g * K + kg] : -1;
             const int p = pk[k] >= 0 ? pk[k] : a.act[g * K];
             const int kk = a.k[p], par = a.par[p];
             inv[k] = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
@@ -183,11 +191,11 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
         // ring rows j0-KRV .. j0+KRV (zero outside the grid)
         for (int jr = j0 - KRV; jr <= j0 + KRV; ++jr) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                double* dst = ring + (static_cast<size_t>(k) * kRing + (jr & (kRing - 1))) * RWS + KRX;
+            for (int k = 0; k < KT; ++k) {
+                double* dst = ring + (static_cast<size_t>(grp * KT + k) * kRing + (jr & (kRing - 1))) * RWS + KRX;
 #pragma unroll
                 for (int u = 0; u < XPT; ++u) {
-                    const int i = t + u * kVarNT;
+                    const int i = xt + u * kVarNT;
                     if (i < nx)
                         dst[i] = (jr >= 0 && jr < nv && pk[k] >= 0) ? in[k][static_cast<size_t>(jr) * nx + i] : 0.0;
                 }
@@ -195,21 +203,21 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
         }
         __syncthreads();
 
-        unsigned long long tb[K], sb[K];
+        unsigned long long tb[KT], sb[KT];
 #pragma unroll
-        for (int k = 0; k < K; ++k) tb[k] = sb[k] = 0;
+        for (int k = 0; k < KT; ++k) tb[k] = sb[k] = 0;
 
         for (int j = j0; j < j1; ++j) {
             // the next row's weights (its buffer was last read in row j-1, before the barrier)
             if (TW && j + 1 < j1) copies(j + 1);
             // prefetch: the ring's next row and this row's accumulator
             const int jn = j + KRV + 1;
-            double nxt[K][XPT], sacc[K][XPT];
+            double nxt[KT][XPT], sacc[KT][XPT];
 #pragma unroll
-            for (int k = 0; k < K; ++k)
+            for (int k = 0; k < KT; ++k)
 #pragma unroll
                 for (int u = 0; u < XPT; ++u) {
-                    const int i = t + u * kVarNT;
+                    const int i = xt + u * kVarNT;
                     const bool ok = i < nx && pk[k] >= 0;
                     nxt[k][u] = (ok && jn < nv) ? in[k][static_cast<size_t>(jn) * nx + i] : 0.0;
                     sacc[k][u] = ok ? Sin[k][static_cast<size_t>(j) * nx + i] : 0.0;
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
             const double* wr = wbuf + (j & 1) * WSTR;
 #pragma unroll
             for (int u = 0; u < XPT; ++u) {
-                const int i = t + u * kVarNT;
+                const int i = xt + u * kVarNT;
                 if (i >= nx) continue;
                 const size_t r = static_cast<size_t>(j) * nx + i;
                 double wg[TW ? 1 : NP]; // the point's weights, all loads in flight at once
@@ -229,18 +237,18 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
 #pragma unroll
                     for (int q = 0; q < NP; ++q) wg[q] = __ldg(a.op.wpm + r * NPP + q);
                 }
-                double acc[K];
+                double acc[KT];
 #pragma unroll
-                for (int k = 0; k < K; ++k) acc[k] = 0.0;
+                for (int k = 0; k < KT; ++k) acc[k] = 0.0;
                 // stencil entries in ascending bit order (== ascending (dv, dx)), all compile-time
                 static_for<NB>([&](auto E) {
                     constexpr int e = decltype(E)::value;
                     constexpr int b = MaskInfo<MASK>::bit_of(e);
                     constexpr int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
                     constexpr int q0 = PF::off(e);
-                    double y[K];
+                    double y[KT];
 #pragma unroll
-                    for (int k = 0; k < K; ++k) y[k] = 0.0;
+                    for (int k = 0; k < KT; ++k) y[k] = 0.0;
                     static_for<PF::cnt(e)>([&](auto C) {
                         constexpr int q = q0 + decltype(C)::value;
                         constexpr int sl = PF::slot(q);
@@ -248,17 +256,17 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
                         if constexpr (TW) w = wr[i * NPP + q];
                         else w = wg[q];
 #pragma unroll
-                        for (int k = 0; k < K; ++k) y[k] += c[k][sl] * w;
+                        for (int k = 0; k < KT; ++k) y[k] += c[k][sl] * w;
                     });
                     const int jr = (j + dv) & (kRing - 1);
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const double x = ring[(static_cast<size_t>(k) * kRing + jr) * RWS + KRX + i + dx];
+                    for (int k = 0; k < KT; ++k) {
+                        const double x = ring[(static_cast<size_t>(grp * KT + k) * kRing + jr) * RWS + KRX + i + dx];
                         acc[k] += y[k] * x;
                     }
                 });
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
+                for (int k = 0; k < KT; ++k) {
                     if (pk[k] < 0) continue;
                     const double tv = acc[k] * inv[k];
                     const double sv = sacc[k][u] + tv;
@@ -270,11 +278,11 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
             }
             // row jn goes to slot jn & 7, which held row jn - 8, long out of the window
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                double* dst = ring + (static_cast<size_t>(k) * kRing + (jn & (kRing - 1))) * RWS + KRX;
+            for (int k = 0; k < KT; ++k) {
+                double* dst = ring + (static_cast<size_t>(grp * KT + k) * kRing + (jn & (kRing - 1))) * RWS + KRX;
 #pragma unroll
                 for (int u = 0; u < XPT; ++u) {
-                    const int i = t + u * kVarNT;
+                    const int i = xt + u * kVarNT;
                     if (i < nx) dst[i] = nxt[k][u];
                 }
             }
@@ -282,21 +290,21 @@ __global__ void __launch_bounds__(kVarNT, 1) term_var_kernel(TermArgs a, int str
             if (TW && t == 0 && j + 2 < j1) arm(j + 2);
             __syncthreads();
         }
-        // path-wide maxima: warp -> CTA -> one atomic per path
+        // path-wide maxima: warp -> group -> one atomic per path (a group's warps are contiguous)
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < KT; ++k) {
             const unsigned long long wt = warp_umax(tb[k]), ws = warp_umax(sb[k]);
             if (lane == 0) {
-                red[k][0][warp] = wt;
-                red[k][1][warp] = ws;
+                red[grp * KT + k][0][warp % (kVarNT / 32)] = wt;
+                red[grp * KT + k][1][warp % (kVarNT / 32)] = ws;
             }
         }
         __syncthreads();
-        if (warp == 0) {
+        if (warp % (kVarNT / 32) == 0) { // the first warp of each group
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                unsigned long long t2 = lane < kVarNT / 32 ? red[k][0][lane] : 0ULL;
-                unsigned long long s2 = lane < kVarNT / 32 ? red[k][1][lane] : 0ULL;
+            for (int k = 0; k < KT; ++k) {
+                unsigned long long t2 = lane < kVarNT / 32 ? red[grp * KT + k][0][lane] : 0ULL;
+                unsigned long long s2 = lane < kVarNT / 32 ? red[grp * KT + k][1][lane] : 0ULL;
                 t2 = warp_umax(t2);
                 s2 = warp_umax(s2);
                 if (lane == 0 && pk[k] >= 0) {
@@ -597,23 +605,28 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     const bool tw = nx <= kVarNT;
     const size_t smem = ((tw ? 2 * static_cast<size_t>(NP | 1) * nx : 0) +
                          static_cast<size_t>(K) * kRing * (nx + 2 * KRX)) * 8;
-    auto go = [&](auto kern) {
+    auto go = [&](auto kern, int nt) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
-        S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kVarNT, smem));
+        S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
         const size_t items = (live_max + K - 1) / K * static_cast<size_t>(strips);
         const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
         const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
-        kern<<<grid, kVarNT, smem, ctx->stream>>>(a, strips);
+        kern<<<grid, nt, smem, ctx->stream>>>(a, strips);
         ctx->k_stream = reinterpret_cast<const void*>(kern);
     };
+    // full-row TMA kernel: two path groups of 256 threads (16 warps per SM; S2B_VAR_G=1: one group)
+    const char* eg = std::getenv("S2B_VAR_G");
+    const bool g2 = K % 2 == 0 && !(eg && eg[0] == '1');
     if constexpr (NP <= 40) {
-        if (tw)
-            go(term_var_kernel<K, FI, KRX, KRV, 1, true>);
+        if (tw && g2)
+            go(term_var_kernel<K, FI, KRX, KRV, 1, true, (K % 2 == 0 ? 2 : 1)>, kVarNT * (K % 2 == 0 ? 2 : 1));
+        else if (tw)
+            go(term_var_kernel<K, FI, KRX, KRV, 1, true>, kVarNT);
         else if (nx <= 2 * kVarNT)
-            go(term_var_kernel<K, FI, KRX, KRV, 2, false>);
+            go(term_var_kernel<K, FI, KRX, KRV, 2, false>, kVarNT);
         else
-            go(term_var_kernel<K, FI, KRX, KRV, 4, false>);
+            go(term_var_kernel<K, FI, KRX, KRV, 4, false>, kVarNT);
     }
 }
 
