@@ -321,8 +321,13 @@ __global__ void __launch_bounds__(kVarNT * G, 1) term_var_kernel(TermArgs a, int
 // two CTAs per SM -- one CTA's per-row barrier and weight wait hide behind the other's math.
 // The ring (RING = 2*KRV+2 rows, slot = row mod RING) holds the part's columns plus KRX halo
 // columns on each side (the neighbour part's values, zero outside the grid).
-template <int K, int FI, int KRX, int KRV, int NT>
-__global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_kernel(TermArgs a, int strips, int gfast) {
+// G path groups as in term_var_kernel: G x NT threads, group g carries KT = K / G paths.
+template <int K, int FI, int KRX, int KRV, int NT, int G = 1>
+__global__ void __launch_bounds__(NT * G, G > 1 ? 1 : (K == 2 ? 512 / NT : 256 / NT))
+    term_varx_kernel(TermArgs a, int strips, int gfast) {
+    constexpr int NTT = NT * G; // threads per CTA
+    constexpr int KT = K / G;
+    static_assert(K % G == 0, "paths per group");
     constexpr uint64_t MASK = kFams[FI].mask;
     using PF = Fam<kFams[FI]>;
     constexpr int RING = 2 * KRV + 2;
@@ -332,7 +337,8 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     const int nx = a.op.nx, nv = a.op.nv;
     const size_t n = static_cast<size_t>(nx) * nv;
     const int parts = (nx + NT - 1) / NT;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int tt = threadIdx.x, lane = tt & 31, warp = tt >> 5;
+    const int t = tt % NT, grp = tt / NT; // column within the part, path group
 
     extern __shared__ __align__(128) double vsm[];
     constexpr int NPP = NP | 1;                       // point-major weight stride (odd: conflict-free)
@@ -341,8 +347,8 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ unsigned long long red[K][2][NT / 32];
 
-    for (int q = t; q < K * RING * RWS; q += NT) ring[q] = 0.0;
-    if (t == 0) {
+    for (int q = tt; q < K * RING * RWS; q += NTT) ring[q] = 0.0;
+    if (tt == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
     // point-major weights per row (columns past the grid are never read)
     auto arm = [&](int jw) { mbar_expect_tx(&bar[jw & 1], static_cast<uint32_t>(wpart * NPP * 8)); };
     auto copies = [&](int jw) {
-        if (t == NT - 32) {
+        if (tt == NTT - 32) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tma_row(wbuf + static_cast<size_t>(jw & 1) * NT * NPP,
                     a.op.wpm + (static_cast<size_t>(jw) * nx + xlo) * NPP, static_cast<uint32_t>(wpart * NPP * 8),
@@ -383,16 +389,17 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
         const int hi_loc = t < KRX ? t : KRX + wpart + (t - KRX);
         const bool has_h = t < 2 * KRX;
         const bool h_in = has_h && hi_col >= 0 && hi_col < nx;
-        int pk[K];
-        const double* in[K];
-        const double* Sin[K];
-        double* Tout[K];
-        double* Sout[K];
-        double inv[K];
-        double c[K][6];
+        int pk[KT];
+        const double* in[KT];
+        const double* Sin[KT];
+        double* Tout[KT];
+        double* Sout[KT];
+        double inv[KT];
+        double c[KT][6];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            pk[k] = g * K + k < live ? a.act[g * K + k] : -1;
+        for (int k = 0; k < KT; ++k) {
+            const int kg = grp * KT + k;
+            pk[k] = g * K + kg < live ? a.act[g * K + kg] : -1;
             const int p = pk[k] >= 0 ? pk[k] : a.act[g * K];
             const int kk = a.k[p], par = a.par[p];
             inv[k] = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
@@ -405,14 +412,14 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
             for (int q = 0; q < 6; ++q) c[k][q] = pk[k] >= 0 ? cp[q] : 0.0;
         }
         __syncthreads(); // the previous item is done with the ring and both weight buffers
-        if (t == 0) {
+        if (tt == 0) {
             arm(j0);
             if (j0 + 1 < j1) arm(j0 + 1);
         }
         __syncthreads(); // armed before any copy lands
         copies(j0);
         auto fill = [&](int k, int jr, double v_own, double v_h) {
-            double* dst = ring + (static_cast<size_t>(k) * RING + slot(jr)) * RWS;
+            double* dst = ring + (static_cast<size_t>(grp * KT + k) * RING + slot(jr)) * RWS;
             if (act) dst[KRX + t] = v_own;
             if (has_h) dst[hi_loc] = v_h;
             if (!act && t < NT) dst[KRX + t] = 0.0; // columns past the grid's edge
@@ -422,19 +429,19 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
         };
         for (int jr = j0 - KRV; jr <= j0 + KRV; ++jr)
 #pragma unroll
-            for (int k = 0; k < K; ++k) fill(k, jr, ldv(k, jr, i, act), ldv(k, jr, hi_col, h_in));
+            for (int k = 0; k < KT; ++k) fill(k, jr, ldv(k, jr, i, act), ldv(k, jr, hi_col, h_in));
         __syncthreads();
 
-        unsigned long long tb[K], sb[K];
+        unsigned long long tb[KT], sb[KT];
 #pragma unroll
-        for (int k = 0; k < K; ++k) tb[k] = sb[k] = 0;
+        for (int k = 0; k < KT; ++k) tb[k] = sb[k] = 0;
 
         for (int j = j0; j < j1; ++j) {
             if (j + 1 < j1) copies(j + 1);
             const int jn = j + KRV + 1;
-            double nxt[K], nxh[K], sacc[K];
+            double nxt[KT], nxh[KT], sacc[KT];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
+            for (int k = 0; k < KT; ++k) {
                 nxt[k] = ldv(k, jn, i, act);
                 nxh[k] = ldv(k, jn, hi_col, h_in);
                 sacc[k] = (act && pk[k] >= 0) ? Sin[k][static_cast<size_t>(j) * nx + i] : 0.0;
@@ -447,33 +454,33 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
             const double* wr = wbuf + static_cast<size_t>(j & 1) * NT * NPP;
             if (act) {
                 const size_t r = static_cast<size_t>(j) * nx + i;
-                double acc[K];
+                double acc[KT];
 #pragma unroll
-                for (int k = 0; k < K; ++k) acc[k] = 0.0;
+                for (int k = 0; k < KT; ++k) acc[k] = 0.0;
                 static_for<NB>([&](auto E) {
                     constexpr int e = decltype(E)::value;
                     constexpr int b = MaskInfo<MASK>::bit_of(e);
                     constexpr int dx = b % kBoxW - kBoxR, dv = b / kBoxW - kBoxR;
                     constexpr int q0 = PF::off(e);
-                    double y[K];
+                    double y[KT];
 #pragma unroll
-                    for (int k = 0; k < K; ++k) y[k] = 0.0;
+                    for (int k = 0; k < KT; ++k) y[k] = 0.0;
                     static_for<PF::cnt(e)>([&](auto C) {
                         constexpr int q = q0 + decltype(C)::value;
                         constexpr int ps = PF::slot(q);
                         const double w = wr[t * NPP + q];
 #pragma unroll
-                        for (int k = 0; k < K; ++k) y[k] += c[k][ps] * w;
+                        for (int k = 0; k < KT; ++k) y[k] += c[k][ps] * w;
                     });
                     const int rs = sl[dv + KRV];
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const double x = ring[(static_cast<size_t>(k) * RING + rs) * RWS + KRX + t + dx];
+                    for (int k = 0; k < KT; ++k) {
+                        const double x = ring[(static_cast<size_t>(grp * KT + k) * RING + rs) * RWS + KRX + t + dx];
                         acc[k] += y[k] * x;
                     }
                 });
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
+                for (int k = 0; k < KT; ++k) {
                     if (pk[k] < 0) continue;
                     const double tv = acc[k] * inv[k];
                     const double sv = sacc[k] + tv;
@@ -486,24 +493,24 @@ __global__ void __launch_bounds__(NT, K == 2 ? 512 / NT : 256 / NT) term_varx_ke
             // row jn replaces row jn - RING (= j - KRV - 1, out of this row's window): every
             // thread is past its reads of that slot only after the barrier of row j - 1
 #pragma unroll
-            for (int k = 0; k < K; ++k) fill(k, jn, nxt[k], nxh[k]);
-            if (t == 0 && j + 2 < j1) arm(j + 2); // buffer j & 1's next phase (see term_var_kernel)
+            for (int k = 0; k < KT; ++k) fill(k, jn, nxt[k], nxh[k]);
+            if (tt == 0 && j + 2 < j1) arm(j + 2); // buffer j & 1's next phase (see term_var_kernel)
             __syncthreads();
         }
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < KT; ++k) {
             const unsigned long long wt = warp_umax(tb[k]), ws = warp_umax(sb[k]);
             if (lane == 0) {
-                red[k][0][warp] = wt;
-                red[k][1][warp] = ws;
+                red[grp * KT + k][0][warp % (NT / 32)] = wt;
+                red[grp * KT + k][1][warp % (NT / 32)] = ws;
             }
         }
         __syncthreads();
-        if (warp == 0) {
+        if (warp % (NT / 32) == 0) { // the first warp of each group
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                unsigned long long t2 = lane < NT / 32 ? red[k][0][lane] : 0ULL;
-                unsigned long long s2 = lane < NT / 32 ? red[k][1][lane] : 0ULL;
+            for (int k = 0; k < KT; ++k) {
+                unsigned long long t2 = lane < NT / 32 ? red[grp * KT + k][0][lane] : 0ULL;
+                unsigned long long s2 = lane < NT / 32 ? red[grp * KT + k][1][lane] : 0ULL;
                 t2 = warp_umax(t2);
                 s2 = warp_umax(s2);
                 if (lane == 0 && pk[k] >= 0) {
@@ -568,20 +575,28 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     const bool varx = (ev ? ev[0] != '0' : nx > kVarNT) || !row_fits;
     if (varx) {
         // x-split TMA kernel, 4 paths per item, several CTAs per SM (S2B_VARX_NT: columns per CTA)
+        // G path groups per CTA (S2B_VARX_G=1: one; default two: twice the warps per SM)
+        const char* eg = std::getenv("S2B_VARX_G");
+        const bool g2 = !(eg && eg[0] == '1');
         auto run = [&](auto ntag, auto ktag) {
             constexpr int NT = decltype(ntag)::value;
             constexpr int KX = decltype(ktag)::value; // paths per item
-            auto kern = term_varx_kernel<KX, FI, KRX, KRV, NT>;
-            const size_t smem = (2 * static_cast<size_t>(NP | 1) * NT + KX * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
-            S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            int per_sm = 0;
-            S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-            const size_t parts = (nx + NT - 1) / NT;
-            const size_t items = (live_max + KX - 1) / KX * static_cast<size_t>(strips) * parts;
-            const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
-            const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
-            kern<<<grid, NT, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
-            ctx->k_stream = reinterpret_cast<const void*>(kern);
+            auto launch = [&](auto kern, int nthreads) {
+                const size_t smem = (2 * static_cast<size_t>(NP | 1) * NT + KX * static_cast<size_t>(2 * KRV + 2) * (NT + 2 * KRX)) * 8;
+                S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                int per_sm = 0;
+                S2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, smem));
+                const size_t parts = (nx + NT - 1) / NT;
+                const size_t items = (live_max + KX - 1) / KX * static_cast<size_t>(strips) * parts;
+                const size_t cap = static_cast<size_t>(std::max(1, per_sm)) * ctx->num_sms;
+                const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min(items, cap))));
+                kern<<<grid, nthreads, smem, ctx->stream>>>(a, strips, nx > 256 ? 1 : 0);
+                ctx->k_stream = reinterpret_cast<const void*>(kern);
+            };
+            if (g2 && KX % 2 == 0)
+                launch(term_varx_kernel<KX, FI, KRX, KRV, NT, (KX % 2 == 0 ? 2 : 1)>, NT * (KX % 2 == 0 ? 2 : 1));
+            else
+                launch(term_varx_kernel<KX, FI, KRX, KRV, NT>, NT);
         };
         const char* en = std::getenv("S2B_VARX_NT");
         const char* ek = std::getenv("S2B_VARX_K");
