@@ -630,9 +630,11 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
         kern<<<grid, nt, smem, ctx->stream>>>(a, strips);
         ctx->k_stream = reinterpret_cast<const void*>(kern);
     };
-    // full-row TMA kernel: two path groups of 256 threads (16 warps per SM; S2B_VAR_G=1: one group)
+    // full-row TMA kernel: one group of 256 threads; S2B_VAR_G=2 runs two path groups (16 warps
+    // per SM, 128 registers) -- measured 7% slower at cfg3 order 3 (each weight load then serves
+    // 2 paths instead of 4), so it stays opt-in
     const char* eg = std::getenv("S2B_VAR_G");
-    const bool g2 = K % 2 == 0 && !(eg && eg[0] == '1');
+    const bool g2 = K % 2 == 0 && eg && eg[0] == '2';
     if constexpr (NP <= 40) {
         if (tw && g2)
             go(term_var_kernel<K, FI, KRX, KRV, 1, true, (K % 2 == 0 ? 2 : 1)>, kVarNT * (K % 2 == 0 ? 2 : 1));
