@@ -575,9 +575,10 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     const bool varx = (ev ? ev[0] != '0' : nx > kVarNT) || !row_fits;
     if (varx) {
         // x-split TMA kernel, 4 paths per item, several CTAs per SM (S2B_VARX_NT: columns per CTA)
-        // G path groups per CTA (S2B_VARX_G=1: one; default two: twice the warps per SM)
+        // G path groups per CTA: S2B_VARX_G=2 doubles the warps per SM; measured equal at cfg3k
+        // and 14% slower at 1024^2 (cfg5 variable), so one group is the default
         const char* eg = std::getenv("S2B_VARX_G");
-        const bool g2 = !(eg && eg[0] == '1');
+        const bool g2 = eg && eg[0] == '2';
         auto run = [&](auto ntag, auto ktag) {
             constexpr int NT = decltype(ntag)::value;
             constexpr int KX = decltype(ktag)::value; // paths per item
