@@ -11,6 +11,10 @@
 //  * the fold has no zero-coefficient branch: with finite weights, adding c*w = +-0 to a
 //    y that started at +0.0 changes no bit (a sum is -0 only if both addends are), which is
 //    the reference's skip; the operator must have finite weights (checked at upload);
+//  * the fold starts at its first product instead of 0.0 + it (one DADD fewer per stencil
+//    entry and path: 19 of 118 fp64 ops at order 3): y can then differ from the reference's
+//    only in the sign of a zero, and the apply's accumulator starts at +0.0, so it absorbs a
+//    +-0 product without a bit changing (x + -0 == x for x != 0, +0 + -0 == +0);
 //  * a work item is (K live paths, strip of kRows output rows); the K paths share every weight
 //    load (the weights are the same for all paths) and the CTA marches down the strip with
 //    the term rows j-KRV .. j+KRV of all K paths in a ring (zero x-halo columns, zero rows
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(kVarNT * G, 1) term_var_kernel(TermArgs a, int
                         if constexpr (TW) w = wr[i * NPP + q];
                         else w = wg[q];
 #pragma unroll
-                        for (int k = 0; k < KT; ++k) y[k] += c[k][sl] * w;
+                        for (int k = 0; k < KT; ++k) y[k] = decltype(C)::value == 0 ? c[k][sl] * w : y[k] + c[k][sl] * w;
                     });
                     const int jr = (j + dv) & (kRing - 1);
 #pragma unroll
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(NT * G, G > 1 ? 1 : (K == 2 ? 512 / NT : 256 /
                         constexpr int ps = PF::slot(q);
                         const double w = wr[t * NPP + q];
 #pragma unroll
-                        for (int k = 0; k < KT; ++k) y[k] += c[k][ps] * w;
+                        for (int k = 0; k < KT; ++k) y[k] = decltype(C)::value == 0 ? c[k][ps] * w : y[k] + c[k][ps] * w;
                     });
                     const int rs = sl[dv + KRV];
 #pragma unroll
