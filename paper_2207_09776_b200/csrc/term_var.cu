@@ -565,7 +565,9 @@ void launch_var_k(s2b_context* ctx, const TermArgs& a, size_t live_max) {
     constexpr int NP = Fam<kFams[FI]>::off(MaskInfo<kFams[FI].mask>::count());
     const int nx = a.op.nx, nv = a.op.nv;
     const char* er = std::getenv("S2B_VAR_ROWS");
-    int vr = er ? std::max(4, std::atoi(er)) : kVarRows;
+    // up to 256 columns one item covers the whole grid height (cfg3: 2.82e8 vs 2.74e8 windows/s
+    // with 128-row strips; the ring prologue and the two-row weight prefetch are paid once)
+    int vr = er ? std::max(4, std::atoi(er)) : (nx <= 256 ? 256 : kVarRows);
     if (!er) // few paths: shorter items keep every SM busy
         while (vr > 16 && (live_max + K - 1) / K * static_cast<size_t>((nv + vr - 1) / vr) *
                                   static_cast<size_t>((nx + 127) / 128) < 4 * static_cast<size_t>(ctx->num_sms))

@@ -43,6 +43,23 @@ def test_engines_bitwise_256(ref, s2b, ctx, engine, order):
     assert stats["path_terms"] > 0
 
 
+@pytest.mark.parametrize("engine", ["xm"], indirect=True)
+@pytest.mark.parametrize("d", [64, 128, 256])
+@pytest.mark.parametrize("tol", [1e-4, 1e-8, 1e-13, 0.3])
+def test_xm_stopping_rule_tolerances(ref, s2b, ctx, engine, d, tol):
+    """The x-march kernel's stopping rule (path-wide maxima through DSMEM slots, one cluster
+    barrier per term) against the reference's decisions at loose, default-like, tight and
+    > 0.1 tolerances, bitwise."""
+    T, dt, dt_leb, M, seed = 0.02, 0.01, 1e-3, 3, 71
+    _, values, want, wst = _ref_run(ref, d, 3, T, dt, dt_leb, M, seed, rec=[0.01], tol=tol)
+    ens, _, _, stats = gpu_magnus(s2b, ctx, "langevin-constant", d, 3, values, dt_leb, T, dt,
+                                  rec=[0.01], seed=seed, expmv_tol=tol)
+    for r, e in enumerate(ens):
+        assert np.array_equal(e.status, wst[r])
+        assert np.array_equal(e.states(), want[r], equal_nan=True)
+    assert stats["engine"] == 2
+
+
 @pytest.mark.parametrize("engine", ["xm", "band"], indirect=True)
 def test_engines_blowup_exits_256(ref, s2b, ctx, engine):
     d, T, dt, dt_leb, M = 256, 0.02, 0.01, 1e-3, 2
