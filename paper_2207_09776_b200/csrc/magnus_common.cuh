@@ -21,8 +21,12 @@ __device__ __forceinline__ int xclass(int i, int nx) {
     return i == 0 ? 0 : (i == 1 ? 1 : (i == nx - 2 ? 3 : (i == nx - 1 ? 4 : 2)));
 }
 
+// |v| as bits, cleared on the high word (one integer LOP3: the 64-bit mask form is otherwise
+// recognised as fabs and issued as a DADD on the fp64 pipe)
 __device__ __forceinline__ unsigned long long abs_bits(double v) {
-    return static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFFFFFULL;
+    const unsigned hi = static_cast<unsigned>(__double2hiint(v)) & 0x7fffffffu;
+    const unsigned lo = static_cast<unsigned>(__double2loint(v));
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 constexpr unsigned long long kInfBits = 0x7FF0000000000000ULL;
 
@@ -63,6 +67,7 @@ struct TermArgs {
     unsigned long long* sn;
     int nstrips;
     int strip_rows; // output rows per work item of term_tma_kernel (kStripRows; S2B_STRIP overrides)
+    int sync2;      // term_tma_kernel: one CTA barrier per two ring steps (S2B_TMA_SYNC=1: every step)
     int8_t e2bit[kBoxBits];
     // entry-major weights of the kernel's mask: wt[(j * NYE + q) * kPairSlots + k] is the
     // k-th source weight (slot order) of Y entry q = cls * NBM + e at row j, zero-padded;
