@@ -970,6 +970,11 @@ TermArgs term_args(MagnusSession& s) {
         }
     }
     a.nstrips = static_cast<int>((s.op->nv + a.strip_rows - 1) / a.strip_rows);
+    {
+        const char* e = std::getenv("S2B_TMA_SYNC");
+        const int g = e ? std::atoi(e) : 2;
+        a.sync_g = g == 1 || g == 4 ? g : 2;
+    }
     a.wt = s.op->d_wt.p;
     a.eslot = s.op->d_eslot.p;
     const uint64_t mask = kVariants[s.op->variant].mask;

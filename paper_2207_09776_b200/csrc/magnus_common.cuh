@@ -67,7 +67,7 @@ struct TermArgs {
     unsigned long long* sn;
     int nstrips;
     int strip_rows; // output rows per work item of term_tma_kernel (kStripRows; S2B_STRIP overrides)
-    int sync2;      // term_tma_kernel: one CTA barrier per two ring steps (S2B_TMA_SYNC=1: every step)
+    int sync_g;     // term_tma_kernel: one CTA barrier per sync_g ring steps (1, 2, 4; S2B_TMA_SYNC)
     int8_t e2bit[kBoxBits];
     // entry-major weights of the kernel's mask: wt[(j * NYE + q) * kPairSlots + k] is the
     // k-th source weight (slot order) of Y entry q = cls * NBM + e at row j, zero-padded;

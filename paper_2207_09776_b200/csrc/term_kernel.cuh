@@ -120,9 +120,14 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
             }
         };
 
+        // ring refill with one CTA barrier per G = sync_g steps: a step s = 0 mod G refills the G
+        // slots that steps s-G .. s-1 read, all released by the barrier after step s-1, with rows
+        // s+8-G .. s+7 (8-G .. 7 rows ahead).  G = 1 is the classic one-barrier-per-row ring.
+        const int G = a.sync_g;
+        const int ahead = kStages - G;
         __syncthreads(); // previous item fully consumed the ring and the Y rows
         if (t == 0) {
-            for (int s = 0; s < kStages - 1 && s < nsteps; ++s) issue(s);
+            for (int s = 0; s < ahead && s < nsteps; ++s) issue(s);
         }
         if (t < 6) c[t] = a.ctab[(static_cast<size_t>(p) * a.nwin + a.win[p]) * 6 + t];
         __syncthreads();
@@ -147,7 +152,10 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
             for (int ph = 0; ph < WROWS; ++ph) {
                 const int s = base + ph;
                 if (s < nsteps) {
-                    if (t == 0 && s + kStages - 1 < nsteps) issue(s + kStages - 1);
+                    if (t == 0 && (s & (G - 1)) == 0) {
+                        for (int q = ahead; q < kStages; ++q)
+                            if (s + q < nsteps) issue(s + q);
+                    }
                     const uint32_t g = gstep + s;
                     const uint32_t slot = g & (kStages - 1);
                     mbar_wait_u(full_u + 8 * slot, (g / kStages) & 1);
@@ -222,7 +230,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) term_tma_kernel(TermArgs a) {
                         tb = umax64(tb, umax64(abs_bits(tA), abs_bits(tB)));
                         sb = umax64(sb, umax64(abs_bits(sA), abs_bits(sB)));
                     }
-                    __syncthreads(); // ring slot consumed by every thread
+                    if ((s & (G - 1)) == G - 1) __syncthreads(); // ring slots consumed by every thread
                 }
             }
         }
