@@ -92,7 +92,7 @@ __device__ __forceinline__ void cluster_barrier_i() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P, int CL>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, int NX, int RPC, int NT, int P, int CL, bool NZ>
 __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterBatch B) {
     using L = XiLayout<MASK, KRX, KRV, BM, NX, RPC>;
     using RE = RowExtI<MASK>;
@@ -353,7 +353,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterBatch B) {
                                                 }
                                             }
                                             const int col = g + q + dx;
-                                            acc[q] += wv * win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))];
+                                            const double pr = wv * win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))];
+                                            // NZ (datum without -0.0): start at the first product, as
+                                            // cluster_xm (DESIGN "Parity")
+                                            acc[q] = (NZ && e == 0) ? pr : acc[q] + pr;
                                         }
                                     }
                                 }
@@ -446,10 +449,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_xmi_kernel(ClusterBatch B) {
 #undef XI_ROFF
 }
 
-template <int V, int NX, int RPC>
+template <int V, int NX, int RPC, bool NZ>
 void launch_xmi(s2b_context* ctx, const ClusterBatch& a) {
     constexpr Variant v = kVariants[V];
-    auto kern = cluster_xmi_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, kXiNT, kXiP, kXiCl>;
+    auto kern = cluster_xmi_kernel<v.rx, v.rv, v.mask, v.bm, NX, RPC, kXiNT, kXiP, kXiCl, NZ>;
     const size_t smem = XiLayout<v.mask, v.rx, v.rv, v.bm, NX, RPC>::bytes();
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -492,10 +495,17 @@ size_t cluster_xmi_scratch(int nx, int nv, int* slots) {
 }
 
 void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterBatch& a) {
-    switch (variant) {
-    case 7: launch_xmi<7, 512, 32>(ctx, a); break;
-    case 8: launch_xmi<8, 512, 32>(ctx, a); break;
-    case 9: launch_xmi<9, 512, 32>(ctx, a); break;
+    bool nz = true;
+    for (int i = 0; i < a.n; ++i) nz = nz && a.a[i].nz;
+    const char* e = std::getenv("S2B_XMI_NZ"); // 0: the literal 0.0 + first product (A/B)
+    if (e && e[0] == '0') nz = false;
+    switch (variant * 2 + (nz ? 1 : 0)) {
+    case 14: launch_xmi<7, 512, 32, false>(ctx, a); break;
+    case 15: launch_xmi<7, 512, 32, true>(ctx, a); break;
+    case 16: launch_xmi<8, 512, 32, false>(ctx, a); break;
+    case 17: launch_xmi<8, 512, 32, true>(ctx, a); break;
+    case 18: launch_xmi<9, 512, 32, false>(ctx, a); break;
+    case 19: launch_xmi<9, 512, 32, true>(ctx, a); break;
     default: fail(S2B_ERR_RUNTIME, "in-place cluster engine: unsupported variant");
     }
     S2B_LAUNCHED(ctx);
