@@ -160,6 +160,9 @@ PROFILE_OF = {
     ("hybrid", 256): "r02_term_tma_hybrid256_ncu.json",
     ("hybrid", 512): "r02_term_tma_hybrid512_ncu.json",
 }
+# E-M captures (scripts/prof_r02.sh em_*): per (preset, kernel) of the bench's E-M leg
+EM_PROFILE_OF = {("cfg2", "em_cluster_ip_kernel"): "r02_em_cluster_ip_cfg2_ncu.json",
+                 ("cfg5", "em_tb_kernel"): "r02_em_tb_cfg5_ncu.json"}
 
 
 def peaks():
@@ -433,10 +436,13 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
     # the on-chip engines are bound by the fp64 pipe, not HBM: report that ceiling beside it
     # (DMUL + DADD per stencil point, no FMA for bitwise parity; +1 DMUL, +1 DADD per point)
     ops_pt = 2 * stencil_points(a.order) + 2
-    if a.family == "langevin-variable":  # + the per-term fold of Y from the source pairs
-        ops_pt += 2 * {1: 7, 2: 15, 3: 39}[a.order]
+    # + the per-term fold of Y from the source pairs: a DMUL per pair and a DADD per pair after
+    # the first of each stencil entry (the fold starts at its first product; term_var.cu)
+    if a.family == "langevin-variable":
+        ops_pt += 2 * {1: 7, 2: 15, 3: 39}[a.order] - stencil_points(a.order)
     elif a.family == "kinetic-variable":
-        ops_pt = 2 * {2: 11, 3: 23}.get(a.order, 5) + 2 + 2 * {2: 24, 3: 64}.get(a.order, 7)
+        npt = {2: 11, 3: 23}.get(a.order, 5)
+        ops_pt = 2 * npt + 2 + 2 * {2: 24, 3: 64}.get(a.order, 7) - npt
     fp64_ops = n * terms * float(ops_pt)
     fp64_peak = fp64_peak_tops()
     compute = {"bound": "fp64", "achieved": fp64_ops / (tk_ms / 1e3) / 1e12 if tk_ms > 0 else 0.0,
@@ -668,17 +674,25 @@ def euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, worl
     del ens
     rate = world * M * n * steps / (ms / 1e3)
     peak, _ = peaks()
+    launched = ctx.kernel_names()["em"]  # mangled name of the step kernel that ran
+    kname = next((k for k in ("em_cluster_ip_kernel", "em_cluster_kernel", "em_tb_kernel", "em_rows_kernel",
+                              "em_step_kernel") if k in launched), launched)
+    roof = {"bound": "hbm", "achieved": 16.0 * rate / world / 1e9, "peak": peak,
+            "unit": "GB/s", "frac": 16.0 * rate / world / 1e9 / peak, "kernel": kname, "kernel_mangled": launched,
+            "note": "whole solve_euler call incl. state init; 16 B/pt/step streaming-equivalent "
+                    "(the cluster kernel keeps the state on chip for all steps)"}
+    pname = EM_PROFILE_OF.get((args.preset, kname))
+    if pname:
+        prof = load_profile(pname)
+        roof["traffic_source"] = f"profiles/{pname} (ncu dram__bytes per path*step)"
+        roof["stale_profile"] = prof.get("kernel_mangled") != launched
+        if not roof["stale_profile"]:
+            roof["traffic_per_path_step"] = prof.get("dram_bytes_per_path_step")
+            roof["traffic_over_algorithmic"] = prof.get("traffic_over_algorithmic")
+            roof["ncu_fp64_pipe_pct_of_active"] = prof.get("fp64_pipe_pct_of_active")
+            roof["profile_same_binary"] = prof.get("lib_sha256") == lib_sha256()
     return {"metric": "euler path*gridpoint*steps/s", "value": rate, "steps": steps,
-            "dt": args.dt_leb, "ms": ms, "blown": blown,
-            "roofline": {"bound": "hbm", "achieved": 16.0 * rate / world / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": 16.0 * rate / world / 1e9 / peak,
-                         "kernel": ("em_tb_kernel" if os.environ.get("S2B_EMXM", "1") == "0" or args.d not in (64, 128, 256, 512)
-                                    or (args.family == "kinetic-variable" and args.d == 256
-                                        and os.environ.get("S2B_EM2", "1") == "0")
-                                    else "em_cluster_kernel" if args.d == 256 and os.environ.get("S2B_EM2", "1") == "0"
-                                    else "em_cluster_ip_kernel"),
-                         "note": "whole solve_euler call incl. state init; 16 B/pt/step streaming-equivalent "
-                                 "(the cluster kernel keeps the state on chip for all steps)"}}
+            "dt": args.dt_leb, "ms": ms, "blown": blown, "roofline": roof}
 
 
 def main():

@@ -139,6 +139,9 @@ int64_t s2b_context_launches(s2b_context *ctx);
  * the cluster-resident engine's and the streaming pass engine's ("" if none), each copied
  * into a caller buffer of `len` bytes.  bench.py matches them against the ncu captures. */
 int s2b_context_kernel_names(s2b_context *ctx, char *cluster, char *stream, size_t len);
+/* Mangled name of the Euler-Maruyama step kernel this context launched last (em_cluster_ip,
+ * em_tb, em_rows or em_step; "" if none), for bench.py's E-M capture check. */
+int s2b_context_em_kernel_name(s2b_context *ctx, char *out, size_t len);
 
 /* ---- operators ----------------------------------------------------------------
  * sources: B, A, A2, BA, BAA, BAB (the CommutatorSet slot order of magnus.cpp:42-52).

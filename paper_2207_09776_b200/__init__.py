@@ -95,10 +95,13 @@ class Context:
         return int(lib().s2b_context_launches(self.h))
 
     def kernel_names(self):
-        """Mangled names of the dominant Magnus kernels this context launched last."""
+        """Mangled names of the dominant Magnus kernels and of the E-M step kernel this context
+        launched last."""
         a, b = C.create_string_buffer(4096), C.create_string_buffer(4096)
         _check(lib().s2b_context_kernel_names(self.h, a, b, 4096))
-        return {"cluster": a.value.decode(), "stream": b.value.decode()}
+        e = C.create_string_buffer(4096)
+        _check(lib().s2b_context_em_kernel_name(self.h, e, 4096))
+        return {"cluster": a.value.decode(), "stream": b.value.decode(), "em": e.value.decode()}
 
     def close(self):
         if getattr(self, "h", None):

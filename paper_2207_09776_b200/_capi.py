@@ -140,6 +140,7 @@ SIGNATURES = {
     "s2b_expmv": (C.c_int, [_VP, _P(Csr), _P(C.c_double), C.c_double, C.c_double,
                             _P(C.c_double), _P(C.c_int)]),
     "s2b_context_kernel_names": (C.c_int, [_VP, C.c_char_p, C.c_char_p, C.c_size_t]),
+    "s2b_context_em_kernel_name": (C.c_int, [_VP, C.c_char_p, C.c_size_t]),
     "s2b_host_ops_assemble_device": (C.c_int, [_VP, _P(Grid), C.c_int, C.c_double, C.c_double,
                                                _P(_P(C.c_double)), C.c_int, _P(_VP)]),
     "s2b_operator_build_device": (C.c_int, [_VP, _P(Grid), C.c_int, C.c_double, C.c_double,

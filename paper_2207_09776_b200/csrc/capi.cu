@@ -710,6 +710,17 @@ int s2b_context_kernel_names(s2b_context* ctx, char* cluster, char* stream, size
     });
 }
 
+int s2b_context_em_kernel_name(s2b_context* ctx, char* out, size_t len) {
+    return guard([&] {
+        need(ctx, "ctx");
+        if (!out || len == 0) return;
+        const char* name = "";
+        if (ctx->k_em) S2B_CUDA(cudaFuncGetName(&name, ctx->k_em));
+        std::strncpy(out, name, len - 1);
+        out[len - 1] = 0;
+    });
+}
+
 int s2b_expmv_workspace_create(s2b_context* ctx, s2b_expmv_workspace** out) {
     return guard([&] {
         need(ctx, "ctx");

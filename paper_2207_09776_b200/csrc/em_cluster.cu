@@ -524,6 +524,7 @@ void launch_em_ip(s2b_context* ctx, const EmXmArgs& a) {
     clusters = grid_cap(std::max(1, std::min(clusters, a.M)));
     cfg.gridDim = dim3(CL * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    ctx->k_em = reinterpret_cast<const void*>(kern);
 }
 
 template <int MASK, bool NZ>
@@ -549,6 +550,7 @@ void launch_em(s2b_context* ctx, const EmXmArgs& a) {
     clusters = grid_cap(std::max(1, std::min(clusters, a.M)));
     cfg.gridDim = dim3(kEmCl * clusters);
     S2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    ctx->k_em = reinterpret_cast<const void*>(kern);
 }
 
 __global__ void em_cluster_status_kernel(const int* blow, const int* rec_k, int R, uint8_t* status, int M) {

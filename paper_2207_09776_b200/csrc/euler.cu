@@ -576,14 +576,19 @@ s2b_ensemble* solve_euler(s2b_context* ctx, const s2b_fields* f, const s2b_euler
             a.in = U[cur].p;
             a.out = U[cur ^ 1].p;
             dim3 grid(gx, static_cast<unsigned>(std::min<size_t>(M, 65535)));
-            if (two)
+            if (two) {
                 tb_fn<<<tb_grid, nt, tb_smem, ctx->stream>>>(a, tb_strips, tb_items);
-            else if (rows)
+                ctx->k_em = reinterpret_cast<const void*>(tb_fn);
+            } else if (rows) {
                 rows_fn<<<rows_grid, nt, 0, ctx->stream>>>(a, kR, strips, items);
-            else if (f->mask & 16)
+                ctx->k_em = reinterpret_cast<const void*>(rows_fn);
+            } else if (f->mask & 16) {
                 em_step_kernel<true><<<grid, 256, 0, ctx->stream>>>(a);
-            else
+                ctx->k_em = reinterpret_cast<const void*>(em_step_kernel<true>);
+            } else {
                 em_step_kernel<false><<<grid, 256, 0, ctx->stream>>>(a);
+                ctx->k_em = reinterpret_cast<const void*>(em_step_kernel<false>);
+            }
             S2B_LAUNCHED(ctx);
             cur ^= 1;
             k += two ? 2 : 1;

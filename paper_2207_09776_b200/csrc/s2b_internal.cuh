@@ -71,6 +71,7 @@ struct s2b_context {
     // bench.py matches against the ncu captures in profiles/)
     const void* k_cluster = nullptr;
     const void* k_stream = nullptr;
+    const void* k_em = nullptr; // the E-M step kernel launched last (s2b_context_em_kernel_name)
 };
 
 namespace s2b {

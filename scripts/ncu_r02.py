@@ -46,7 +46,7 @@ def main():
         roof = line["roofline"]
         paths = line["config"]["paths_per_gpu"]
         n = line["config"]["grid"] ** 2
-        spk = line["path_terms_per_window"]
+        spk = line.get("path_terms_per_window")
         hyb = roof.get("hybrid_paths") or 0
         traffic = f("dram__bytes_read.sum") + f("dram__bytes_write.sum")
         dur = f("gpu__time_duration.sum")
@@ -99,7 +99,14 @@ def main():
             "opcode_mix_pct": {k: round(v / tot * 100, 2) for k, v in mix.most_common(14)},
             "bench_line": {"config": line["config"]["workload"], "path_terms_per_window": spk, "hybrid_paths": hyb},
         }
-        if stream:
+        if name.startswith("em_"):
+            # E-M: the cluster kernel runs every step of the timed solve in its launch, em_tb two
+            steps = 2 if "em_tb" in s["kernel"] else line["euler_maruyama"]["steps"]
+            s["em_steps_in_launch"] = steps
+            s["dram_bytes_per_path_step"] = traffic / (paths * steps)
+            s["algorithmic_bytes"] = 16.0 * n * paths * steps
+            s["traffic_over_algorithmic"] = traffic / s["algorithmic_bytes"]
+        elif stream:
             s["live_paths_in_pass"] = live
             s["dram_bytes_per_path_term"] = traffic / live
             s["algorithmic_bytes"] = 32.0 * n * live

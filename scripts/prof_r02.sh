@@ -14,7 +14,10 @@ CMD[var_cfg3]="$B --config cfg3 --paths 1184 --T 0.02";         KERN[var_cfg3]="
 CMD[varx_cfg3k]="$B --config cfg3k --paths 1184 --T 0.02";      KERN[varx_cfg3k]="term_varx_kernel"; SKIP[varx_cfg3k]=40
 CMD[tma_cfg5]="$B --config cfg5 --paths 296 --T 0.001";         KERN[tma_cfg5]="term_tma_kernel"; SKIP[tma_cfg5]=40
 CMD[varx_cfg5var]="$B --config cfg5 --family langevin-variable --paths 296 --T 0.001"; KERN[varx_cfg5var]="term_varx_kernel"; SKIP[varx_cfg5var]=40
-NAMES=${@:-xm_cfg2 xm_cfg1 tma_hybrid256 xmi_cfg4 tma_hybrid512 var_cfg3 varx_cfg3k tma_cfg5 varx_cfg5var}
+# E-M: the timed solve_euler of the bench's E-M leg (the warm-up solve is launch 0)
+CMD[em_cfg2]="$B --paths 288 --euler-steps 40";                 KERN[em_cfg2]="em_cluster_ip_kernel"; SKIP[em_cfg2]=1
+CMD[em_cfg5]="$B --config cfg5 --paths 296 --T 0.001 --euler-steps 20"; KERN[em_cfg5]="em_tb_kernel"; SKIP[em_cfg5]=6
+NAMES=${@:-xm_cfg2 xm_cfg1 tma_hybrid256 xmi_cfg4 tma_hybrid512 var_cfg3 varx_cfg3k tma_cfg5 varx_cfg5var em_cfg2 em_cfg5}
 for nm in $NAMES; do
   ${CMD[$nm]} > gpurun_out/plain_$nm.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:${KERN[$nm]} -s ${SKIP[$nm]} -c 1 \
