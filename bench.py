@@ -335,6 +335,25 @@ def run_reference(args):
     return 0
 
 
+def sass_sha256(mangled):
+    """sha256 of one kernel's SASS instructions in the shipped library (cuobjdump -sass -fun):
+    the capture-vs-run check that survives rebuilds (-lineinfo embeds source mtimes, so the
+    .so bytes change on every rebuild while the machine code does not)."""
+    import hashlib
+    import re
+    import subprocess
+    if not mangled:
+        return None
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", "-fun", mangled,
+                              os.path.join(ROOT, "paper_2207_09776_b200", "lib", "libspde2d_b200.so")],
+                             capture_output=True, text=True, timeout=120).stdout
+    except Exception:
+        return None
+    ins = [ln.split(";")[0].strip() for ln in out.splitlines() if re.match(r"\s+/\*[0-9a-f]{4,}\*/", ln)]
+    return hashlib.sha256("\n".join(ins).encode()).hexdigest() if ins else None
+
+
 def lib_sha256():
     import hashlib
     try:
@@ -459,6 +478,8 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
                               + (" + the streaming-engine capture of the hybrid slice" if hyb else ""),
             "stale_profile": bool(stale or stream_stale),
             "profile_same_binary": (not stale) and prof.get("lib_sha256") == lib_sha256(),
+            "profile_same_sass": (not stale) and prof.get("sass_sha256") is not None
+                                 and prof.get("sass_sha256") == sass_sha256(launched),
             "hybrid_paths": hyb, "note": engine["note"]}
     if stale:
         roof["profile_kernel"] = prof.get("kernel_mangled") or prof.get("kernel")
@@ -691,6 +712,7 @@ def euler_leg(args, s2b, ctx, grid, phi, paths, stream, torch, dist, local, worl
             roof["traffic_over_algorithmic"] = prof.get("traffic_over_algorithmic")
             roof["ncu_fp64_pipe_pct_of_active"] = prof.get("fp64_pipe_pct_of_active")
             roof["profile_same_binary"] = prof.get("lib_sha256") == lib_sha256()
+            roof["profile_same_sass"] = prof.get("sass_sha256") is not None and prof.get("sass_sha256") == sass_sha256(launched)
     return {"metric": "euler path*gridpoint*steps/s", "value": rate, "steps": steps,
             "dt": args.dt_leb, "ms": ms, "blown": blown, "roofline": roof}
 

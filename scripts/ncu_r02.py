@@ -71,10 +71,13 @@ def main():
             pass
         tot = sum(mix.values()) or 1.0
         lib = os.path.join("paper_2207_09776_b200", "lib", "libspde2d_b200.so")
+        sys.path.insert(0, os.getcwd())
+        from bench import sass_sha256
         s = {
             "kernel": d["Kernel Name"][0],
             "lib_sha256": hashlib.sha256(open(lib, "rb").read()).hexdigest(),
             "kernel_mangled": dm["Kernel Name"][0],
+            "sass_sha256": sass_sha256(dm["Kernel Name"][0]),
             "capture": f"ncu --set full --clock-control none --import-source on, one launch; scripts/prof_r02.sh {name}",
             "duration_ms": dur * 1e3,
             "dram_bytes_read": f("dram__bytes_read.sum"),
