@@ -7,9 +7,10 @@ B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --euler-steps
 declare -A CMD KERN SKIP
 CMD[xm_cfg2]="$B --paths 288";                                  KERN[xm_cfg2]="cluster_xm_kernel"; SKIP[xm_cfg2]=1
 CMD[xm_cfg1]="$B --config cfg1 --paths 296";                   KERN[xm_cfg1]="cluster_xm_kernel"; SKIP[xm_cfg1]=1
-CMD[tma_hybrid256]="$B --paths 288";                            KERN[tma_hybrid256]="term_tma_kernel"; SKIP[tma_hybrid256]=40
+# the hybrid slice is only split off from 64 paths up: 600 paths -> 72 streaming paths at 256^2
+CMD[tma_hybrid256]="$B --paths 600";                            KERN[tma_hybrid256]="term_tma_kernel"; SKIP[tma_hybrid256]=40
 CMD[xmi_cfg4]="$B --config cfg4 --paths 112 --T 0.01";          KERN[xmi_cfg4]="cluster_xmi_kernel"; SKIP[xmi_cfg4]=1
-CMD[tma_hybrid512]="$B --config cfg4 --paths 140 --T 0.01";     KERN[tma_hybrid512]="term_tma_kernel"; SKIP[tma_hybrid512]=40
+CMD[tma_hybrid512]="$B --config cfg4 --paths 560 --T 0.01";     KERN[tma_hybrid512]="term_tma_kernel"; SKIP[tma_hybrid512]=40
 CMD[var_cfg3]="$B --config cfg3 --paths 1184 --T 0.02";         KERN[var_cfg3]="term_var_kernel"; SKIP[var_cfg3]=40
 CMD[varx_cfg3k]="$B --config cfg3k --paths 1184 --T 0.02";      KERN[varx_cfg3k]="term_varx_kernel"; SKIP[varx_cfg3k]=40
 CMD[tma_cfg5]="$B --config cfg5 --paths 296 --T 0.001";         KERN[tma_cfg5]="term_tma_kernel"; SKIP[tma_cfg5]=40
