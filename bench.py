@@ -38,7 +38,8 @@ ENGINES = {
                 "streaming-equivalent rate, traffic the real DRAM bytes; bound by the fp64 pipe; by default "
                 "20% of the paths run on the streaming engine on the idle SMs (S2B_HYBRID)"},
     0: {"name": "stream", "kernel": "term_tma_kernel", "profile": "term_kernel_ncu.json",
-        "note": "streaming pass engine: term and accumulator round-trip HBM every Taylor term"},
+        "note": "streaming pass engine: term and accumulator round-trip HBM every Taylor term (constant "
+                "Langevin on grids >= 256 columns: the x-march term_xs_kernel, x-major tiles by TMA)"},
     1: {"name": "cluster-band", "kernel": "cluster_magnus_kernel", "profile": "cluster_kernel_ncu.json",
         "note": "cluster-resident: the path stays in shared memory for the window; achieved is the "
                 "streaming-equivalent rate (can exceed HBM peak), traffic the real DRAM bytes"},
@@ -155,7 +156,7 @@ PROFILE_OF = {
     ("cfg4", "langevin-constant", "cluster-xmi"): "r02_xmi_cfg4_ncu.json",
     ("cfg3", "langevin-variable", "stream"): "r02_term_var_cfg3_ncu.json",
     ("cfg3k", "kinetic-variable", "stream"): "r02_term_varx_cfg3k_ncu.json",
-    ("cfg5", "langevin-constant", "stream"): "r02_term_tma_cfg5_ncu.json",
+    ("cfg5", "langevin-constant", "stream"): "r02_term_xs_cfg5_ncu.json",
     ("cfg5", "langevin-variable", "stream"): "r02_term_varx_cfg5var_ncu.json",
     ("hybrid", 256): "r02_term_tma_hybrid256_ncu.json",
     ("hybrid", 512): "r02_term_tma_hybrid512_ncu.json",
@@ -427,7 +428,8 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
             engine["kernel"] = "term_varx_kernel"  # x-split variant: wide grids, 64 source pairs
     names = ctx.kernel_names()
     launched = names["stream"] if engine["name"] == "stream" else names["cluster"]
-    for kname in ("term_varx_kernel", "term_var_kernel", "term_generic_k_kernel", "term2_kernel", "term_tma_kernel"):
+    for kname in ("term_varx_kernel", "term_var_kernel", "term_generic_k_kernel", "term2_kernel", "term_xs_kernel",
+                  "term_tma_kernel"):
         if engine["name"] == "stream" and kname in launched:
             engine["kernel"] = kname  # the name of the kernel that actually ran
             break

@@ -876,6 +876,10 @@ struct MagnusSession {
     DevBuf<int> tpar;
     DevBuf<unsigned long long> tn2, sn2;
     bool finished = false;         // finish() moved the buffers out: every later call is refused
+    // streaming x-march engine (term_xs.cu): T/S are x-major while its pass loop runs
+    bool use_xs = false;
+    bool xs_major = false;
+    DevBuf<double> yg; // the window's folded Y rows per path
     std::vector<cudaEvent_t> ev;
     s2b_magnus_stats stats{};
 
@@ -922,6 +926,11 @@ namespace {
 
 void run_records(MagnusSession& s, const double* S2base = nullptr) {
     if (s.R <= 1) return;
+    if (s.xs_major) {
+        xs_records(s.ctx, s.cnt.p, s.recq.p, s.S[0].p, s.S[1].p, s.rec_ptrs.p, static_cast<int>(s.op->nx),
+                   static_cast<int>(s.op->nv), s.M);
+        return;
+    }
     dim3 grid(static_cast<unsigned>(std::min<size_t>((s.n + 255) / 256, 64)), 64);
     record_kernel<<<grid, 256, 0, s.ctx->stream>>>(s.cnt.p, s.recq.p, s.S[0].p, s.S[1].p, s.rec_ptrs.p, s.n, S2base);
     S2B_LAUNCHED(s.ctx);
@@ -993,7 +1002,9 @@ void launch_term(MagnusSession& s) {
         S2B_CUDA(cudaEventCreate(&e1));
         S2B_CUDA(cudaEventRecord(e0, s.ctx->stream));
     }
-    if (variant == 0) {
+    if (s.xs_major) {
+        launch_term_xs(s.ctx, s.op, a, s.iv.p + s.M, s.yg.p, s.M, s.nz);
+    } else if (variant == 0) {
         const int bs = 256;
         const size_t blocks_per_path = (s.n + bs - 1) / bs;
         const int grid = grid_for(s.ctx, s.M * blocks_per_path, bs);
@@ -1127,6 +1138,7 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
             const bool ok = op->variant != 0 &&
                             cluster_engine_supported(op->variant, static_cast<int>(op->nx), static_cast<int>(op->nv));
             s->use_cluster = ok && !(eng && std::strcmp(eng, "stream") == 0);
+            s->use_xs = !s->use_cluster && term_xs_supported(op);
             if (s->use_cluster && cluster_xmi_supported(op->variant, static_cast<int>(op->nx), static_cast<int>(op->nv)))
                 s->sx.alloc(cluster_xmi_scratch(static_cast<int>(op->nx), static_cast<int>(op->nv), &s->sx_slots));
         }
@@ -1231,7 +1243,24 @@ void prepare_windows(MagnusSession* s, size_t w0, size_t w1) {
 
 // The streaming pass engine over paths [p_lo, M): one Taylor term of every live path per
 // pass, per-path state machines in control_kernel (see the file header).
+// x-major <-> row-major for the streaming x-march engine: every path's current accumulator
+// S[par[p]][p] is transposed into T[par[p]][p] (the term buffers are dead at a window boundary),
+// then the S and T buffers trade places.
+void xs_relayout(MagnusSession* s, bool to_xmajor) {
+    const int nx = static_cast<int>(s->op->nx), nv = static_cast<int>(s->op->nv);
+    xs_transpose_paths(s->ctx, s->S[0].p, s->S[1].p, s->T[0].p, s->T[1].p, s->iv.p + 5 * s->M, s->M,
+                       to_xmajor ? nv : nx, to_xmajor ? nx : nv);
+    std::swap(s->S[0].p, s->T[0].p);
+    std::swap(s->S[1].p, s->T[1].p);
+    s->xs_major = to_xmajor;
+}
+
 void stream_loop(MagnusSession* s, int stop, int p_lo) {
+    const bool xs = s->use_xs && p_lo == 0;
+    if (xs) {
+        if (!s->yg.p) s->yg.alloc(term_xs_y_doubles(s->op, s->M));
+        xs_relayout(s, true);
+    }
     {
         // (re)activate every live path at the current window boundary; window 0 also
         // initialises the per-path state (parity, records, counters)
@@ -1260,6 +1289,7 @@ void stream_loop(MagnusSession* s, int stop, int p_lo) {
         }
         chunk = std::min(chunk * 2, 64);
     }
+    if (xs) xs_relayout(s, false);
 }
 
 // The two-term streaming engine over paths [p_lo, M): two Taylor terms of every live path per

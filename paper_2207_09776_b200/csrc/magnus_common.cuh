@@ -288,5 +288,17 @@ bool cluster_xmi_supported(int variant, int nx, int nv);
 size_t cluster_xmi_scratch(int nx, int nv, int* slots);
 void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterBatch& b);
 
+// Streaming x-march engine (term_xs.cu): the compressed Langevin stencils on grids no cluster
+// holds (nx >= 256, multiples of 128 x 32).  While it runs, a session's term and accumulator
+// vectors are x-major ([path][x][v]); S2B_XS=0 disables it.
+bool term_xs_supported(const s2b_operator* op);
+size_t term_xs_y_doubles(const s2b_operator* op, size_t M);
+void launch_term_xs(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, const int* seg, double* Yg,
+                    size_t M, bool nz);
+void xs_transpose_paths(s2b_context* ctx, const double* S0, const double* S1, double* T0, double* T1,
+                        const int* par, size_t M, int R, int C);
+void xs_records(s2b_context* ctx, const int* cnt, const int4* recq, const double* S0, const double* S1,
+                double* const* rec, int nx, int nv, size_t M);
+
 } // namespace mg
 } // namespace s2b

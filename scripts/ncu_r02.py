@@ -50,7 +50,7 @@ def main():
         hyb = roof.get("hybrid_paths") or 0
         traffic = f("dram__bytes_read.sum") + f("dram__bytes_write.sum")
         dur = f("gpu__time_duration.sum")
-        stream = name.startswith(("tma", "var"))
+        stream = name.startswith(("tma", "var", "xs"))
         live = (hyb if name.startswith("tma_hybrid") else paths)
         stalls = {k[34:-23]: float(v[0]) for k, v in d.items()
                   if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")}

@@ -12,7 +12,8 @@ from test_gpu_parity import gpu_magnus
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = {"xm": {}, "band": {"S2B_XM": "0"}, "stream": {"S2B_ENGINE": "stream"}}
+ENGINES = {"xm": {}, "band": {"S2B_XM": "0"}, "stream": {"S2B_ENGINE": "stream"},
+           "stream-tma": {"S2B_ENGINE": "stream", "S2B_XS": "0"}}
 
 
 @pytest.fixture
@@ -60,7 +61,7 @@ def test_xm_stopping_rule_tolerances(ref, s2b, ctx, engine, d, tol):
     assert stats["engine"] == 2
 
 
-@pytest.mark.parametrize("engine", ["xm", "band"], indirect=True)
+@pytest.mark.parametrize("engine", ["xm", "band", "stream", "stream-tma"], indirect=True)
 def test_engines_blowup_exits_256(ref, s2b, ctx, engine):
     d, T, dt, dt_leb, M = 256, 0.02, 0.01, 1e-3, 2
     # window norm cap
@@ -132,7 +133,8 @@ def test_euler_engines_blowup_256(ref, s2b, ctx, em_engine, d):
     assert np.array_equal(ens[0].states(), want[0])
 
 
-ENGINES_512 = {"xmi": {}, "stream": {"S2B_ENGINE": "stream"}}
+ENGINES_512 = {"xmi": {}, "stream": {"S2B_ENGINE": "stream"},
+               "stream-tma": {"S2B_ENGINE": "stream", "S2B_XS": "0"}}
 
 
 @pytest.fixture

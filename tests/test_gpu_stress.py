@@ -1,7 +1,7 @@
 """Race / synchronisation stress in place of compute-sanitizer (closed on this GPU pool, see
 profiles/r02_sanitizer.txt): every synchronisation-heavy kernel -- DSMEM halo pushes and
 cluster barriers (cluster_xm, cluster_xmi, cluster_magnus, em_cluster), TMA rings with
-mbarrier phases (term_tma, term_var, term_varx, em_tb) -- is run with its persistent grid capped
+mbarrier phases (term_tma, term_xs, term_var, term_varx, em_tb) -- is run with its persistent grid capped
 at 1, 2, 3 and 5 CTAs / clusters (S2B_GRID_CAP) and at full size, several times.  Different
 grids change which work items share an SM, how long every CTA runs and how its mbarrier
 phases wrap across items; a race or a missed wait shows up as a bit difference between runs.
@@ -38,8 +38,11 @@ CASES = {
     "cluster_xm-256": (lambda s, c: _magnus(s, c, 256, M=3), {}),
     "cluster_xmi-512": (lambda s, c: _magnus(s, c, 512, M=2, dt=0.0005), {}),
     "cluster_band-256": (lambda s, c: _magnus(s, c, 256, M=3, order=2), {"S2B_XM": "0"}),
-    "term_tma-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream"}),
-    "term_tma-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {}),
+    "term_tma-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream", "S2B_XS": "0"}),
+    "term_xs-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream"}),
+    "term_xs-512": (lambda s, c: _magnus(s, c, 512, M=2), {"S2B_ENGINE": "stream"}),
+    "term_tma-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {"S2B_XS": "0"}),
+    "term_xs-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {}),
     "term2-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream", "S2B_TERM2": "1"}),
     "term_var-256": (lambda s, c: _magnus(s, c, 256, "langevin-variable", M=5, dt=0.001), {}),
     "em_cluster_ip-64": (lambda s, c: _euler(s, c, 64, M=7), {}),
