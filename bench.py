@@ -39,7 +39,9 @@ ENGINES = {
                 "20% of the paths run on the streaming engine on the idle SMs (S2B_HYBRID)"},
     0: {"name": "stream", "kernel": "term_tma_kernel", "profile": "term_kernel_ncu.json",
         "note": "streaming pass engine: term and accumulator round-trip HBM every Taylor term (constant "
-                "Langevin on grids >= 256 columns: the x-march term_xs_kernel, x-major tiles by TMA)"},
+                "Langevin on grids >= 256 columns: the x-march term_xs2_kernel, x-major tiles by TMA, TWO "
+                "terms per pass -- 40 B per two terms, so achieved is the 32 B/term streaming-equivalent "
+                "rate and traffic the real DRAM bytes)"},
     1: {"name": "cluster-band", "kernel": "cluster_magnus_kernel", "profile": "cluster_kernel_ncu.json",
         "note": "cluster-resident: the path stays in shared memory for the window; achieved is the "
                 "streaming-equivalent rate (can exceed HBM peak), traffic the real DRAM bytes"},
@@ -156,7 +158,7 @@ PROFILE_OF = {
     ("cfg4", "langevin-constant", "cluster-xmi"): "r02_xmi_cfg4_ncu.json",
     ("cfg3", "langevin-variable", "stream"): "r02_term_var_cfg3_ncu.json",
     ("cfg3k", "kinetic-variable", "stream"): "r02_term_varx_cfg3k_ncu.json",
-    ("cfg5", "langevin-constant", "stream"): "r02_term_xs_cfg5_ncu.json",
+    ("cfg5", "langevin-constant", "stream"): "r02_term_xs2_cfg5_ncu.json",
     ("cfg5", "langevin-variable", "stream"): "r02_term_varx_cfg5var_ncu.json",
     ("hybrid", 256): "r02_term_tma_hybrid256_ncu.json",
     ("hybrid", 512): "r02_term_tma_hybrid512_ncu.json",
@@ -428,8 +430,8 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
             engine["kernel"] = "term_varx_kernel"  # x-split variant: wide grids, 64 source pairs
     names = ctx.kernel_names()
     launched = names["stream"] if engine["name"] == "stream" else names["cluster"]
-    for kname in ("term_varx_kernel", "term_var_kernel", "term_generic_k_kernel", "term2_kernel", "term_xs_kernel",
-                  "term_tma_kernel"):
+    for kname in ("term_varx_kernel", "term_var_kernel", "term_generic_k_kernel", "term2_kernel", "term_xs2_kernel",
+                  "term_xs_kernel", "term_tma_kernel"):
         if engine["name"] == "stream" and kname in launched:
             engine["kernel"] = kname  # the name of the kernel that actually ran
             break
@@ -475,7 +477,9 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
             "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
             "kernel": engine["kernel"], "kernel_mangled": launched, "engine": engine["name"],
             "launches": tk_launches, "kernel_ms": tk_ms,
-            "bytes_model": "32 B per path*gridpoint*term (24 B for the k=1 term of a segment)",
+            "bytes_model": "32 B per path*gridpoint*term (24 B for the k=1 term of a segment)"
+                           + ("; term_xs2_kernel moves 40 B per two terms, so this is its streaming-equivalent rate"
+                              if engine["kernel"] == "term_xs2_kernel" else ""),
             "traffic_source": f"profiles/{prof_name} (ncu dram__bytes, scaled per launch)"
                               + (" + the streaming-engine capture of the hybrid slice" if hyb else ""),
             "stale_profile": bool(stale or stream_stale),

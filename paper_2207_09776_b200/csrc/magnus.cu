@@ -879,7 +879,8 @@ struct MagnusSession {
     // streaming x-march engine (term_xs.cu): T/S are x-major while its pass loop runs
     bool use_xs = false;
     bool xs_major = false;
-    DevBuf<double> yg; // the window's folded Y rows per path
+    DevBuf<double> yg;   // the window's folded Y rows per path
+    DevBuf<int4> xs_meta; // per live path of a pass: (path, k, parity, segments)
     std::vector<cudaEvent_t> ev;
     s2b_magnus_stats stats{};
 
@@ -927,7 +928,7 @@ namespace {
 void run_records(MagnusSession& s, const double* S2base = nullptr) {
     if (s.R <= 1) return;
     if (s.xs_major) {
-        xs_records(s.ctx, s.cnt.p, s.recq.p, s.S[0].p, s.S[1].p, s.rec_ptrs.p, static_cast<int>(s.op->nx),
+        xs_records(s.ctx, s.cnt.p, s.recq.p, s.S[0].p, s.S[1].p, S2base, s.rec_ptrs.p, static_cast<int>(s.op->nx),
                    static_cast<int>(s.op->nv), s.M);
         return;
     }
@@ -1003,7 +1004,7 @@ void launch_term(MagnusSession& s) {
         S2B_CUDA(cudaEventRecord(e0, s.ctx->stream));
     }
     if (s.xs_major) {
-        launch_term_xs(s.ctx, s.op, a, s.iv.p + s.M, s.yg.p, s.M, s.nz);
+        launch_term_xs(s.ctx, s.op, a, s.iv.p + s.M, s.yg.p, s.xs_meta.p, s.M, s.nz);
     } else if (variant == 0) {
         const int bs = 256;
         const size_t blocks_per_path = (s.n + bs - 1) / bs;
@@ -1076,6 +1077,17 @@ void launch_term2(MagnusSession& s) {
     const int nt = static_cast<int>((std::max<size_t>((s.op->nx + 1) / 2, nye) + 31) / 32 * 32);
     const int H = kVariants[variant].rx <= 2 ? 2 : 4;
     const size_t rw = s.op->nx + 2 * H;
+    if (s.xs_major) {
+        launch_term_xs2(s.ctx, s.op, a, b, s.iv.p + s.M, s.yg.p, s.xs_meta.p, s.M, s.nz);
+        S2B_LAUNCHED(s.ctx);
+        s.stats.term_launches += 1;
+        if (s.timing) {
+            S2B_CUDA(cudaEventRecord(e1, s.ctx->stream));
+            s.ev.push_back(e0);
+            s.ev.push_back(e1);
+        }
+        return;
+    }
     const size_t smem = 128 + (kStages * rw + kStages * s.op->nx + 2 * rw + 8 * static_cast<size_t>(yst) +
                                static_cast<size_t>(kPairSlots) * nye) * 8;
     const size_t work = s.M * static_cast<size_t>(a.nstrips);
@@ -1259,6 +1271,7 @@ void stream_loop(MagnusSession* s, int stop, int p_lo) {
     const bool xs = s->use_xs && p_lo == 0;
     if (xs) {
         if (!s->yg.p) s->yg.alloc(term_xs_y_doubles(s->op, s->M));
+        if (!s->xs_meta.p) s->xs_meta.alloc(s->M);
         xs_relayout(s, true);
     }
     {
@@ -1297,6 +1310,7 @@ void stream_loop(MagnusSession* s, int stop, int p_lo) {
 // S0/S1 (normalize2_kernel), so the session looks exactly as after one-term passes.
 void stream_loop2(MagnusSession* s, int stop, int p_lo) {
     const size_t M = s->M, n = s->n;
+    const bool xs = s->use_xs && p_lo == 0 && term_xs2_enabled();
     if (!s->S2.p || s->s2_lo != static_cast<size_t>(p_lo)) {
         s->S2.release();
         s->S2.alloc((M - p_lo) * n);
@@ -1311,6 +1325,11 @@ void stream_loop2(MagnusSession* s, int stop, int p_lo) {
     S2B_CUDA(cudaMemsetAsync(s->tn2.p, 0, s->tn2.bytes(), s->ctx->stream));
     S2B_CUDA(cudaMemsetAsync(s->sn2.p, 0, s->sn2.bytes(), s->ctx->stream));
     const double* S2base = s->S2.p - s->s2_lo * n;
+    if (xs) {
+        if (!s->yg.p) s->yg.alloc(term_xs_y_doubles(s->op, s->M));
+        if (!s->xs_meta.p) s->xs_meta.alloc(s->M);
+        xs_relayout(s, true);
+    }
     {
         Ctl c = s->ctl(stop);
         c.p_lo = p_lo;
@@ -1345,6 +1364,7 @@ void stream_loop2(MagnusSession* s, int stop, int p_lo) {
             s->iv.p + 5 * M, M, p_lo);
         S2B_LAUNCHED(s->ctx);
     }
+    if (xs) xs_relayout(s, false);
 }
 
 // Hybrid split: the clusters of the x-march engines pack 15 x 8 (256^2) or 7 x 16 (512^2) per
@@ -1542,7 +1562,7 @@ void session_advance(MagnusSession* s, size_t n_windows) {
         s->cur_window = stop;
         return;
     }
-    if (term2_enabled(*s))
+    if (term2_enabled(*s) || (s->use_xs && term_xs2_enabled()))
         stream_loop2(s, stop, 0);
     else
         stream_loop(s, stop, 0);

@@ -294,11 +294,15 @@ void launch_cluster_xmi(s2b_context* ctx, int variant, const ClusterBatch& b);
 bool term_xs_supported(const s2b_operator* op);
 size_t term_xs_y_doubles(const s2b_operator* op, size_t M);
 void launch_term_xs(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, const int* seg, double* Yg,
-                    size_t M, bool nz);
+                    int4* meta4, size_t M, bool nz);
 void xs_transpose_paths(s2b_context* ctx, const double* S0, const double* S1, double* T0, double* T1,
                         const int* par, size_t M, int R, int C);
 void xs_records(s2b_context* ctx, const int* cnt, const int4* recq, const double* S0, const double* S1,
-                double* const* rec, int nx, int nv, size_t M);
+                const double* S2, double* const* rec, int nx, int nv, size_t M);
+// two Taylor terms per pass (term_xs2_kernel, term2's buffer protocol; default, S2B_XS2=0 disables)
+bool term_xs2_enabled();
+void launch_term_xs2(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, const Term2Args& b, const int* seg,
+                     double* Yg, int4* meta4, size_t M, bool nz);
 
 } // namespace mg
 } // namespace s2b

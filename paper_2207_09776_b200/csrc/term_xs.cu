@@ -93,6 +93,13 @@ __device__ __forceinline__ void tma_tile3(uint32_t dst, const CUtensorMap* map, 
         : "memory");
 }
 
+// st.global under a predicate (keeps an epilogue branch-free: the compiler otherwise wraps a
+// conditional store and its operands in a divergent branch)
+__device__ __forceinline__ void st_if(double* ptr, double v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(ptr), "d"(v),
+                 "r"(static_cast<int>(p)));
+}
+
 } // namespace
 
 // T0, T1, S0, S1 with the term box (rows + halo, columns + halo); S0, S1 with the accumulator box
@@ -108,7 +115,8 @@ namespace {
 // the BM entries.  The fold is the one of every other engine: slots ascending from 0.0, zero
 // coefficients skipped.
 template <uint64_t MASK, uint32_t BM>
-__global__ void xs_fold_kernel(TermArgs a, const int* __restrict__ seg, double* __restrict__ Yg, int YW) {
+__global__ void xs_fold_kernel(TermArgs a, const int* __restrict__ seg, double* __restrict__ Yg, int YW, int yrows,
+                               int4* __restrict__ meta4, const int* __restrict__ tpar) {
     constexpr int NBM = MaskInfo<MASK>::count();
     constexpr int NBB = popc32x(BM);
     constexpr int NYE = kClasses * NBM;
@@ -118,6 +126,9 @@ __global__ void xs_fold_kernel(TermArgs a, const int* __restrict__ seg, double* 
     const int live = a.cnt[0];
     for (int q = blockIdx.y; q < live; q += gridDim.y) {
         const int p = a.act[q];
+        // every live path's (path, k, parity, segments) for the term kernel's producer
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            meta4[q] = make_int4(p, a.k[p], a.par[p] | (tpar ? tpar[p] << 2 : 0), a.nseg[p]);
         if (a.k[p] != 1 || seg[p] != 0) continue;
         const double* c = a.ctab + (static_cast<size_t>(p) * a.nwin + a.win[p]) * 6;
         for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nv * NE; u += gridDim.x * blockDim.x) {
@@ -145,14 +156,15 @@ __global__ void xs_fold_kernel(TermArgs a, const int* __restrict__ seg, double* 
                 const double cs = __ldg(c + sl);
                 if (cs != 0.0) y += cs * __ldg(wr + k);
             }
-            Yg[(static_cast<size_t>(p) * nv + row) * YW + j] = y;
+            Yg[(static_cast<size_t>(p) * yrows + row + 2) * YW + j] = y;
         }
     }
 }
 
-template <int KRX, int KRV, uint64_t MASK, uint32_t BM, bool NZ>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, bool NZ, int NVC>
 __global__ void __launch_bounds__(kXsNT, 1)
-    term_xs_kernel(const __grid_constant__ XsMaps maps, TermArgs a, const double* __restrict__ Yg, int nrb, int nxt) {
+    term_xs_kernel(const __grid_constant__ XsMaps maps, TermArgs a, const double* __restrict__ Yg, int yrows,
+                   const int4* __restrict__ meta4, int nrb, int nxt, int pf) {
     using L = XsLayout<KRX, KRV, MASK, BM>;
     using RE = XsRow<MASK>;
     constexpr int NBM = L::NBM, NBB = L::NBB, YW = L::YW, TR = L::TR;
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(kXsNT, 1)
     static_assert(LX % P == 0, "march groups");
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int nx = a.op.nx, nv = a.op.nv;
+    const int nx = a.op.nx, nv = NVC > 0 ? NVC : a.op.nv; // compile-time column height: immediate store offsets
     const size_t n = static_cast<size_t>(nx) * nv;
 
     extern __shared__ unsigned char smem_raw[];
@@ -186,18 +198,34 @@ __global__ void __launch_bounds__(kXsNT, 1)
     const long long nsteps = mine * nxt;
 
     // step g: item blockIdx.x + (g / nxt) * gridDim.x, tile g % nxt
+    // The producer (thread 0) reads each item's (path, k, parity, segments) one item ahead, so the
+    // issue of an item's first tile never waits on a global load (a late producer holds every
+    // warp at the next CTA barrier)
+    const long long nitems = mine;
+    auto item_meta = [&](long long it) -> int4 {
+        return it < nitems ? __ldg(meta4 + (blockIdx.x + it * gridDim.x) / nrb) : make_int4(0, 1, 0, 1);
+    };
+    int4 cur_m = make_int4(0, 1, 0, 1), next_m = make_int4(0, 1, 0, 1);
+    if (t == 0) next_m = item_meta(0);
     auto issue = [&](long long g) {
         const long long it = g / nxt;
         const int tile = static_cast<int>(g - it * nxt);
+        if (tile == 0) {
+            if (pf) {
+                cur_m = next_m;
+                next_m = item_meta(it + 1);
+            } else {
+                cur_m = item_meta(it);
+            }
+        }
         const long long wi = blockIdx.x + it * gridDim.x;
-        const int p = a.act[wi / nrb];
+        const int p = cur_m.x, kk = cur_m.y, par = cur_m.z;
         const int rb = static_cast<int>(wi % nrb);
-        const int kk = a.k[p], par = a.par[p];
         const int slot = static_cast<int>(g % kXsStages);
         // read by every thread at the step, after at least one CTA barrier (kXsStages >= 2)
         meta[slot][0] = p;
         meta[slot][1] = par;
-        minv[slot] = 1.0 / (static_cast<double>(a.nseg[p]) * kk);
+        minv[slot] = 1.0 / (static_cast<double>(cur_m.w) * kk);
         const uint32_t bar = full_u + 8 * slot;
         const uint32_t st = base_u + slot * L::STAGE;
         uint32_t bytes = L::TBYTES + L::SBYTES;
@@ -208,7 +236,7 @@ __global__ void __launch_bounds__(kXsNT, 1)
         tma_tile3(st + L::SOFF, &maps.s[par], rb * kXsRows, tile * kCW, p, bar);
         if (tile == 0)
             tma_row_u(base_u + L::YOFF + static_cast<uint32_t>(it & 1) * L::YSTR,
-                      Yg + (static_cast<size_t>(p) * nv + static_cast<size_t>(rb) * kXsRows) * YW, L::YBYTES, bar);
+                      Yg + (static_cast<size_t>(p) * yrows + static_cast<size_t>(rb) * kXsRows + 2) * YW, L::YBYTES, bar);
     };
     if (t == 0)
         for (long long g = 0; g < kXsStages && g < nsteps; ++g) issue(g);
@@ -347,6 +375,335 @@ __global__ void __launch_bounds__(kXsNT, 1)
     }
 }
 
+// ---- two Taylor terms per pass (temporal blocking) ------------------------------------------
+//
+// term_xs2_kernel applies the generator twice per pass: t_k is computed into shared memory and
+// never leaves the SM, so a pass reads t_{k-1}, s_{k-1} and writes t_{k+1}, s_{k+1} and s_k (the
+// stopping rule may end the segment at k) -- 40 B per two terms instead of 64 B.  It follows
+// term2_kernel's buffer protocol, so stream_loop2 / control2_kernel / normalize2 drive it
+// unchanged: T[tpar] -> T[tpar^1] (t_{k+1}); S[sidx] -> S[(sidx+1)%3] (s_{k+1}), S[(sidx+2)%3]
+// (s_k); maxima of term k in tn/sn, of term k+1 in tn2/sn2.
+// Work item (path, 28-row block [v0, v0+28)); lane r is row v0-2+r in both phases:
+//  * phase 1: t_k on 32 rows (2 halo rows on each side, recomputed by the neighbouring items;
+//    rows outside the grid are zero) over tile columns [jW+2, jW+W+2), into the shared t_k
+//    buffer TK whose first 4 columns [jW-2, jW+2) were computed by the previous tile (the x-march
+//    runs ahead by 2 columns; tile 0 computes columns 0, 1 itself and zeroes -2, -1).  Lanes
+//    2..29 also form s_k = s_{k-1} + t_k and write it.
+//  * phase 2: t_{k+1} = (Y t_k) / (s (k+1)) on lanes 2..29 over [jW, jW+W), s_{k+1} =
+//    (s_{k-1} + t_k) + t_{k+1} -- the same operations on the same operands as two single passes.
+constexpr int kX2Out = 28; // output rows per item
+constexpr int kX2Stages = 2;
+
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM>
+struct Xs2Layout {
+    static constexpr int NBM = MaskInfo<MASK>::count();
+    static constexpr int NBB = popc32x(BM);
+    static constexpr int YW = (NBM + 4 * NBB) | 1;
+    static constexpr int TR = 36;               // input rows v0-4 .. v0+32
+    static constexpr int TX = kCW + 6;          // input columns jW-2 .. jW+W+4
+    static constexpr int SR = kX2Out;           // s_{k-1} rows v0 .. v0+28
+    static constexpr int SX = kCW + 2;          // s_{k-1} columns jW .. jW+W+2
+    static constexpr int KX = kCW + 4;          // t_k columns jW-2 .. jW+W+2
+    static constexpr int TBYTES = TR * TX * 8;
+    static constexpr int SBYTES = SR * SX * 8;
+    static constexpr int YBYTES = 32 * YW * 8;
+    static constexpr int SOFF = (TBYTES + 127) / 128 * 128;
+    static constexpr int STAGE = SOFF + (SBYTES + 127) / 128 * 128;
+    static constexpr int KOFF = kX2Stages * STAGE;
+    static constexpr int YOFF = KOFF + KX * 32 * 8;
+    static constexpr int YSTR = (YBYTES + 127) / 128 * 128;
+    static constexpr int BAROFF = YOFF + 2 * YSTR;
+    static constexpr size_t bytes() { return 128 + BAROFF + 64; }
+    static_assert(KRX <= 2 && KRV <= 2, "two-term tiles carry 2 halo rows / columns per term");
+    static_assert(SR * 8 % 16 == 0 && TR * 8 % 16 == 0 && YBYTES % 16 == 0, "TMA extents");
+};
+
+// The x-march of one thread over NPTS points of its row: point i reads the tile at
+// tin[(i + dx) * CS + dv].  Points [0, LB) take the x-boundary classes 0, 1; points RB0, RB0+1
+// (RB0 >= 0) the classes nx-2, nx-1 (Y entries of BM from yb, the row's boundary block).
+// epi(i, acc) receives the point's stencil sum (summed from 0.0 in ascending (dv, dx) order, or
+// from the first product under NZ).
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, bool NZ, int CS, int NPTS, int LB, int RB0, class Epi>
+__device__ __forceinline__ void xs_march(const double* tin, const double* y, const double* yb, Epi&& epi) {
+    using RE = XsRow<MASK>;
+    constexpr int NBB = popc32x(BM);
+    constexpr int P = 4, RW = 8;
+    static_assert(RE::span(0) + P - 1 <= RW && RE::span(1) + P - 1 <= RW && RE::span(2) + P - 1 <= RW, "ring size");
+    double win[(2 * KRV + 1) * RW];
+#pragma unroll
+    for (int dv = -KRV; dv <= KRV; ++dv) {
+        if (RE::span(dv) > 0) {
+#pragma unroll
+            for (int cc = 0; cc < RW; ++cc)
+                if (cc < RE::span(dv) - 1) win[(dv + KRV) * RW + cc] = tin[(RE::lo(dv) + cc) * CS + dv];
+        }
+    }
+#pragma unroll
+    for (int gq = 0; gq < NPTS; gq += P) {
+#pragma unroll
+        for (int dv = -KRV; dv <= KRV; ++dv)
+            if (RE::span(dv) > 0) {
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    if (gq + q < NPTS) {
+                        const int col = gq + q + RE::hi(dv);
+                        win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))] = tin[col * CS + dv];
+                    }
+                }
+            }
+        double acc[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) acc[q] = 0.0;
+#pragma unroll
+        for (int dv = -KRV; dv <= KRV; ++dv) {
+#pragma unroll
+            for (int dx = -KRX; dx <= KRX; ++dx) {
+                if (MaskInfo<MASK>::has(dx, dv)) {
+                    const int e = MaskInfo<MASK>::rank(box_bit(dx, dv));
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        const int i = gq + q;
+                        if (i < NPTS) {
+                            double wv = y[e];
+                            if constexpr (NBB > 0) {
+                                if ((BM >> e) & 1) {
+                                    const int k4 = i < LB ? i : (RB0 >= 0 && i >= RB0 && i < RB0 + 2 ? 2 + (i - RB0) : -1);
+                                    if (k4 >= 0) wv = yb[k4 * NBB + bm_rankx(BM, e)];
+                                }
+                            }
+                            const int col = i + dx;
+                            const double pr = wv * win[(dv + KRV) * RW + ((col - RE::lo(dv)) & (RW - 1))];
+                            acc[q] = (NZ && e == 0) ? pr : acc[q] + pr;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+            if (gq + q < NPTS) epi(gq + q, acc[q]);
+    }
+}
+
+// T0, T1, S0, S1, S2 with the input box; S0, S1, S2 with the accumulator box
+struct Xs2Maps {
+    CUtensorMap t[5];
+    CUtensorMap s[3];
+};
+
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, bool NZ, int NVC>
+__global__ void __launch_bounds__(kXsNT, 1)
+    term_xs2_kernel(const __grid_constant__ Xs2Maps maps, TermArgs a, Term2Args b, const double* __restrict__ Yg,
+                    int yrows, const int4* __restrict__ meta4, int nrb, int nxt) {
+    using L = Xs2Layout<KRX, KRV, MASK, BM>;
+    constexpr int NBM = L::NBM, YW = L::YW;
+    constexpr int NW = kXsNT / 32;
+    constexpr int LX = kCW / NW;
+    static_assert(LX == 16, "16 columns per warp");
+
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int nx = a.op.nx, nv = NVC > 0 ? NVC : a.op.nv;
+    const size_t n = static_cast<size_t>(nx) * nv;
+
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t base_u = (smem_u32(smem_raw) + 127u) & ~127u;
+    unsigned char* base = smem_raw + (base_u - smem_u32(smem_raw));
+    const uint32_t full_u = base_u + L::BAROFF;
+    double* TK = reinterpret_cast<double*>(base + L::KOFF); // [KX][32]
+    __shared__ unsigned long long red[2][4][NW];
+    __shared__ int meta[kX2Stages][3];  // path, accumulator index, term parity
+    __shared__ double minv[kX2Stages][2];
+
+    for (int q = t; q < L::KX * 32; q += kXsNT) TK[q] = 0.0;
+    if (t == 0) {
+        for (int s = 0; s < kX2Stages; ++s) mbar_init(reinterpret_cast<uint64_t*>(base + L::BAROFF) + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const long long items = static_cast<long long>(a.cnt[0]) * nrb;
+    const long long mine = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long nsteps = mine * nxt;
+    auto item_meta = [&](long long it) -> int4 {
+        return it < mine ? __ldg(meta4 + (blockIdx.x + it * gridDim.x) / nrb) : make_int4(0, 1, 0, 1);
+    };
+    int4 cur_m = make_int4(0, 1, 0, 1), next_m = make_int4(0, 1, 0, 1);
+    if (t == 0) next_m = item_meta(0);
+    auto issue = [&](long long g) {
+        const long long it = g / nxt;
+        const int tile = static_cast<int>(g - it * nxt);
+        if (tile == 0) {
+            cur_m = next_m;
+            next_m = item_meta(it + 1);
+        }
+        const long long wi = blockIdx.x + it * gridDim.x;
+        const int p = cur_m.x, kk = cur_m.y, sidx = cur_m.z & 3, tp = cur_m.z >> 2;
+        const int v0 = static_cast<int>(wi % nrb) * kX2Out;
+        const int slot = static_cast<int>(g % kX2Stages);
+        meta[slot][0] = p;
+        meta[slot][1] = sidx;
+        meta[slot][2] = tp;
+        minv[slot][0] = 1.0 / (static_cast<double>(cur_m.w) * kk);
+        minv[slot][1] = 1.0 / (static_cast<double>(cur_m.w) * (kk + 1));
+        const uint32_t bar = full_u + 8 * slot;
+        const uint32_t st = base_u + slot * L::STAGE;
+        uint32_t bytes = L::TBYTES + L::SBYTES;
+        if (tile == 0) bytes += L::YBYTES;
+        mbar_expect_tx_u(bar, bytes);
+        // term k-1: the accumulator itself at a segment's first term (term = accum = y)
+        tma_tile3(st, &maps.t[kk == 1 ? 2 + sidx : tp], v0 - 4, tile * kCW - 2, p, bar);
+        tma_tile3(st + L::SOFF, &maps.s[sidx], v0, tile * kCW, p, bar);
+        if (tile == 0) // Y rows v0-2 .. v0+30 (padded layout: row v at index v + 2)
+            tma_row_u(base_u + L::YOFF + static_cast<uint32_t>(it & 1) * L::YSTR,
+                      Yg + (static_cast<size_t>(p) * yrows + static_cast<size_t>(v0)) * YW, L::YBYTES, bar);
+    };
+    if (t == 0)
+        for (long long g = 0; g < kX2Stages && g < nsteps; ++g) issue(g);
+    __syncthreads();
+
+    double y[NBM];
+    double inv1 = 0.0, inv2 = 0.0;
+    unsigned long long tm1 = 0, sm1 = 0, tm2 = 0, sm2 = 0;
+    int p = 0, v0 = 0;
+    bool rowok = false, own = false;
+    double* Tn = nullptr; // t_{k+1}
+    double* Sa = nullptr; // s_{k+1}
+    double* Sb = nullptr; // s_k
+
+    for (long long g = 0; g < nsteps; ++g) {
+        const long long it = g / nxt;
+        const int tile = static_cast<int>(g - it * nxt);
+        const int slot = static_cast<int>(g % kX2Stages);
+        mbar_wait_u(full_u + 8 * slot, static_cast<uint32_t>((g / kX2Stages) & 1));
+        const double* ybuf = reinterpret_cast<const double*>(base + L::YOFF + (it & 1) * L::YSTR);
+        if (tile == 0) {
+            const long long wi = blockIdx.x + it * gridDim.x;
+            p = meta[slot][0];
+            const int sidx = meta[slot][1], tp = meta[slot][2];
+            v0 = static_cast<int>(wi % nrb) * kX2Out;
+            const int vr = v0 - 2 + lane;
+            rowok = vr >= 0 && vr < nv;
+            own = lane >= 2 && lane < 2 + kX2Out && vr < nv;
+            inv1 = minv[slot][0];
+            inv2 = minv[slot][1];
+            const size_t pbase = static_cast<size_t>(p) * n;
+            double* const S2 = b.S2;
+            Tn = (tp ? a.T0 : a.T1) + pbase;
+            Sa = (sidx == 0 ? a.S1 : sidx == 1 ? S2 : a.S0) + pbase;
+            Sb = (sidx == 0 ? S2 : sidx == 1 ? a.S0 : a.S1) + pbase;
+#pragma unroll
+            for (int e = 0; e < NBM; ++e) y[e] = ybuf[lane * YW + e];
+            tm1 = sm1 = tm2 = sm2 = 0;
+        }
+        const double* yb = ybuf + lane * YW + NBM;
+        const double* tt = reinterpret_cast<const double*>(base + slot * L::STAGE);
+        const double* ts = reinterpret_cast<const double*>(base + slot * L::STAGE + L::SOFF);
+        const int jW = tile * kCW;
+        const int vr = v0 - 2 + lane;
+        const size_t vo = static_cast<size_t>(vr);
+
+        // Every warp runs ONE unrolled march per phase over its 16 columns; the x-boundary
+        // columns (other Y classes) and the two columns past the grid are masked out of that
+        // march's epilogue and handled by 2-point marches of the edge warps (small code: the
+        // instruction cache holds the kernel).  Epilogues are branch-free: rows a lane does not
+        // own are computed and dropped by predicated stores and selects.
+        const bool edge_l = tile == 0 && warp == 0, edge_r = tile == nxt - 1 && warp == NW - 1;
+        // ---- phase 1: t_k (and s_k) over columns [jW+2, jW+W+2) (+ columns 0, 1 at tile 0)
+        {
+            const int xa = jW + 2 + warp * LX;
+            const int hi1 = edge_r ? LX - 4 : LX; // columns nx-2.. of the last tile: below
+            double* const sbw = Sb + static_cast<size_t>(xa) * nv + vo; // column xa of this lane
+            auto epi1 = [&](int x, double acc, bool keep) {
+                double tv = acc * inv1;
+                tv = rowok ? tv : 0.0;
+                TK[(x - jW + 2) * 32 + lane] = tv;
+                const double sv = ts[(x - jW) * kX2Out + (lane - 2)] + tv;
+                const bool w = own && keep;
+                st_if(sbw + (x - xa) * nv, sv, w);
+                tm1 = umax64(tm1, w ? abs_bits(tv) : 0ull);
+                sm1 = umax64(sm1, w ? abs_bits(sv) : 0ull);
+            };
+            const double* tin = tt + (xa - jW + 2) * L::TR + (lane + 2);
+            xs_march<KRX, KRV, MASK, BM, NZ, L::TR, LX, 0, -1>(tin, y, yb,
+                                                               [&](int i, double acc) { epi1(xa + i, acc, i < hi1); });
+            if (edge_l) // columns 0, 1: classes 0, 1
+                xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 2, -1>(tt + 2 * L::TR + (lane + 2), y, yb,
+                                                                   [&](int i, double acc) { epi1(i, acc, true); });
+            if (edge_r) { // columns nx-2, nx-1: classes 3, 4; nx, nx+1 are outside the grid (zero)
+                xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 0, 0>(tin + (LX - 4) * L::TR, y, yb,
+                                                                  [&](int i, double acc) { epi1(xa + LX - 4 + i, acc, true); });
+                TK[(xa + LX - 2 - jW + 2) * 32 + lane] = 0.0;
+                TK[(xa + LX - 1 - jW + 2) * 32 + lane] = 0.0;
+            }
+        }
+        __syncthreads(); // t_k of the tile (+ the carried columns) complete
+        // the 4 t_k columns the next tile needs on its left: read now, placed after the barrier
+        double carry = 0.0;
+        if (t < 128) carry = TK[(kCW + t / 32) * 32 + (t & 31)];
+
+        // ---- phase 2: t_{k+1}, s_{k+1} over [jW, jW+W) on lanes 2..29
+        {
+            const int xa = jW + warp * LX;
+            const int lo2 = edge_l ? 2 : 0, hi2 = edge_r ? LX - 2 : LX;
+            const size_t cw = static_cast<size_t>(xa) * nv + vo; // column xa of this lane
+            double* const tnw = Tn + cw;
+            double* const saw = Sa + cw;
+            auto epi2 = [&](int x, double acc, bool keep) {
+                const double tk = TK[(x - jW + 2) * 32 + lane];
+                const double sk = ts[(x - jW) * kX2Out + (lane - 2)] + tk;
+                const double tv = acc * inv2;
+                const double sv = sk + tv;
+                const bool w = own && keep;
+                st_if(tnw + (x - xa) * nv, tv, w);
+                st_if(saw + (x - xa) * nv, sv, w);
+                tm2 = umax64(tm2, w ? abs_bits(tv) : 0ull);
+                sm2 = umax64(sm2, w ? abs_bits(sv) : 0ull);
+            };
+            const double* tin = TK + (xa - jW + 2) * 32 + lane;
+            xs_march<KRX, KRV, MASK, BM, NZ, 32, LX, 0, -1>(
+                tin, y, yb, [&](int i, double acc) { epi2(xa + i, acc, i >= lo2 && i < hi2); });
+            if (edge_l)
+                xs_march<KRX, KRV, MASK, BM, NZ, 32, 2, 2, -1>(tin, y, yb,
+                                                                [&](int i, double acc) { epi2(xa + i, acc, true); });
+            if (edge_r)
+                xs_march<KRX, KRV, MASK, BM, NZ, 32, 2, 0, 0>(
+                    tin + (LX - 2) * 32, y, yb, [&](int i, double acc) { epi2(xa + LX - 2 + i, acc, true); });
+        }
+
+        const bool last = tile == nxt - 1;
+        if (last) {
+            const unsigned long long w1 = warp_umax(tm1), w2 = warp_umax(sm1), w3 = warp_umax(tm2), w4 = warp_umax(sm2);
+            if (lane == 0) {
+                red[it & 1][0][warp] = w1;
+                red[it & 1][1][warp] = w2;
+                red[it & 1][2][warp] = w3;
+                red[it & 1][3][warp] = w4;
+            }
+        }
+        __syncthreads(); // the stage and TK are consumed
+        if (t < 128) { // next tile of this item: carry; first tile of an item: columns -2, -1 are zero
+            if (!last)
+                TK[t] = carry;
+            else if (t < 64)
+                TK[t] = 0.0;
+        }
+        if (t == 0) {
+            if (last) {
+                unsigned long long r[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) r[q] = umax64(r[q], red[it & 1][q][w]);
+                if (r[0]) atomicMax(&a.tn[p], r[0]);
+                if (r[1]) atomicMax(&a.sn[p], r[1]);
+                if (r[2]) atomicMax(&b.tn2[p], r[2]);
+                if (r[3]) atomicMax(&b.sn2[p], r[3]);
+            }
+            if (g + kX2Stages < nsteps) issue(g + kX2Stages);
+        }
+    }
+}
+
 // per-path transpose: dst[p][c][r] = src[p][r][c] of an R x C matrix (R, C multiples of 32);
 // path p's source is S[par[p]], its destination T[par[p]] (par == nullptr: buffer 0)
 __global__ void xs_transpose_kernel(const double* __restrict__ s0, const double* __restrict__ s1,
@@ -371,14 +728,14 @@ __global__ void xs_transpose_kernel(const double* __restrict__ s0, const double*
 // queued record snapshots S[par][p] (x-major) -> rec[r][p] (row-major), as record_kernel
 __global__ void xs_record_kernel(const int* __restrict__ cnt, const int4* __restrict__ recq,
                                  const double* __restrict__ S0, const double* __restrict__ S1,
-                                 double* const* __restrict__ rec, int nx, int nv) {
+                                 const double* __restrict__ S2, double* const* __restrict__ rec, int nx, int nv) {
     __shared__ double tile[32][33];
     const size_t n = static_cast<size_t>(nx) * nv;
     const int nq = cnt[2];
     const int v0 = blockIdx.x * 32, x0 = blockIdx.y * 32; // source rows are x, columns v
     for (int q = blockIdx.z; q < nq; q += gridDim.z) {
         const int4 e = recq[q];
-        const double* src = (e.z ? S1 : S0) + static_cast<size_t>(e.x) * n;
+        const double* src = (e.z == 2 ? S2 : e.z ? S1 : S0) + static_cast<size_t>(e.x) * n;
         double* dst = rec[e.y] + static_cast<size_t>(e.x) * n;
         for (int k = threadIdx.y; k < 32; k += blockDim.y)
             tile[k][threadIdx.x] = src[static_cast<size_t>(x0 + k) * nv + v0 + threadIdx.x];
@@ -444,40 +801,104 @@ int xs_yw(int variant) {
     }
 }
 
+// Y rows per path in the padded layout (row v at index v + 2; both kernels' blocks fit, even)
+int xs_yrows(int nv) {
+    const int r32 = (nv + kXsRows - 1) / kXsRows * kXsRows, r28 = (nv + kX2Out - 1) / kX2Out * kX2Out;
+    return (std::max(r32, r28) + 4 + 1) & ~1;
+}
+
+// the window's Y rows of every path that enters a window this pass, and the pass's item metadata
+template <int V>
+void launch_xs_fold(s2b_context* ctx, const TermArgs& a, const int* seg, double* Yg, int4* meta4, const int* tpar,
+                    size_t M) {
+    constexpr Variant v = kVariants[V];
+    using L = typename XsV<V>::L;
+    const int nv = a.op.nv;
+    dim3 grid(static_cast<unsigned>(std::max(1, (nv * (L::NBM + 4 * L::NBB) + 255) / 256)),
+              static_cast<unsigned>(std::min<size_t>(std::max<size_t>(M, 1), 512)));
+    xs_fold_kernel<v.mask, v.bm><<<grid, 256, 0, ctx->stream>>>(a, seg, Yg, L::YW, xs_yrows(nv), meta4, tpar);
+    S2B_LAUNCHED(ctx);
+}
+
 template <int V, bool NZ>
-void launch_xs_v(s2b_context* ctx, const TermArgs& a, const int* seg, double* Yg, size_t live_max) {
+void launch_xs_v(s2b_context* ctx, const TermArgs& a, const int* seg, double* Yg, int4* meta4, size_t live_max) {
     constexpr Variant v = kVariants[V];
     using L = typename XsV<V>::L;
     const int nx = a.op.nx, nv = a.op.nv;
     const size_t M = live_max;
-    // the window's Y rows of every path that enters a window this pass
-    {
-        dim3 grid(static_cast<unsigned>(std::max(1, (nv * (L::NBM + 4 * L::NBB) + 255) / 256)),
-                  static_cast<unsigned>(std::min<size_t>(std::max<size_t>(M, 1), 512)));
-        xs_fold_kernel<v.mask, v.bm><<<grid, 256, 0, ctx->stream>>>(a, seg, Yg, L::YW);
-        S2B_LAUNCHED(ctx);
-    }
+    launch_xs_fold<V>(ctx, a, seg, Yg, meta4, nullptr, M);
     XsMaps maps{};
     const double* tb[4] = {a.T0, a.T1, a.S0, a.S1};
     for (int i = 0; i < 4; ++i) encode_xmaj(&maps.t[i], tb[i], M, nx, nv, L::TR, L::TX);
     encode_xmaj(&maps.s[0], a.S0, M, nx, nv, kXsRows, kCW);
     encode_xmaj(&maps.s[1], a.S1, M, nx, nv, kXsRows, kCW);
-    auto kern = term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ>;
+    auto kern = nv == 1024 ? term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 1024> : term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 0>;
     const size_t smem = L::bytes();
-    static int configured_device = -1;
-    if (configured_device != ctx->device) {
+    static int configured_device[2] = {-1, -1};
+    if (configured_device[nv == 1024] != ctx->device) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured_device = ctx->device;
+        configured_device[nv == 1024] = ctx->device;
     }
     const int nrb = nv / kXsRows, nxt = nx / kCW;
     const size_t work = M * static_cast<size_t>(nrb);
     const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min<size_t>(work, ctx->num_sms))));
-    kern<<<grid, kXsNT, smem, ctx->stream>>>(maps, a, Yg, nrb, nxt);
+    const char* pfe = std::getenv("S2B_XS_PF");
+    const int pf = pfe ? std::atoi(pfe) : 1;
+    kern<<<grid, kXsNT, smem, ctx->stream>>>(maps, a, Yg, xs_yrows(nv), meta4, nrb, nxt, pf);
+    S2B_LAUNCHED(ctx);
+    ctx->k_stream = reinterpret_cast<const void*>(kern);
+}
+
+template <int V, bool NZ>
+void launch_xs2_v(s2b_context* ctx, const TermArgs& a, const Term2Args& b, const int* seg, double* Yg, int4* meta4,
+                  size_t live_max) {
+    constexpr Variant v = kVariants[V];
+    using L = Xs2Layout<v.rx, v.rv, v.mask, v.bm>;
+    static_assert(L::YW == XsV<V>::L::YW, "one Y layout for both kernels");
+    const int nx = a.op.nx, nv = a.op.nv;
+    const size_t M = live_max;
+    launch_xs_fold<V>(ctx, a, seg, Yg, meta4, b.tpar, M);
+    Xs2Maps maps{};
+    const double* tb[5] = {a.T0, a.T1, a.S0, a.S1, b.S2};
+    for (int i = 0; i < 5; ++i) encode_xmaj(&maps.t[i], tb[i], M, nx, nv, L::TR, L::TX);
+    for (int i = 0; i < 3; ++i) encode_xmaj(&maps.s[i], tb[2 + i], M, nx, nv, L::SR, L::SX);
+    auto kern = nv == 1024 ? term_xs2_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 1024> : term_xs2_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 0>;
+    const size_t smem = L::bytes();
+    static int configured_device[2] = {-1, -1};
+    if (configured_device[nv == 1024] != ctx->device) {
+        S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured_device[nv == 1024] = ctx->device;
+    }
+    const int nrb = (nv + kX2Out - 1) / kX2Out, nxt = nx / kCW;
+    const size_t work = M * static_cast<size_t>(nrb);
+    const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min<size_t>(work, ctx->num_sms))));
+    kern<<<grid, kXsNT, smem, ctx->stream>>>(maps, a, b, Yg, xs_yrows(nv), meta4, nrb, nxt);
     S2B_LAUNCHED(ctx);
     ctx->k_stream = reinterpret_cast<const void*>(kern);
 }
 
 } // namespace
+
+// two Taylor terms per pass on the x-march engine (stream_loop2 with term_xs2_kernel), the
+// default; S2B_XS2=0 keeps one term per pass.  cfg5: 1.44e9 vs 1.25e9 windows/s (same run),
+// fp64 pipe 56% of active cycles, DRAM 40 B per two path*gridpoint*terms
+bool term_xs2_enabled() {
+    const char* e = std::getenv("S2B_XS2");
+    return !(e && e[0] == '0');
+}
+
+void launch_term_xs2(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, const Term2Args& b, const int* seg,
+                     double* Yg, int4* meta4, size_t M, bool nz) {
+    switch (op->variant * 2 + (nz ? 1 : 0)) {
+    case 14: launch_xs2_v<7, false>(ctx, a, b, seg, Yg, meta4, M); break;
+    case 15: launch_xs2_v<7, true>(ctx, a, b, seg, Yg, meta4, M); break;
+    case 16: launch_xs2_v<8, false>(ctx, a, b, seg, Yg, meta4, M); break;
+    case 17: launch_xs2_v<8, true>(ctx, a, b, seg, Yg, meta4, M); break;
+    case 18: launch_xs2_v<9, false>(ctx, a, b, seg, Yg, meta4, M); break;
+    case 19: launch_xs2_v<9, true>(ctx, a, b, seg, Yg, meta4, M); break;
+    default: fail(S2B_ERR_RUNTIME, "x-major two-term engine: unsupported variant");
+    }
+}
 
 bool term_xs_supported(const s2b_operator* op) {
     const char* e = std::getenv("S2B_XS");
@@ -488,18 +909,18 @@ bool term_xs_supported(const s2b_operator* op) {
 }
 
 size_t term_xs_y_doubles(const s2b_operator* op, size_t M) {
-    return M * op->nv * static_cast<size_t>(xs_yw(op->variant));
+    return M * static_cast<size_t>(xs_yrows(static_cast<int>(op->nv))) * static_cast<size_t>(xs_yw(op->variant));
 }
 
 void launch_term_xs(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, const int* seg, double* Yg,
-                    size_t M, bool nz) {
+                    int4* meta4, size_t M, bool nz) {
     switch (op->variant * 2 + (nz ? 1 : 0)) {
-    case 14: launch_xs_v<7, false>(ctx, a, seg, Yg, M); break;
-    case 15: launch_xs_v<7, true>(ctx, a, seg, Yg, M); break;
-    case 16: launch_xs_v<8, false>(ctx, a, seg, Yg, M); break;
-    case 17: launch_xs_v<8, true>(ctx, a, seg, Yg, M); break;
-    case 18: launch_xs_v<9, false>(ctx, a, seg, Yg, M); break;
-    case 19: launch_xs_v<9, true>(ctx, a, seg, Yg, M); break;
+    case 14: launch_xs_v<7, false>(ctx, a, seg, Yg, meta4, M); break;
+    case 15: launch_xs_v<7, true>(ctx, a, seg, Yg, meta4, M); break;
+    case 16: launch_xs_v<8, false>(ctx, a, seg, Yg, meta4, M); break;
+    case 17: launch_xs_v<8, true>(ctx, a, seg, Yg, meta4, M); break;
+    case 18: launch_xs_v<9, false>(ctx, a, seg, Yg, meta4, M); break;
+    case 19: launch_xs_v<9, true>(ctx, a, seg, Yg, meta4, M); break;
     default: fail(S2B_ERR_RUNTIME, "x-major streaming engine: unsupported variant");
     }
 }
@@ -515,10 +936,10 @@ void xs_transpose_paths(s2b_context* ctx, const double* S0, const double* S1, do
 }
 
 void xs_records(s2b_context* ctx, const int* cnt, const int4* recq, const double* S0, const double* S1,
-                double* const* rec, int nx, int nv, size_t M) {
+                const double* S2, double* const* rec, int nx, int nv, size_t M) {
     dim3 grid(static_cast<unsigned>(nv / 32), static_cast<unsigned>(nx / 32),
               static_cast<unsigned>(std::min<size_t>(std::max<size_t>(M, 1), 64)));
-    xs_record_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(cnt, recq, S0, S1, rec, nx, nv);
+    xs_record_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(cnt, recq, S0, S1, S2, rec, nx, nv);
     S2B_LAUNCHED(ctx);
 }
 

@@ -110,9 +110,12 @@ def main():
             s["algorithmic_bytes"] = 16.0 * n * paths * steps
             s["traffic_over_algorithmic"] = traffic / s["algorithmic_bytes"]
         elif stream:
+            # term_xs2_kernel applies two Taylor terms per launch: 40 B per two terms by design
+            tpl = 2 if name.startswith("xs2") else 1
             s["live_paths_in_pass"] = live
-            s["dram_bytes_per_path_term"] = traffic / live
-            s["algorithmic_bytes"] = 32.0 * n * live
+            s["terms_per_launch"] = tpl
+            s["dram_bytes_per_path_term"] = traffic / live / tpl
+            s["algorithmic_bytes"] = (40.0 if tpl == 2 else 32.0) * n * live
             s["traffic_over_algorithmic"] = traffic / s["algorithmic_bytes"]
         else:
             cl = paths - hyb

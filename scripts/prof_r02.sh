@@ -14,7 +14,8 @@ CMD[tma_hybrid512]="$B --config cfg4 --paths 560 --T 0.01";     KERN[tma_hybrid5
 CMD[var_cfg3]="$B --config cfg3 --paths 1184 --T 0.02";         KERN[var_cfg3]="term_var_kernel"; SKIP[var_cfg3]=40
 CMD[varx_cfg3k]="$B --config cfg3k --paths 1184 --T 0.02";      KERN[varx_cfg3k]="term_varx_kernel"; SKIP[varx_cfg3k]=40
 CMD[tma_cfg5]="$B --config cfg5 --paths 296 --T 0.001";         KERN[tma_cfg5]="term_tma_kernel"; SKIP[tma_cfg5]=40
-CMD[xs_cfg5]="$B --config cfg5 --paths 296 --T 0.001";          KERN[xs_cfg5]="term_xs_kernel"; SKIP[xs_cfg5]=40
+CMD[xs_cfg5]="env S2B_XS2=0 $B --config cfg5 --paths 296 --T 0.001";          KERN[xs_cfg5]="term_xs_kernel"; SKIP[xs_cfg5]=40
+CMD[xs2_cfg5]="$B --config cfg5 --paths 296 --T 0.001"; KERN[xs2_cfg5]="term_xs2_kernel"; SKIP[xs2_cfg5]=20
 CMD[varx_cfg5var]="$B --config cfg5 --family langevin-variable --paths 296 --T 0.001"; KERN[varx_cfg5var]="term_varx_kernel"; SKIP[varx_cfg5var]=40
 # E-M: the timed solve_euler of the bench's E-M leg (the warm-up solve is launch 0)
 CMD[em_cfg2]="$B --paths 288 --euler-steps 40";                 KERN[em_cfg2]="em_cluster_ip_kernel"; SKIP[em_cfg2]=1

@@ -1,0 +1,5 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-.}"
+timeout 1500 python -m pytest tests/test_gpu_xs.py tests/test_gpu_stress.py -q -x -k "xs" > gpurun_out/xs_tests.log 2>&1
+echo "tests rc=$?"; tail -3 gpurun_out/xs_tests.log
+bash scripts/xs_ab.sh "S2B_XS2=0" "S2B_XS2=1"
