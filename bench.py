@@ -36,7 +36,7 @@ ENGINES = {
     3: {"name": "cluster-xmi", "kernel": "cluster_xmi_kernel", "profile": "xmi_kernel_ncu.json",
         "note": "cluster-resident in-place x-march (16-CTA clusters, accumulator in L2): achieved is the "
                 "streaming-equivalent rate, traffic the real DRAM bytes; bound by the fp64 pipe; by default "
-                "20% of the paths run on the streaming engine on the idle SMs (S2B_HYBRID)"},
+                "25% of the paths run on the streaming x-march engine (term_xs_kernel) on the idle SMs (S2B_HYBRID)"},
     0: {"name": "stream", "kernel": "term_tma_kernel", "profile": "term_kernel_ncu.json",
         "note": "streaming pass engine: term and accumulator round-trip HBM every Taylor term (constant "
                 "Langevin on grids >= 256 columns: the x-march term_xs2_kernel, x-major tiles by TMA, TWO "
@@ -48,7 +48,7 @@ ENGINES = {
     2: {"name": "cluster-xm", "kernel": "cluster_xm_kernel", "profile": "xm_kernel_ncu.json",
         "note": "cluster-resident x-march: the path stays in shared memory for the window; achieved is "
                 "the streaming-equivalent rate (can exceed HBM peak), traffic the real DRAM bytes; the "
-                "binding limit is the fp64 pipe (compute_roofline); by default 12% of the paths run on "
+                "binding limit is the fp64 pipe (compute_roofline); by default 16% of the paths run on "
                 "the streaming engine concurrently, on the SMs the 8-CTA clusters leave idle (S2B_HYBRID)"},
 }
 
@@ -160,8 +160,8 @@ PROFILE_OF = {
     ("cfg3k", "kinetic-variable", "stream"): "r02_term_varx_cfg3k_ncu.json",
     ("cfg5", "langevin-constant", "stream"): "r02_term_xs2_cfg5_ncu.json",
     ("cfg5", "langevin-variable", "stream"): "r02_term_varx_cfg5var_ncu.json",
-    ("hybrid", 256): "r02_term_tma_hybrid256_ncu.json",
-    ("hybrid", 512): "r02_term_tma_hybrid512_ncu.json",
+    ("hybrid", 256): "r02_term_xs_hybrid256_ncu.json",
+    ("hybrid", 512): "r02_term_xs_hybrid512_ncu.json",
 }
 # E-M captures (scripts/prof_r02.sh em_*): per (preset, kernel) of the bench's E-M leg
 EM_PROFILE_OF = {("cfg2", "em_cluster_ip_kernel"): "r02_em_cluster_ip_cfg2_ncu.json",

@@ -878,6 +878,7 @@ struct MagnusSession {
     bool finished = false;         // finish() moved the buffers out: every later call is refused
     // streaming x-march engine (term_xs.cu): T/S are x-major while its pass loop runs
     bool use_xs = false;
+    bool xs_slice = false; // the hybrid run's streaming slice on the x-march engine
     bool xs_major = false;
     DevBuf<double> yg;   // the window's folded Y rows per path
     DevBuf<int4> xs_meta; // per live path of a pass: (path, k, parity, segments)
@@ -1151,6 +1152,7 @@ MagnusSession* session_create(s2b_context* ctx, const s2b_operator* op, const s2
                             cluster_engine_supported(op->variant, static_cast<int>(op->nx), static_cast<int>(op->nv));
             s->use_cluster = ok && !(eng && std::strcmp(eng, "stream") == 0);
             s->use_xs = !s->use_cluster && term_xs_supported(op);
+            s->xs_slice = s->use_cluster && term_xs_slice_supported(op);
             if (s->use_cluster && cluster_xmi_supported(op->variant, static_cast<int>(op->nx), static_cast<int>(op->nv)))
                 s->sx.alloc(cluster_xmi_scratch(static_cast<int>(op->nx), static_cast<int>(op->nv), &s->sx_slots));
         }
@@ -1258,8 +1260,13 @@ void prepare_windows(MagnusSession* s, size_t w0, size_t w1) {
 // x-major <-> row-major for the streaming x-march engine: every path's current accumulator
 // S[par[p]][p] is transposed into T[par[p]][p] (the term buffers are dead at a window boundary),
 // then the S and T buffers trade places.
-void xs_relayout(MagnusSession* s, bool to_xmajor) {
+void xs_relayout(MagnusSession* s, bool to_xmajor, int p_lo = 0) {
     const int nx = static_cast<int>(s->op->nx), nv = static_cast<int>(s->op->nv);
+    if (p_lo > 0) { // a hybrid slice: the cluster kernel owns paths [0, p_lo) of the same buffers
+        xs_transpose_paths_inplace(s->ctx, s->S[0].p, s->S[1].p, s->iv.p + 5 * s->M, p_lo, s->M, nx);
+        s->xs_major = to_xmajor;
+        return;
+    }
     xs_transpose_paths(s->ctx, s->S[0].p, s->S[1].p, s->T[0].p, s->T[1].p, s->iv.p + 5 * s->M, s->M,
                        to_xmajor ? nv : nx, to_xmajor ? nx : nv);
     std::swap(s->S[0].p, s->T[0].p);
@@ -1268,11 +1275,11 @@ void xs_relayout(MagnusSession* s, bool to_xmajor) {
 }
 
 void stream_loop(MagnusSession* s, int stop, int p_lo) {
-    const bool xs = s->use_xs && p_lo == 0;
+    const bool xs = p_lo == 0 ? s->use_xs : s->xs_slice;
     if (xs) {
         if (!s->yg.p) s->yg.alloc(term_xs_y_doubles(s->op, s->M));
         if (!s->xs_meta.p) s->xs_meta.alloc(s->M);
-        xs_relayout(s, true);
+        xs_relayout(s, true, p_lo);
     }
     {
         // (re)activate every live path at the current window boundary; window 0 also
@@ -1302,7 +1309,7 @@ void stream_loop(MagnusSession* s, int stop, int p_lo) {
         }
         chunk = std::min(chunk * 2, 64);
     }
-    if (xs) xs_relayout(s, false);
+    if (xs) xs_relayout(s, false, p_lo);
 }
 
 // The two-term streaming engine over paths [p_lo, M): two Taylor terms of every live path per
@@ -1375,8 +1382,12 @@ double hybrid_fraction(const MagnusSession* s) {
     const char* e = std::getenv("S2B_HYBRID");
     if (e) return std::atof(e);
     const int v = s->op->variant, nx = static_cast<int>(s->op->nx), nv = static_cast<int>(s->op->nv);
-    if (cluster_xm_supported(v, nx, nv)) return nx == 256 ? 0.12 : (nx == 128 ? 0.06 : 0.0); // 120 / 132 / 148 SMs busy
-    if (cluster_xmi_supported(v, nx, nv)) return 0.20;
+    // the x-march streaming slice (term_xs_kernel) is 1.2-1.45x term_tma_kernel per SM, so it takes a
+    // larger share: cfg2 1.375e9 (tma, 0.12) -> 1.485e9 windows/s (xs, 0.16), cfg4 6.48e8 (tma,
+    // 0.20) -> 7.04e8 (xs, 0.25), same run (scripts/xs_hybrid.sh)
+    if (cluster_xm_supported(v, nx, nv))
+        return nx == 256 ? (s->xs_slice ? 0.16 : 0.12) : (nx == 128 ? 0.06 : 0.0); // 120 / 132 / 148 SMs busy
+    if (cluster_xmi_supported(v, nx, nv)) return s->xs_slice ? 0.25 : 0.20;
     return 0.0;
 }
 

@@ -297,6 +297,9 @@ void launch_term_xs(s2b_context* ctx, const s2b_operator* op, const TermArgs& a,
                     int4* meta4, size_t M, bool nz);
 void xs_transpose_paths(s2b_context* ctx, const double* S0, const double* S1, double* T0, double* T1,
                         const int* par, size_t M, int R, int C);
+void xs_transpose_paths_inplace(s2b_context* ctx, double* S0, double* S1, const int* par, size_t p_lo, size_t M,
+                                int d);
+bool term_xs_slice_supported(const s2b_operator* op);
 void xs_records(s2b_context* ctx, const int* cnt, const int4* recq, const double* S0, const double* S1,
                 const double* S2, double* const* rec, int nx, int nv, size_t M);
 // two Taylor terms per pass (term_xs2_kernel, term2's buffer protocol; default, S2B_XS2=0 disables)

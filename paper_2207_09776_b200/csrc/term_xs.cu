@@ -725,6 +725,34 @@ __global__ void xs_transpose_kernel(const double* __restrict__ s0, const double*
     }
 }
 
+// in-place transpose of paths [p_lo, M) of square d x d states S[par[p]][p] (its own inverse):
+// block (bi, bj), bi <= bj, swaps the transposed 32 x 32 tiles (bi, bj) and (bj, bi)
+__global__ void xs_transpose_inplace_kernel(double* __restrict__ s0, double* __restrict__ s1,
+                                            const int* __restrict__ par, int d, size_t p_lo, size_t M) {
+    __shared__ double ta[32][33], tb[32][33];
+    const int T = d / 32;
+    int bi = 0, rem = blockIdx.x; // pair index -> (bi, bj), bj >= bi
+    while (rem >= T - bi) {
+        rem -= T - bi;
+        ++bi;
+    }
+    const int bj = bi + rem;
+    const size_t n = static_cast<size_t>(d) * d;
+    for (size_t p = p_lo + blockIdx.z; p < M; p += gridDim.z) {
+        double* m = (par[p] ? s1 : s0) + p * n;
+        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+            ta[k][threadIdx.x] = m[static_cast<size_t>(bi * 32 + k) * d + bj * 32 + threadIdx.x];
+            tb[k][threadIdx.x] = m[static_cast<size_t>(bj * 32 + k) * d + bi * 32 + threadIdx.x];
+        }
+        __syncthreads();
+        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+            m[static_cast<size_t>(bi * 32 + k) * d + bj * 32 + threadIdx.x] = tb[threadIdx.x][k];
+            m[static_cast<size_t>(bj * 32 + k) * d + bi * 32 + threadIdx.x] = ta[threadIdx.x][k];
+        }
+        __syncthreads();
+    }
+}
+
 // queued record snapshots S[par][p] (x-major) -> rec[r][p] (row-major), as record_kernel
 __global__ void xs_record_kernel(const int* __restrict__ cnt, const int4* __restrict__ recq,
                                  const double* __restrict__ S0, const double* __restrict__ S1,
@@ -832,12 +860,18 @@ void launch_xs_v(s2b_context* ctx, const TermArgs& a, const int* seg, double* Yg
     for (int i = 0; i < 4; ++i) encode_xmaj(&maps.t[i], tb[i], M, nx, nv, L::TR, L::TX);
     encode_xmaj(&maps.s[0], a.S0, M, nx, nv, kXsRows, kCW);
     encode_xmaj(&maps.s[1], a.S1, M, nx, nv, kXsRows, kCW);
-    auto kern = nv == 1024 ? term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 1024> : term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 0>;
+    // compile-time column heights of the benchmark grids (immediate store offsets): 1024^2 and the
+    // hybrid slices at 256^2 / 512^2
+    const int nvc = nv == 1024 ? 3 : nv == 512 ? 2 : nv == 256 ? 1 : 0;
+    auto kern = nvc == 3   ? term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 1024>
+                : nvc == 2 ? term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 512>
+                : nvc == 1 ? term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 256>
+                           : term_xs_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 0>;
     const size_t smem = L::bytes();
-    static int configured_device[2] = {-1, -1};
-    if (configured_device[nv == 1024] != ctx->device) {
+    static int configured_device[4] = {-1, -1, -1, -1};
+    if (configured_device[nvc] != ctx->device) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured_device[nv == 1024] = ctx->device;
+        configured_device[nvc] = ctx->device;
     }
     const int nrb = nv / kXsRows, nxt = nx / kCW;
     const size_t work = M * static_cast<size_t>(nrb);
@@ -933,6 +967,24 @@ void xs_transpose_paths(s2b_context* ctx, const double* S0, const double* S1, do
               static_cast<unsigned>(std::min<size_t>(M, 65535)));
     xs_transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(S0, S1, T0, T1, par, R, C, M);
     S2B_LAUNCHED(ctx);
+}
+
+void xs_transpose_paths_inplace(s2b_context* ctx, double* S0, double* S1, const int* par, size_t p_lo, size_t M,
+                                int d) {
+    if (M <= p_lo) return;
+    const int T = d / 32;
+    dim3 grid(static_cast<unsigned>(T * (T + 1) / 2), 1, static_cast<unsigned>(std::min<size_t>(M - p_lo, 65535)));
+    xs_transpose_inplace_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(S0, S1, par, d, p_lo, M);
+    S2B_LAUNCHED(ctx);
+}
+
+// the x-march engine for the streaming slice of a hybrid run (paths the cluster engine leaves
+// to the idle SMs): square grids only (the slice is relaid out in place); S2B_XS_SLICE=0 keeps
+// term_tma_kernel there
+bool term_xs_slice_supported(const s2b_operator* op) {
+    const char* e = std::getenv("S2B_XS_SLICE");
+    if (e && e[0] == '0') return false;
+    return term_xs_supported(op) && op->nx == op->nv;
 }
 
 void xs_records(s2b_context* ctx, const int* cnt, const int4* recq, const double* S0, const double* S1,

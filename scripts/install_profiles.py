@@ -10,7 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = {"xm_cfg2": "r02_xm_cfg2_ncu.json", "xm_cfg1": "r02_xm_cfg1_ncu.json", "xmi_cfg4": "r02_xmi_cfg4_ncu.json",
          "var_cfg3": "r02_term_var_cfg3_ncu.json", "varx_cfg3k": "r02_term_varx_cfg3k_ncu.json",
          "tma_cfg5": "r02_term_tma_cfg5_ncu.json", "xs_cfg5": "r02_term_xs_cfg5_ncu.json", "xs2_cfg5": "r02_term_xs2_cfg5_ncu.json", "varx_cfg5var": "r02_term_varx_cfg5var_ncu.json",
-         "tma_hybrid256": "r02_term_tma_hybrid256_ncu.json", "tma_hybrid512": "r02_term_tma_hybrid512_ncu.json",
+         "tma_hybrid256": "r02_term_tma_hybrid256_ncu.json", "xs_hybrid256": "r02_term_xs_hybrid256_ncu.json",
+         "xs_hybrid512": "r02_term_xs_hybrid512_ncu.json", "tma_hybrid512": "r02_term_tma_hybrid512_ncu.json",
          "em_cfg2": "r02_em_cluster_ip_cfg2_ncu.json", "em_cfg5": "r02_em_tb_cfg5_ncu.json"}
 for name in sys.argv[1:] or NAMES:
     src = os.path.join(ROOT, "gpurun_out", f"ncu_{name}.json")

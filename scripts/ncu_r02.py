@@ -51,7 +51,7 @@ def main():
         traffic = f("dram__bytes_read.sum") + f("dram__bytes_write.sum")
         dur = f("gpu__time_duration.sum")
         stream = name.startswith(("tma", "var", "xs"))
-        live = (hyb if name.startswith("tma_hybrid") else paths)
+        live = (hyb if "_hybrid" in name else paths)
         stalls = {k[34:-23]: float(v[0]) for k, v in d.items()
                   if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")}
         src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],

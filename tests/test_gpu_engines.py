@@ -169,8 +169,9 @@ def test_engines_blowup_exits_512(ref, s2b, ctx, engine512):
     assert np.array_equal(ens[-1].status, wst[-1]) and ens[-1].blowup_count() == M
 
 
+@pytest.mark.parametrize("slice_engine", ["xs", "tma"])
 @pytest.mark.parametrize("d", [256, 512])
-def test_hybrid_split_bitwise(s2b, ctx, monkeypatch, d):
+def test_hybrid_split_bitwise(s2b, ctx, monkeypatch, d, slice_engine):
     """S2B_HYBRID: a slice of the paths runs on the streaming engine beside the cluster kernel
     (on the SMs the clusters leave idle); every path's result is unchanged."""
     T, dt, dt_leb, M = 0.02, 0.01, 1e-3, 96
@@ -179,6 +180,7 @@ def test_hybrid_split_bitwise(s2b, ctx, monkeypatch, d):
     paths = s2b.BrownianPaths.philox(T, dt_leb, M, seed=23, ctx=ctx)
     phi = s2b.gaussian_datum(g)
     cfg = s2b.MagnusConfig(order=3, dt=dt, record_times=[0.01])
+    monkeypatch.setenv("S2B_XS_SLICE", "1" if slice_engine == "xs" else "0")
     monkeypatch.setenv("S2B_HYBRID", "0")
     want = s2b.solve_iterated_magnus(cfg, op, phi, paths, T, g)
     monkeypatch.setenv("S2B_HYBRID", "0.3")
