@@ -4,7 +4,7 @@
 # (summarised on the box by scripts/ncu_r02.py; install here with scripts/install_profiles.py
 # and scripts/summarize_r02.py).
 mkdir -p gpurun_out
-python -m pytest tests -q -m gpu 2>&1 | tail -6 > gpurun_out/pytest_gpu.log
+python -m pytest tests -q -m gpu 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 python bench.py > gpurun_out/bench_default.log 2>&1
 for c in cfg1 cfg3 cfg3k cfg4 cfg5; do python bench.py --config $c > gpurun_out/bench_$c.log 2>&1; done
