@@ -489,6 +489,13 @@ def magnus_leg(a, s2b, ctx, torch, stream, dist, local, world, rank, keep_sessio
             "hybrid_paths": hyb, "note": engine["note"]}
     if stale:
         roof["profile_kernel"] = prof.get("kernel_mangled") or prof.get("kernel")
+    if engine["kernel"] == "term_xs2_kernel":
+        # the two-term kernel's own algorithmic bytes: t_{k-1}, s_{k-1} in, t_{k+1}, s_{k+1}, s_k out
+        # per two terms (20 B per term); the streaming-equivalent frac above counts 32 B per term
+        kb = 20.0 * n * terms
+        roof["kernel_bytes_model"] = "40 B per two path*gridpoint*terms (term_xs2_kernel)"
+        roof["kernel_bytes_achieved"] = kb / (tk_ms / 1e3) / 1e9 if tk_ms > 0 else 0.0
+        roof["kernel_bytes_frac"] = roof["kernel_bytes_achieved"] / peak
     out = {"value": value, "ms_max": ms_max, "terms": terms, "roofline": roof, "compute_roofline": compute,
            "clocks": clk, "launches": launches, "n": n, "M": M, "nwin": nwin, "win": a.warmup + a.steps}
     if keep_session:
