@@ -1,6 +1,7 @@
 """Engine coverage at the benchmark grid (256 x 256): every Magnus engine — the x-march
 cluster kernel (default for constant Langevin), the row-band cluster kernel (S2B_XM=0) and
-the streaming pass engine (S2B_ENGINE=stream) — against the reference CPU solver on
+the streaming pass engines (S2B_ENGINE=stream: the x-march kernels with two terms per pass
+and, S2B_XS2=0, one; S2B_XS=0: the row-march kernel) — against the reference CPU solver on
 identical increments, bit for bit, including the blow-up exits (norm cap, non-finite
 terms, exhausted Taylor budget) and record snapshots."""
 import os
@@ -13,6 +14,7 @@ from test_gpu_parity import gpu_magnus
 pytestmark = pytest.mark.gpu
 
 ENGINES = {"xm": {}, "band": {"S2B_XM": "0"}, "stream": {"S2B_ENGINE": "stream"},
+           "stream-xs1": {"S2B_ENGINE": "stream", "S2B_XS2": "0"},
            "stream-tma": {"S2B_ENGINE": "stream", "S2B_XS": "0"}}
 
 
@@ -61,7 +63,7 @@ def test_xm_stopping_rule_tolerances(ref, s2b, ctx, engine, d, tol):
     assert stats["engine"] == 2
 
 
-@pytest.mark.parametrize("engine", ["xm", "band", "stream", "stream-tma"], indirect=True)
+@pytest.mark.parametrize("engine", ["xm", "band", "stream", "stream-xs1", "stream-tma"], indirect=True)
 def test_engines_blowup_exits_256(ref, s2b, ctx, engine):
     d, T, dt, dt_leb, M = 256, 0.02, 0.01, 1e-3, 2
     # window norm cap
