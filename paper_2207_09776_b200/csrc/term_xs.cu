@@ -394,23 +394,32 @@ __global__ void __launch_bounds__(kXsNT, 1)
 constexpr int kX2Out = 28; // output rows per item
 constexpr int kX2Stages = 2;
 
-template <int KRX, int KRV, uint64_t MASK, uint32_t BM>
+// H = false: 28 output rows per item, lanes 0, 1, 30, 31 compute t_k's halo rows (idle in
+// phase 2).  H = true: 32 output rows per item (every lane owns its row in both phases); the 4
+// halo rows of t_k are computed by a 2-point march per lane (lanes = 4 rows x 8 column pairs of
+// the warp's 16 columns).  Row strides 42 / 38 (not 40 / 36) keep those lanes' shared-memory
+// accesses at most 2-way conflicted.
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, bool H>
 struct Xs2Layout {
     static constexpr int NBM = MaskInfo<MASK>::count();
     static constexpr int NBB = popc32x(BM);
     static constexpr int YW = (NBM + 4 * NBB) | 1;
-    static constexpr int TR = 36;               // input rows v0-4 .. v0+32
-    static constexpr int TX = kCW + 6;          // input columns jW-2 .. jW+W+4
-    static constexpr int SR = kX2Out;           // s_{k-1} rows v0 .. v0+28
-    static constexpr int SX = kCW + 2;          // s_{k-1} columns jW .. jW+W+2
-    static constexpr int KX = kCW + 4;          // t_k columns jW-2 .. jW+W+2
+    static constexpr int OUT = H ? 32 : kX2Out;   // output rows per item
+    static constexpr int RO = H ? 0 : -2;         // lane r is row v0 + RO + r
+    static constexpr int TR = H ? 42 : 36;        // input rows from v0-4 (H uses 40)
+    static constexpr int TX = kCW + 6;            // input columns jW-2 .. jW+W+4
+    static constexpr int SR = OUT;                // s_{k-1} rows v0 .. v0+OUT
+    static constexpr int SX = kCW + 2;            // s_{k-1} columns jW .. jW+W+2
+    static constexpr int KX = kCW + 4;            // t_k columns jW-2 .. jW+W+2
+    static constexpr int KR = H ? 38 : 32;        // t_k column stride (rows from v0-2; H uses 36)
+    static constexpr int YR = H ? 36 : 32;        // Y rows per item, from v0-2
     static constexpr int TBYTES = TR * TX * 8;
     static constexpr int SBYTES = SR * SX * 8;
-    static constexpr int YBYTES = 32 * YW * 8;
+    static constexpr int YBYTES = YR * YW * 8;
     static constexpr int SOFF = (TBYTES + 127) / 128 * 128;
     static constexpr int STAGE = SOFF + (SBYTES + 127) / 128 * 128;
     static constexpr int KOFF = kX2Stages * STAGE;
-    static constexpr int YOFF = KOFF + KX * 32 * 8;
+    static constexpr int YOFF = KOFF + (KX * KR * 8 + 127) / 128 * 128;
     static constexpr int YSTR = (YBYTES + 127) / 128 * 128;
     static constexpr int BAROFF = YOFF + 2 * YSTR;
     static constexpr size_t bytes() { return 128 + BAROFF + 64; }
@@ -491,12 +500,12 @@ struct Xs2Maps {
     CUtensorMap s[3];
 };
 
-template <int KRX, int KRV, uint64_t MASK, uint32_t BM, bool NZ, int NVC>
+template <int KRX, int KRV, uint64_t MASK, uint32_t BM, bool NZ, int NVC, bool H>
 __global__ void __launch_bounds__(kXsNT, 1)
     term_xs2_kernel(const __grid_constant__ Xs2Maps maps, TermArgs a, Term2Args b, const double* __restrict__ Yg,
                     int yrows, const int4* __restrict__ meta4, int nrb, int nxt) {
-    using L = Xs2Layout<KRX, KRV, MASK, BM>;
-    constexpr int NBM = L::NBM, YW = L::YW;
+    using L = Xs2Layout<KRX, KRV, MASK, BM, H>;
+    constexpr int NBM = L::NBM, YW = L::YW, KR = L::KR, SR = L::SR, RO = L::RO;
     constexpr int NW = kXsNT / 32;
     constexpr int LX = kCW / NW;
     static_assert(LX == 16, "16 columns per warp");
@@ -509,12 +518,12 @@ __global__ void __launch_bounds__(kXsNT, 1)
     const uint32_t base_u = (smem_u32(smem_raw) + 127u) & ~127u;
     unsigned char* base = smem_raw + (base_u - smem_u32(smem_raw));
     const uint32_t full_u = base_u + L::BAROFF;
-    double* TK = reinterpret_cast<double*>(base + L::KOFF); // [KX][32]
+    double* TK = reinterpret_cast<double*>(base + L::KOFF); // [KX][KR]
     __shared__ unsigned long long red[2][4][NW];
     __shared__ int meta[kX2Stages][3];  // path, accumulator index, term parity
     __shared__ double minv[kX2Stages][2];
 
-    for (int q = t; q < L::KX * 32; q += kXsNT) TK[q] = 0.0;
+    for (int q = t; q < L::KX * KR; q += kXsNT) TK[q] = 0.0;
     if (t == 0) {
         for (int s = 0; s < kX2Stages; ++s) mbar_init(reinterpret_cast<uint64_t*>(base + L::BAROFF) + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(kXsNT, 1)
         }
         const long long wi = blockIdx.x + it * gridDim.x;
         const int p = cur_m.x, kk = cur_m.y, sidx = cur_m.z & 3, tp = cur_m.z >> 2;
-        const int v0 = static_cast<int>(wi % nrb) * kX2Out;
+        const int v0 = static_cast<int>(wi % nrb) * L::OUT;
         const int slot = static_cast<int>(g % kX2Stages);
         meta[slot][0] = p;
         meta[slot][1] = sidx;
@@ -553,7 +562,7 @@ __global__ void __launch_bounds__(kXsNT, 1)
         // term k-1: the accumulator itself at a segment's first term (term = accum = y)
         tma_tile3(st, &maps.t[kk == 1 ? 2 + sidx : tp], v0 - 4, tile * kCW - 2, p, bar);
         tma_tile3(st + L::SOFF, &maps.s[sidx], v0, tile * kCW, p, bar);
-        if (tile == 0) // Y rows v0-2 .. v0+30 (padded layout: row v at index v + 2)
+        if (tile == 0) // Y rows v0-2 .. v0-2+YR (padded layout: row v at index v + 2)
             tma_row_u(base_u + L::YOFF + static_cast<uint32_t>(it & 1) * L::YSTR,
                       Yg + (static_cast<size_t>(p) * yrows + static_cast<size_t>(v0)) * YW, L::YBYTES, bar);
     };
@@ -580,10 +589,10 @@ __global__ void __launch_bounds__(kXsNT, 1)
             const long long wi = blockIdx.x + it * gridDim.x;
             p = meta[slot][0];
             const int sidx = meta[slot][1], tp = meta[slot][2];
-            v0 = static_cast<int>(wi % nrb) * kX2Out;
-            const int vr = v0 - 2 + lane;
+            v0 = static_cast<int>(wi % nrb) * L::OUT;
+            const int vr = v0 + RO + lane;
             rowok = vr >= 0 && vr < nv;
-            own = lane >= 2 && lane < 2 + kX2Out && vr < nv;
+            own = (H || (lane >= 2 && lane < 2 + kX2Out)) && vr < nv;
             inv1 = minv[slot][0];
             inv2 = minv[slot][1];
             const size_t pbase = static_cast<size_t>(p) * n;
@@ -592,15 +601,17 @@ __global__ void __launch_bounds__(kXsNT, 1)
             Sa = (sidx == 0 ? a.S1 : sidx == 1 ? S2 : a.S0) + pbase;
             Sb = (sidx == 0 ? S2 : sidx == 1 ? a.S0 : a.S1) + pbase;
 #pragma unroll
-            for (int e = 0; e < NBM; ++e) y[e] = ybuf[lane * YW + e];
+            for (int e = 0; e < NBM; ++e) y[e] = ybuf[(lane + RO + 2) * YW + e];
             tm1 = sm1 = tm2 = sm2 = 0;
         }
-        const double* yb = ybuf + lane * YW + NBM;
+        const double* yb = ybuf + (lane + RO + 2) * YW + NBM;
         const double* tt = reinterpret_cast<const double*>(base + slot * L::STAGE);
         const double* ts = reinterpret_cast<const double*>(base + slot * L::STAGE + L::SOFF);
         const int jW = tile * kCW;
-        const int vr = v0 - 2 + lane;
+        const int vr = v0 + RO + lane;
         const size_t vo = static_cast<size_t>(vr);
+        const int kr = lane + RO + 2; // this lane's row in the t_k buffer
+        const int sr = lane + RO;     // ... in the s_{k-1} tile
 
         // Every warp runs ONE unrolled march per phase over its 16 columns; the x-boundary
         // columns (other Y classes) and the two columns past the grid are masked out of that
@@ -616,30 +627,54 @@ __global__ void __launch_bounds__(kXsNT, 1)
             auto epi1 = [&](int x, double acc, bool keep) {
                 double tv = acc * inv1;
                 tv = rowok ? tv : 0.0;
-                TK[(x - jW + 2) * 32 + lane] = tv;
-                const double sv = ts[(x - jW) * kX2Out + (lane - 2)] + tv;
+                TK[(x - jW + 2) * KR + kr] = tv;
+                const double sv = ts[(x - jW) * SR + sr] + tv;
                 const bool w = own && keep;
                 st_if(sbw + (x - xa) * nv, sv, w);
                 tm1 = umax64(tm1, w ? abs_bits(tv) : 0ull);
                 sm1 = umax64(sm1, w ? abs_bits(sv) : 0ull);
             };
-            const double* tin = tt + (xa - jW + 2) * L::TR + (lane + 2);
+            const double* tin = tt + (xa - jW + 2) * L::TR + (lane + RO + 4);
             xs_march<KRX, KRV, MASK, BM, NZ, L::TR, LX, 0, -1>(tin, y, yb,
                                                                [&](int i, double acc) { epi1(xa + i, acc, i < hi1); });
             if (edge_l) // columns 0, 1: classes 0, 1
-                xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 2, -1>(tt + 2 * L::TR + (lane + 2), y, yb,
+                xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 2, -1>(tt + 2 * L::TR + (lane + RO + 4), y, yb,
                                                                    [&](int i, double acc) { epi1(i, acc, true); });
             if (edge_r) { // columns nx-2, nx-1: classes 3, 4; nx, nx+1 are outside the grid (zero)
                 xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 0, 0>(tin + (LX - 4) * L::TR, y, yb,
                                                                   [&](int i, double acc) { epi1(xa + LX - 4 + i, acc, true); });
-                TK[(xa + LX - 2 - jW + 2) * 32 + lane] = 0.0;
-                TK[(xa + LX - 1 - jW + 2) * 32 + lane] = 0.0;
+                TK[(xa + LX - 2 - jW + 2) * KR + kr] = 0.0;
+                TK[(xa + LX - 1 - jW + 2) * KR + kr] = 0.0;
+            }
+            if constexpr (H) {
+                // t_k's halo rows v0-2, v0-1, v0+32, v0+33 over the warp's 16 columns: lane =
+                // (row h, column pair c); Y of that row read from shared memory
+                const int h = lane >> 3, c = lane & 7;
+                const int hr = h < 2 ? h : 32 + h; // row in the t_k buffer (v0 - 2 + hr)
+                const int vh = v0 - 2 + hr;
+                const bool hok = vh >= 0 && vh < nv;
+                const double* yh = ybuf + hr * YW;
+                const int xh = xa + 2 * c;
+                const double* tinh = tt + (xh - jW + 2) * L::TR + (hr + 2);
+                auto epih = [&](int x, double acc, bool keep) {
+                    const double tv = acc * inv1;
+                    TK[(x - jW + 2) * KR + hr] = hok && keep ? tv : 0.0;
+                };
+                if (edge_r && c == 6) // columns nx-2, nx-1
+                    xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 0, 0>(tinh, yh, yh + NBM,
+                                                                      [&](int i, double acc) { epih(xh + i, acc, true); });
+                else // (edge_r, c == 7: columns nx, nx+1 are outside the grid)
+                    xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 0, -1>(
+                        tinh, yh, yh + NBM, [&](int i, double acc) { epih(xh + i, acc, !(edge_r && c == 7)); });
+                if (edge_l && c == 0) // columns 0, 1
+                    xs_march<KRX, KRV, MASK, BM, NZ, L::TR, 2, 2, -1>(tt + 2 * L::TR + (hr + 2), yh, yh + NBM,
+                                                                       [&](int i, double acc) { epih(i, acc, true); });
             }
         }
         __syncthreads(); // t_k of the tile (+ the carried columns) complete
         // the 4 t_k columns the next tile needs on its left: read now, placed after the barrier
         double carry = 0.0;
-        if (t < 128) carry = TK[(kCW + t / 32) * 32 + (t & 31)];
+        if (t < 4 * KR) carry = TK[kCW * KR + t];
 
         // ---- phase 2: t_{k+1}, s_{k+1} over [jW, jW+W) on lanes 2..29
         {
@@ -649,8 +684,8 @@ __global__ void __launch_bounds__(kXsNT, 1)
             double* const tnw = Tn + cw;
             double* const saw = Sa + cw;
             auto epi2 = [&](int x, double acc, bool keep) {
-                const double tk = TK[(x - jW + 2) * 32 + lane];
-                const double sk = ts[(x - jW) * kX2Out + (lane - 2)] + tk;
+                const double tk = TK[(x - jW + 2) * KR + kr];
+                const double sk = ts[(x - jW) * SR + sr] + tk;
                 const double tv = acc * inv2;
                 const double sv = sk + tv;
                 const bool w = own && keep;
@@ -659,15 +694,15 @@ __global__ void __launch_bounds__(kXsNT, 1)
                 tm2 = umax64(tm2, w ? abs_bits(tv) : 0ull);
                 sm2 = umax64(sm2, w ? abs_bits(sv) : 0ull);
             };
-            const double* tin = TK + (xa - jW + 2) * 32 + lane;
-            xs_march<KRX, KRV, MASK, BM, NZ, 32, LX, 0, -1>(
+            const double* tin = TK + (xa - jW + 2) * KR + kr;
+            xs_march<KRX, KRV, MASK, BM, NZ, KR, LX, 0, -1>(
                 tin, y, yb, [&](int i, double acc) { epi2(xa + i, acc, i >= lo2 && i < hi2); });
             if (edge_l)
-                xs_march<KRX, KRV, MASK, BM, NZ, 32, 2, 2, -1>(tin, y, yb,
+                xs_march<KRX, KRV, MASK, BM, NZ, KR, 2, 2, -1>(tin, y, yb,
                                                                 [&](int i, double acc) { epi2(xa + i, acc, true); });
             if (edge_r)
-                xs_march<KRX, KRV, MASK, BM, NZ, 32, 2, 0, 0>(
-                    tin + (LX - 2) * 32, y, yb, [&](int i, double acc) { epi2(xa + LX - 2 + i, acc, true); });
+                xs_march<KRX, KRV, MASK, BM, NZ, KR, 2, 0, 0>(
+                    tin + (LX - 2) * KR, y, yb, [&](int i, double acc) { epi2(xa + LX - 2 + i, acc, true); });
         }
 
         const bool last = tile == nxt - 1;
@@ -681,10 +716,10 @@ __global__ void __launch_bounds__(kXsNT, 1)
             }
         }
         __syncthreads(); // the stage and TK are consumed
-        if (t < 128) { // next tile of this item: carry; first tile of an item: columns -2, -1 are zero
+        if (t < 4 * KR) { // next tile of this item: carry; first tile of an item: columns -2, -1 are zero
             if (!last)
                 TK[t] = carry;
-            else if (t < 64)
+            else if (t < 2 * KR)
                 TK[t] = 0.0;
         }
         if (t == 0) {
@@ -883,12 +918,13 @@ void launch_xs_v(s2b_context* ctx, const TermArgs& a, const int* seg, double* Yg
     ctx->k_stream = reinterpret_cast<const void*>(kern);
 }
 
-template <int V, bool NZ>
+template <int V, bool NZ, bool H>
 void launch_xs2_v(s2b_context* ctx, const TermArgs& a, const Term2Args& b, const int* seg, double* Yg, int4* meta4,
                   size_t live_max) {
     constexpr Variant v = kVariants[V];
-    using L = Xs2Layout<v.rx, v.rv, v.mask, v.bm>;
+    using L = Xs2Layout<v.rx, v.rv, v.mask, v.bm, H>;
     static_assert(L::YW == XsV<V>::L::YW, "one Y layout for both kernels");
+    static_assert(L::bytes() <= 227 * 1024, "shared memory");
     const int nx = a.op.nx, nv = a.op.nv;
     const size_t M = live_max;
     launch_xs_fold<V>(ctx, a, seg, Yg, meta4, b.tpar, M);
@@ -896,14 +932,15 @@ void launch_xs2_v(s2b_context* ctx, const TermArgs& a, const Term2Args& b, const
     const double* tb[5] = {a.T0, a.T1, a.S0, a.S1, b.S2};
     for (int i = 0; i < 5; ++i) encode_xmaj(&maps.t[i], tb[i], M, nx, nv, L::TR, L::TX);
     for (int i = 0; i < 3; ++i) encode_xmaj(&maps.s[i], tb[2 + i], M, nx, nv, L::SR, L::SX);
-    auto kern = nv == 1024 ? term_xs2_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 1024> : term_xs2_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 0>;
+    auto kern = nv == 1024 ? term_xs2_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 1024, H>
+                           : term_xs2_kernel<v.rx, v.rv, v.mask, v.bm, NZ, 0, H>;
     const size_t smem = L::bytes();
     static int configured_device[2] = {-1, -1};
     if (configured_device[nv == 1024] != ctx->device) {
         S2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         configured_device[nv == 1024] = ctx->device;
     }
-    const int nrb = (nv + kX2Out - 1) / kX2Out, nxt = nx / kCW;
+    const int nrb = (nv + L::OUT - 1) / L::OUT, nxt = nx / kCW;
     const size_t work = M * static_cast<size_t>(nrb);
     const int grid = grid_cap(static_cast<int>(std::max<size_t>(1, std::min<size_t>(work, ctx->num_sms))));
     kern<<<grid, kXsNT, smem, ctx->stream>>>(maps, a, b, Yg, xs_yrows(nv), meta4, nrb, nxt);
@@ -923,13 +960,17 @@ bool term_xs2_enabled() {
 
 void launch_term_xs2(s2b_context* ctx, const s2b_operator* op, const TermArgs& a, const Term2Args& b, const int* seg,
                      double* Yg, int4* meta4, size_t M, bool nz) {
+    // 32-row items with the halo rows of t_k done by separate 2-point marches (default; cfg5
+    // 1.538e9 vs 1.472e9 windows/s for 28-row items with halo lanes, same run); S2B_XS2H=0: 28-row
+    const char* he = std::getenv("S2B_XS2H");
+    const bool h = !(he && he[0] == '0');
     switch (op->variant * 2 + (nz ? 1 : 0)) {
-    case 14: launch_xs2_v<7, false>(ctx, a, b, seg, Yg, meta4, M); break;
-    case 15: launch_xs2_v<7, true>(ctx, a, b, seg, Yg, meta4, M); break;
-    case 16: launch_xs2_v<8, false>(ctx, a, b, seg, Yg, meta4, M); break;
-    case 17: launch_xs2_v<8, true>(ctx, a, b, seg, Yg, meta4, M); break;
-    case 18: launch_xs2_v<9, false>(ctx, a, b, seg, Yg, meta4, M); break;
-    case 19: launch_xs2_v<9, true>(ctx, a, b, seg, Yg, meta4, M); break;
+    case 14: (h ? launch_xs2_v<7, false, true> : launch_xs2_v<7, false, false>)(ctx, a, b, seg, Yg, meta4, M); break;
+    case 15: (h ? launch_xs2_v<7, true, true> : launch_xs2_v<7, true, false>)(ctx, a, b, seg, Yg, meta4, M); break;
+    case 16: (h ? launch_xs2_v<8, false, true> : launch_xs2_v<8, false, false>)(ctx, a, b, seg, Yg, meta4, M); break;
+    case 17: (h ? launch_xs2_v<8, true, true> : launch_xs2_v<8, true, false>)(ctx, a, b, seg, Yg, meta4, M); break;
+    case 18: (h ? launch_xs2_v<9, false, true> : launch_xs2_v<9, false, false>)(ctx, a, b, seg, Yg, meta4, M); break;
+    case 19: (h ? launch_xs2_v<9, true, true> : launch_xs2_v<9, true, false>)(ctx, a, b, seg, Yg, meta4, M); break;
     default: fail(S2B_ERR_RUNTIME, "x-major two-term engine: unsupported variant");
     }
 }

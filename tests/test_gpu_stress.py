@@ -43,8 +43,10 @@ CASES = {
     "term_xs-512": (lambda s, c: _magnus(s, c, 512, M=2), {"S2B_ENGINE": "stream", "S2B_XS2": "0"}),
     "term_tma-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {"S2B_XS": "0"}),
     "term_xs-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {"S2B_XS2": "0"}),
-    "term_xs2-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream", "S2B_XS2": "1"}),
-    "term_xs2-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {"S2B_XS2": "1"}),
+    "term_xs2-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream", "S2B_XS2H": "0"}),
+    "term_xs2-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {"S2B_XS2H": "0"}),
+    "term_xs2h-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream"}),
+    "term_xs2h-1024": (lambda s, c: _magnus(s, c, 1024, M=2, dt=0.0002), {}),
     "term2-256": (lambda s, c: _magnus(s, c, 256, M=3), {"S2B_ENGINE": "stream", "S2B_TERM2": "1"}),
     "term_var-256": (lambda s, c: _magnus(s, c, 256, "langevin-variable", M=5, dt=0.001), {}),
     "em_cluster_ip-64": (lambda s, c: _euler(s, c, 64, M=7), {}),

@@ -12,10 +12,11 @@ from test_gpu_parity import gpu_magnus
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["1", "2"], ids=["xs1", "xs2"])
+@pytest.fixture(params=["1", "2", "2h"], ids=["xs1", "xs2", "xs2h"])
 def terms(request, monkeypatch):
-    """terms per pass of the x-march engine"""
-    monkeypatch.setenv("S2B_XS2", "1" if request.param == "2" else "0")
+    """terms per pass of the x-march engine (2h: 32-row items, t_k's halo rows by 2-point marches)"""
+    monkeypatch.setenv("S2B_XS2", "0" if request.param == "1" else "1")
+    monkeypatch.setenv("S2B_XS2H", "1" if request.param == "2h" else "0")
     return request.param
 
 
@@ -60,6 +61,7 @@ def test_xs_equals_row_march_non_square(s2b, ctx, monkeypatch, terms, nx, nv, or
     got, st_xs, _ = _solve(s2b, ctx, g, order, phi, M, T, dt, 41, rec=[0.002, 0.004])
     monkeypatch.setenv("S2B_XS", "0")
     monkeypatch.setenv("S2B_XS2", "0")
+    monkeypatch.setenv("S2B_XS2H", "0")
     want, st_tma, _ = _solve(s2b, ctx, g, order, phi, M, T, dt, 41, rec=[0.002, 0.004])
     assert len(got) == len(want) == 3
     for w, e in zip(want, got):
@@ -133,10 +135,13 @@ def test_xs_kernel_is_the_one_launched(s2b, ctx, monkeypatch):
     assert "term_tma_kernel" in ctx.kernel_names().get("stream", "")
 
 
-def test_xs2_kernel_is_the_one_launched_1024(ref, s2b, ctx, monkeypatch):
-    """cfg5's grid with two terms per pass: term_xs2_kernel runs and the result is the
-    reference's, bit for bit (records included)."""
+@pytest.mark.parametrize("halo", ["0", "1"])
+def test_xs2_kernel_is_the_one_launched_1024(ref, s2b, ctx, monkeypatch, halo):
+    """cfg5's grid with two terms per pass (28-row items, or 32-row items with separate halo
+    marches): term_xs2_kernel runs and the result is the reference's, bit for bit (records
+    included)."""
     monkeypatch.setenv("S2B_XS2", "1")
+    monkeypatch.setenv("S2B_XS2H", halo)
     d, T, dt, dt_leb, M, seed = 1024, 4e-4, 2e-4, 1e-5, 2, 1027
     ops = ref.Ops("langevin-constant", d, order=3)
     values, _ = ref.simulate_brownian(T, dt_leb, M, seed)
