@@ -383,14 +383,18 @@ __global__ void __launch_bounds__(kXsNT, 1)
 // term2_kernel's buffer protocol, so stream_loop2 / control2_kernel / normalize2 drive it
 // unchanged: T[tpar] -> T[tpar^1] (t_{k+1}); S[sidx] -> S[(sidx+1)%3] (s_{k+1}), S[(sidx+2)%3]
 // (s_k); maxima of term k in tn/sn, of term k+1 in tn2/sn2.
-// Work item (path, 28-row block [v0, v0+28)); lane r is row v0-2+r in both phases:
-//  * phase 1: t_k on 32 rows (2 halo rows on each side, recomputed by the neighbouring items;
-//    rows outside the grid are zero) over tile columns [jW+2, jW+W+2), into the shared t_k
-//    buffer TK whose first 4 columns [jW-2, jW+2) were computed by the previous tile (the x-march
-//    runs ahead by 2 columns; tile 0 computes columns 0, 1 itself and zeroes -2, -1).  Lanes
-//    2..29 also form s_k = s_{k-1} + t_k and write it.
-//  * phase 2: t_{k+1} = (Y t_k) / (s (k+1)) on lanes 2..29 over [jW, jW+W), s_{k+1} =
-//    (s_{k-1} + t_k) + t_{k+1} -- the same operations on the same operands as two single passes.
+// Work item (path, block of output rows starting at v0); two item shapes (Xs2Layout::H):
+//  * H (default): 32-row blocks, lane r is row v0+r in both phases.  Phase 1: t_k on the 32
+//    rows over tile columns [jW+2, jW+W+2), then t_k's 2 halo rows on each side (recomputed by
+//    the neighbouring items) by a 2-point march per lane; all of it into the shared t_k buffer TK
+//    whose first 4 columns [jW-2, jW+2) were computed by the previous tile (the x-march runs
+//    ahead by 2 columns; tile 0 computes columns 0, 1 itself and zeroes -2, -1); every lane also
+//    forms s_k = s_{k-1} + t_k and writes it.  Phase 2: t_{k+1} = (Y t_k) / (s (k+1)) over
+//    [jW, jW+W) and s_{k+1} = (s_{k-1} + t_k) + t_{k+1} -- the same operations on the same
+//    operands as two single passes.
+//  * !H (S2B_XS2H=0): 28-row blocks, lane r is row v0-2+r; lanes 0, 1, 30, 31 compute the halo
+//    rows of t_k in phase 1 and idle in phase 2.
+// Rows and columns outside the grid are zero in TK.
 constexpr int kX2Out = 28; // output rows per item
 constexpr int kX2Stages = 2;
 
